@@ -1,0 +1,278 @@
+/*
+ * sesgd_oracle.c -- TEST INFRASTRUCTURE: the plain, slow CPU oracle for the
+ * Shuffle-Exchange SGD hot path.  See sesgd_oracle.h for the contract.
+ *
+ * Built with gcc -O2 -ffp-contract=off (no -ffast-math), so every float
+ * expression below is a sequence of single IEEE-754 binary32 (or binary64)
+ * round-to-nearest operations in exactly the order written (R10).
+ *
+ * Follows Algorithm 1 in its own order, per iteration t:
+ *   lines 3-8   local step     xh_i = x_i - eta * (momentum-smoothed gradient)  (R8, R11)
+ *   lines 9-10  new groups     G_t = generate_groups(sigma, t)                  (R1-R6)
+ *   line 11     x_{i,t+1} = Ring-AllReduce(xh_i; G_{i,t}) = group mean          (Eq. 6, R7)
+ * The Eq. 5 ("gradient") variant is ORC_MODE_GRAD (R9).
+ *
+ * Parity status of every function: pinned by tests/test_oracle_pins.py (see
+ * DESIGN.md "Oracle pins"); nothing here is "parity unpinned" except agreement
+ * with the paper's own (unpublished) PRNG and runs, which no test can reach.
+ */
+#include "sesgd_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../synth/synth_gen.h"
+
+/* ---- R2: splitmix64, exactly as S:61 (SPEC core.rng_next) ---- */
+uint64_t orc_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t orc_splitmix64_next(uint64_t *state) {
+  *state += 0x9E3779B97F4A7C15ULL;
+  return orc_mix(*state);
+}
+
+/* ---- R5: rejection-bounded draw (S:71 with the 2^64 overflow resolved) ---- */
+uint64_t orc_bounded(uint64_t *state, uint64_t bound, int *err) {
+  if (bound == 0) {
+    if (err) *err = 1;
+    return 0;
+  }
+  if (err) *err = 0;
+  /* floor(2^64/bound)*bound = 2^64 - (2^64 mod bound); 2^64 mod bound = (0 - bound) % bound */
+  uint64_t rem = (0 - bound) % bound;
+  for (;;) {
+    uint64_t w = orc_splitmix64_next(state);
+    if (rem == 0 || w < (uint64_t)0 - rem) return w % bound;
+  }
+}
+
+/* ---- A1: shuffle-exchange groups (R1, R3, R4, R6) ---- */
+static int cmp_i32(const void *a, const void *b) {
+  int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+  return (x > y) - (x < y);
+}
+
+int orc_groups(uint64_t seed, int64_t t, int32_t n, int32_t m, int32_t *raw, int32_t *canon,
+               int32_t *group_of) {
+  if (n < 1 || m < 1 || m > n || t < 0) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  int32_t k = n / m;
+  int32_t *p = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t *groups = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)k);
+  /* "Initialize the pseudo-random algorithm with sigma" (Alg.1 line 1); per-iteration
+   * seed s_t = mix(sigma XOR t) gives random access in t (R3). */
+  uint64_t state = orc_mix(seed ^ (uint64_t)t);
+  for (int32_t i = 0; i < n; ++i) p[i] = i;
+  /* R4: Durstenfeld Fisher-Yates, descending i */
+  for (int32_t i = n - 1; i >= 1; --i) {
+    int32_t j = (int32_t)orc_bounded(&state, (uint64_t)(i + 1), NULL);
+    int32_t tmp = p[i];
+    p[i] = p[j];
+    p[j] = tmp;
+  }
+  if (raw) memcpy(raw, p, sizeof(int32_t) * (size_t)n);
+  /* R6: group j = slots [j*m, (j+1)*m), sorted ascending; groups ordered by smallest member */
+  memcpy(groups, p, sizeof(int32_t) * (size_t)n);
+  for (int32_t j = 0; j < k; ++j) qsort(groups + (size_t)j * m, (size_t)m, sizeof(int32_t), cmp_i32);
+  for (int32_t j = 0; j < k; ++j) order[j] = j;
+  for (int32_t a = 1; a < k; ++a) { /* insertion sort of group indices by first member */
+    int32_t cur = order[a], b = a - 1;
+    while (b >= 0 && groups[(size_t)order[b] * m] > groups[(size_t)cur * m]) {
+      order[b + 1] = order[b];
+      --b;
+    }
+    order[b + 1] = cur;
+  }
+  for (int32_t j = 0; j < k; ++j) {
+    const int32_t *src = groups + (size_t)order[j] * m;
+    for (int32_t r = 0; r < m; ++r) {
+      if (canon) canon[(size_t)j * m + r] = src[r];
+      if (group_of) group_of[src[r]] = j;
+    }
+  }
+  free(p);
+  free(groups);
+  free(order);
+  return ORC_OK;
+}
+
+/* ---- A6/A7: Eq. 2 and Eq. 3 exact forms ---- */
+int orc_latency(int32_t n, int32_t m, double bytes, double nu, double tau, double out[5]) {
+  if (n < 1 || m < 1 || m > n) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  if (!(nu > 0.0) || !(tau >= 0.0) || !(bytes >= 0.0) || !out) return ORC_EINVAL;
+  /* T = 2(n-1) * (G/(n nu) + t_tau)   -- Eq. 2 with the ring over n workers */
+  double ring_hs = 2.0 * (double)(n - 1);
+  double ring_s = ring_hs * (bytes / ((double)n * nu) + tau);
+  /* SESGD: the same ring inside a group of m = n/k workers (Eq. 3 before the approximation) */
+  double se_hs = 2.0 * (double)(m - 1);
+  double se_s = se_hs * (bytes / ((double)m * nu) + tau);
+  out[0] = ring_hs;
+  out[1] = se_hs;
+  out[2] = ring_s;
+  out[3] = se_s;
+  if (se_s == 0.0)
+    out[4] = (ring_s == 0.0) ? 1.0 : INFINITY;
+  else
+    out[4] = ring_s / se_s;
+  return ORC_OK;
+}
+
+/* ---- A2/A5 (Eq. 6) and Eq. 5 variant: one iteration, binary32 ---- */
+int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                 const float *g, float lr, float mu, int32_t mode) {
+  if (n < 1 || m < 1 || m > n || L < 0 || !canon) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  int32_t k = n / m;
+  const float fm = (float)m;
+  if (mode == ORC_MODE_PARAM) {
+    float *xh = (float *)malloc(sizeof(float) * (size_t)n * (size_t)(L > 0 ? L : 1));
+    /* Alg.1 lines 3-8 on every worker: v_i <- mu v_i + g_i ; xh_i <- x_i - eta v_i (R8) */
+    for (int32_t i = 0; i < n; ++i) {
+      for (int64_t e = 0; e < L; ++e) {
+        size_t at = (size_t)i * (size_t)L + (size_t)e;
+        float mv = mu * v[at];
+        float vn = mv + g[at];
+        float step = lr * vn;
+        v[at] = vn;
+        xh[at] = x[at] - step;
+      }
+    }
+    /* Alg.1 line 11 / Eq. 6: x_i <- (k/n) sum_{j in g(i,t)} xh_j = group mean (R7);
+     * left fold in ascending member id, one division by m (R10) */
+    for (int32_t j = 0; j < k; ++j) {
+      const int32_t *G = canon + (size_t)j * m;
+      for (int64_t e = 0; e < L; ++e) {
+        float s = xh[(size_t)G[0] * (size_t)L + (size_t)e];
+        for (int32_t r = 1; r < m; ++r) s = s + xh[(size_t)G[r] * (size_t)L + (size_t)e];
+        float mean = s / fm;
+        for (int32_t r = 0; r < m; ++r) x[(size_t)G[r] * (size_t)L + (size_t)e] = mean;
+      }
+    }
+    free(xh);
+  } else if (mode == ORC_MODE_GRAD) {
+    /* Eq. 5 variant: gb_G = group mean of g ; v_i <- mu v_i + gb ; x_i <- x_i - eta v_i */
+    for (int32_t j = 0; j < k; ++j) {
+      const int32_t *G = canon + (size_t)j * m;
+      for (int64_t e = 0; e < L; ++e) {
+        float s = g[(size_t)G[0] * (size_t)L + (size_t)e];
+        for (int32_t r = 1; r < m; ++r) s = s + g[(size_t)G[r] * (size_t)L + (size_t)e];
+        float gb = s / fm;
+        for (int32_t r = 0; r < m; ++r) {
+          size_t at = (size_t)G[r] * (size_t)L + (size_t)e;
+          float mv = mu * v[at];
+          float vn = mv + gb;
+          float step = lr * vn;
+          v[at] = vn;
+          x[at] = x[at] - step;
+        }
+      }
+    }
+  } else {
+    return ORC_EINVAL;
+  }
+  return ORC_OK;
+}
+
+/* ---- the same, binary64 (for invariants / closed forms; not the GPU gate) ---- */
+int orc_step_f64(int32_t n, int32_t m, const int32_t *canon, int64_t L, double *x, double *v,
+                 const double *g, double lr, double mu, int32_t mode) {
+  if (n < 1 || m < 1 || m > n || L < 0 || !canon) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  int32_t k = n / m;
+  const double dm = (double)m;
+  if (mode == ORC_MODE_PARAM) {
+    double *xh = (double *)malloc(sizeof(double) * (size_t)n * (size_t)(L > 0 ? L : 1));
+    for (int32_t i = 0; i < n; ++i) {
+      for (int64_t e = 0; e < L; ++e) {
+        size_t at = (size_t)i * (size_t)L + (size_t)e;
+        double mv = mu * v[at];
+        double vn = mv + g[at];
+        double step = lr * vn;
+        v[at] = vn;
+        xh[at] = x[at] - step;
+      }
+    }
+    for (int32_t j = 0; j < k; ++j) {
+      const int32_t *G = canon + (size_t)j * m;
+      for (int64_t e = 0; e < L; ++e) {
+        double s = xh[(size_t)G[0] * (size_t)L + (size_t)e];
+        for (int32_t r = 1; r < m; ++r) s = s + xh[(size_t)G[r] * (size_t)L + (size_t)e];
+        double mean = s / dm;
+        for (int32_t r = 0; r < m; ++r) x[(size_t)G[r] * (size_t)L + (size_t)e] = mean;
+      }
+    }
+    free(xh);
+  } else if (mode == ORC_MODE_GRAD) {
+    for (int32_t j = 0; j < k; ++j) {
+      const int32_t *G = canon + (size_t)j * m;
+      for (int64_t e = 0; e < L; ++e) {
+        double s = g[(size_t)G[0] * (size_t)L + (size_t)e];
+        for (int32_t r = 1; r < m; ++r) s = s + g[(size_t)G[r] * (size_t)L + (size_t)e];
+        double gb = s / dm;
+        for (int32_t r = 0; r < m; ++r) {
+          size_t at = (size_t)G[r] * (size_t)L + (size_t)e;
+          double mv = mu * v[at];
+          double vn = mv + gb;
+          double step = lr * vn;
+          v[at] = vn;
+          x[at] = x[at] - step;
+        }
+      }
+    }
+  } else {
+    return ORC_EINVAL;
+  }
+  return ORC_OK;
+}
+
+/* ---- T iterations with synthetic gradients at chosen coordinates ---- */
+int orc_run_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
+                const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode, float *x,
+                float *v) {
+  if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || S < 0) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  float *g = (float *)malloc(sizeof(float) * (size_t)n * (size_t)(S > 0 ? S : 1));
+  int32_t *canon = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int rc = ORC_OK;
+  for (int64_t t = t0; t < t0 + T && rc == ORC_OK; ++t) {
+    for (int32_t i = 0; i < n; ++i) { /* Alg.1 lines 4-6: worker i's gradient (synthetic) */
+      uint64_t key = synth_grad_key(s_g, i, t);
+      for (int64_t e = 0; e < S; ++e)
+        g[(size_t)i * (size_t)S + (size_t)e] = synth_grad(key, coords ? coords[e] : e);
+    }
+    rc = orc_groups(seed, t, n, m, NULL, canon, NULL); /* Alg.1 lines 9-10 */
+    if (rc == ORC_OK) rc = orc_step_f32(n, m, canon, S, x, v, g, lr, mu, mode);
+  }
+  free(g);
+  free(canon);
+  return rc;
+}
+
+int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
+                const int64_t *coords, uint64_t s_g, double lr, double mu, int32_t mode, double *x,
+                double *v) {
+  if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || S < 0) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  double *g = (double *)malloc(sizeof(double) * (size_t)n * (size_t)(S > 0 ? S : 1));
+  int32_t *canon = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int rc = ORC_OK;
+  for (int64_t t = t0; t < t0 + T && rc == ORC_OK; ++t) {
+    for (int32_t i = 0; i < n; ++i) {
+      uint64_t key = synth_grad_key(s_g, i, t);
+      for (int64_t e = 0; e < S; ++e)
+        g[(size_t)i * (size_t)S + (size_t)e] = (double)synth_grad(key, coords ? coords[e] : e);
+    }
+    rc = orc_groups(seed, t, n, m, NULL, canon, NULL);
+    if (rc == ORC_OK) rc = orc_step_f64(n, m, canon, S, x, v, g, lr, mu, mode);
+  }
+  free(g);
+  free(canon);
+  return rc;
+}
