@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the SESGD group sync+update hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sesgd|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): n = 8 workers, group_size = 2, ResNet-50 DDP
+buckets (5 buckets, 25,557,032 fp32 per worker), PARAM mode (Eq. 6), lr 0.1,
+momentum 0.9.  N=1: all 8 workers resident on one B200 (kernel K6).  N>1: 8/N
+workers per GPU, groups exchange over NVLink P2P (kernel K3); the total work is
+fixed ("scaling": "strong").  One step = one SESGD iteration over all buckets
+of all workers (every row of SURVEY.md Sec. 8(a): schedule, local step, group
+handshake + exchange + average, write-back).
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "group sync+update GB/s per GPU & iters/s at 1/2/4/8 B200 (fraction of roofline)"
+N_WORKERS, GROUP_SIZE, LR, MU, SEED = 8, 2, 0.1, 0.9, 42
+BYTES_PER_WORKER_ELEM = 20  # algorithmic HBM bytes: read g, v, x; write v, x (fp32)
+NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md), nominal 900
+PAPER_CONTEXT = {"speedup_16w_0.1ms": 1.7, "speedup_16w_5ms": 5.0,
+                 "source": "PAPER.md:7, P:411, P:436 (K80 + 1 Gbps Ethernet; end-to-end training, not this metric)"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="sesgd", choices=["sesgd", "reference"])
+    p.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16", "config1"])
+    p.add_argument("--n", type=int, default=N_WORKERS)
+    p.add_argument("--group-size", type=int, default=GROUP_SIZE)
+    p.add_argument("--mode", default="param", choices=["param", "grad"])
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(kernel: str, workload: str):
+    """dram bytes per launch from the committed ncu --set full summary (profiles/traffic.json)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    return d.get(f"{workload}/{kernel}")
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    _NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+              0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+              0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._NAMES.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def cpu_oracle_rate(n, m, budget_s, mode):
+    """Time the oracle as it stands (single-threaded C) on a bounded coordinate sample of the
+    same workload.  Returns (GB/s, sample description, seconds)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    omode = oracle.MODE_PARAM if mode == "param" else oracle.MODE_GRAD
+
+    def run(S, T, t0=0):
+        coords = np.arange(S, dtype=np.int64) * 7 % 25557032
+        x = np.tile(synth.x0_host(S, coords=coords), (n, 1))
+        v = np.zeros_like(x)
+        t = time.perf_counter()
+        oracle.run(n, m, SEED, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, t0=t0, coords=coords)
+        return time.perf_counter() - t
+
+    probe_S, probe_T = 20000, 2
+    dt = run(probe_S, probe_T)
+    rate = n * probe_S * probe_T / dt  # worker-elements / s
+    T = 4
+    S = int(max(1000, min(25557032, rate * budget_s / (n * T))))
+    dt = run(S, T)
+    gbs = BYTES_PER_WORKER_ELEM * n * S * T / dt / 1e9
+    sample = (f"n={n}, m={m}: {S} of 25,557,032 coordinates x {T} iterations "
+              f"({n * S * T:.3g} worker-elements, {dt:.1f} s, single-threaded C oracle, fp32-emulate)")
+    return gbs, sample, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+    n, m = args.n, args.group_size
+    omode = oracle.MODE_PARAM if args.mode == "param" else oracle.MODE_GRAD
+    # each step: one oracle iteration over a bounded coordinate sample of the workload
+    steps, warm = args.steps, args.warmup
+    per_step_budget = max(0.02, min(1.0, 120.0 / max(1, steps + warm)))
+    S0 = 20000
+    coords = np.arange(S0, dtype=np.int64)
+    x = np.tile(synth.x0_host(S0, coords=coords), (n, 1))
+    v = np.zeros_like(x)
+    t = time.perf_counter()
+    oracle.run(n, m, SEED, 1, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, coords=coords)
+    rate = n * S0 / (time.perf_counter() - t)
+    S = int(max(1000, min(25557032, rate * per_step_budget / n)))
+    coords = np.arange(S, dtype=np.int64)
+    x = np.tile(synth.x0_host(S, coords=coords), (n, 1))
+    v = np.zeros_like(x)
+    for t in range(warm):
+        oracle.run(n, m, SEED, 1, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, t0=t, coords=coords)
+    t0 = time.perf_counter()
+    for t in range(warm, warm + steps):
+        oracle.run(n, m, SEED, 1, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, t0=t, coords=coords)
+    dt = time.perf_counter() - t0
+    gbs = BYTES_PER_WORKER_ELEM * n * S * steps / dt / 1e9
+    sample = f"n={n}, m={m}: {S} of 25,557,032 coordinates per step, 1 iteration per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"cfg2 sample: {sample}", "n": n, "group_size": m, "mode": args.mode},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_sesgd(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2007_00433_b200 import sesgd as C
+    from paper_2007_00433_b200.engine import SESGDEngine
+    from paper_2007_00433_b200.workloads import WORKLOADS
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    n, m = args.n, args.group_size
+    if n % world:
+        raise SystemExit("n must be a multiple of the GPU count")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    buckets = list(WORKLOADS[args.workload])
+    L = sum(buckets)
+    mode = C.MODE_PARAM_AVG if args.mode == "param" else C.MODE_GRAD_AVG
+    eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world)
+    r = eng.r
+    stream = torch.cuda.current_stream(dev)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    for s, w in enumerate(eng.local_workers):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), stream.cuda_stream)
+            synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), w, 0, stream.cuda_stream)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    nb = len(buckets)
+    t_next = 0
+    for _ in range(args.warmup):
+        eng.step(t_next, LR, MU, stream)
+        t_next += 1
+    eng.poll()
+    K = args.steps
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nb)]
+          for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for k in range(K):
+            eng.begin_iter(t_next)
+            for b in range(nb):
+                ev[k][b][0].record(stream)
+                eng.sync_step(b, LR, MU, stream)
+                ev[k][b][1].record(stream)
+            t_next += 1
+        end.record(stream)
+        barrier()
+    eng.poll()
+    ms_total = max_over_ranks(start.elapsed_time(end))
+    ms_step = ms_total / K
+    launch_ms = [[ev[k][b][0].elapsed_time(ev[k][b][1]) for b in range(nb)] for k in range(K)]
+    kern_ms_total = max_over_ranks(sum(map(sum, launch_ms)))
+    total_bytes = BYTES_PER_WORKER_ELEM * L * n  # whole job, per step
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+    per_gpu = value / world
+    # dominant kernel roofline (all timed launches are the one fused kernel)
+    hbm_peak, peak_src = measured_peaks()
+    algo_bytes_per_step_gpu = BYTES_PER_WORKER_ELEM * L * r
+    if world == 1:
+        kernel = "k6_resident"
+        achieved = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "peak_source": peak_src,
+                "algo_bytes_per_launch": [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets],
+                "kernel": kernel}
+    else:
+        kernel = "k3_oneshot"
+        # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction
+        s_span = min(m, world)  # groups of m workers, 1 per GPU when r == 1
+        nvl_bytes = 2 * (s_span - 1) / s_span * 4 * L * r if s_span > 1 else 0.0
+        achieved_nvl = nvl_bytes * K / (kern_ms_total * 1e-3) / 1e9
+        achieved_hbm = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
+        t_hbm = algo_bytes_per_step_gpu / (hbm_peak * 1e9)
+        t_nvl = nvl_bytes / (NVLINK_PEER_GBS * 1e9)
+        if t_nvl >= t_hbm:
+            roof = {"bound": "nvlink", "achieved": achieved_nvl, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                    "frac": achieved_nvl / NVLINK_PEER_GBS,
+                    "peak_source": "measured peer copy per direction, B200_PROFILING.md (nominal 900)"}
+        else:
+            roof = {"bound": "hbm", "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved_hbm / hbm_peak, "peak_source": peak_src}
+        roof.update({"hbm_achieved": achieved_hbm, "nvlink_algo_bytes_per_step": nvl_bytes,
+                     "t_roof_us": max(t_hbm, t_nvl) * 1e6, "kernel": kernel})
+    roof["traffic"] = traffic_for(kernel, f"{args.workload}_n{n}_m{m}_g{world}")
+
+    # ---- e2e through the C-ABI host-buffer call (H2D of g, D2H of x inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        g_host = [[torch.empty(Lb, dtype=torch.float32).pin_memory() for _ in range(r)] for Lb in buckets]
+        x_host = [[torch.empty(Lb, dtype=torch.float32).pin_memory() for _ in range(r)] for Lb in buckets]
+        for b in range(nb):
+            for s in range(r):
+                g_host[b][s].copy_(eng.g(s, b))
+        eng.step_host(t_next, LR, MU, g_host, x_host, stream)
+        t_next += 1
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            eng.step_host(t_next, LR, MU, g_host, x_host, stream)
+            t_next += 1
+        e1.record(stream)
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.e2e_steps
+        e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * L * n, "d2h_bytes_per_step": 4 * L * n,
+               "ms_per_step": e2e_ms, "steps": args.e2e_steps,
+               "api": "sesgd_sync_step_host (pinned host g in, updated x out, every worker)"}
+    eng.poll()
+
+    stats = [eng.stats(b) for b in range(nb)]
+    lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, 1.5e-6)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gbs, sample, _ = cpu_oracle_rate(n, m, args.cpu_seconds, args.mode)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample}
+    clocks = clk.summary()
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": (f"cfg2: n={n} workers, group_size={m}, {args.workload} DDP buckets "
+                             f"({nb} buckets, {L:,} fp32 per worker), {args.mode.upper()} mode, "
+                             f"lr {LR}, momentum {MU}; {r} worker(s) resident per GPU"),
+                "n": n, "group_size": m, "workers_per_gpu": r,
+                "path": "resident (K6)" if world == 1 else "one-shot NVLink P2P (K3)",
+                "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush",
+                "parallelism": f"sesgd groups over {world} GPU(s)",
+            },
+            "iters_per_s": 1e3 / ms_step,
+            "gbs_per_gpu": per_gpu,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": K * nb,
+            "clocks": clocks,
+            "handshakes": {
+                "sesgd_per_tensor": lat["sesgd_handshakes"], "ring_per_tensor": lat["ring_handshakes"],
+                "kernel_rounds_per_bucket": stats[0]["handshake_rounds"],
+                "model": "Eq.2/Eq.3 exact (sesgd_latency_model), nu=770 GB/s, tau=1.5 us (assumed until K7 probe)",
+                "model_ratio": lat["ratio"],
+            },
+            "paper_context": PAPER_CONTEXT,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_sesgd(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,190 @@
+/*
+ * sesgd.h -- C ABI of libsesgd.so, the B200-native hot path of Shuffle-Exchange
+ * SGD (SESGD, arXiv 2007.00433).
+ *
+ * Citations: P:n = the paper's PAPER.md line n, S:n = SPEC.md line n; R1..R17 are
+ * the readings of the paper listed in DESIGN.md ("Readings").
+ *
+ * What one iteration computes (Algorithm 1; Eq. 6):
+ *   for every worker i (R8: local momentum, never communicated, v <- mu v + g):
+ *     v_i   <- mu (x) v_i (+) g_i
+ *     xh_i  <- x_i (-) lr (x) v_i                               (Alg.1 lines 3-8)
+ *   G_t = shuffle-exchange partition of the n workers into n/m groups  (lines 9-10)
+ *   x_i  <- (xh_{a0} (+) xh_{a1} (+) ... (+) xh_{a(m-1)}) (/) m  (line 11, R7, R10)
+ * with (x)(+)(-)(/) single binary32 round-to-nearest operations (no FMA
+ * contraction), a0 < a1 < ... the members of i's group.  SESGD_MODE_GRAD_AVG is
+ * the Eq. 5 variant: gbar = fold(g)/m ; v <- mu v + gbar ; x <- x - lr v.
+ *
+ * Memory: every parameter / momentum / gradient buffer is CALLER-OWNED device
+ * memory (fp32, contiguous); the library never frees it.  Multi-GPU peer
+ * workspaces are caller-owned peer-mapped device memory (e.g. from
+ * torch.distributed._symmetric_memory).  The library owns only the context and
+ * small device tables it allocates itself (freed by sesgd_destroy).
+ *
+ * Threading: a context is not thread-safe; use one per process (per device).
+ * Errors: every int-returning call returns SESGD_OK (0) or a negative code;
+ * sesgd_last_error(ctx) gives a human-readable reason for the last failure.
+ */
+#ifndef SESGD_H
+#define SESGD_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SESGD_API __attribute__((visibility("default")))
+#else
+#define SESGD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---- */
+#define SESGD_OK 0
+#define SESGD_EINVAL (-1)   /* bad argument (range, NULL, size mismatch) */
+#define SESGD_ENOTDIV (-2)  /* group_size does not divide n (R13) */
+#define SESGD_ESTATE (-3)   /* call out of order / layout mismatch across ranks */
+#define SESGD_ECUDA (-4)    /* CUDA runtime error; see sesgd_last_error */
+#define SESGD_ETIMEOUT (-5) /* a group peer did not signal within the timeout */
+#define SESGD_ENOMEM (-6)   /* host or device allocation failed */
+#define SESGD_ENOTSUP (-7)  /* configuration not supported by this build */
+
+/* ---- compile-time limits ---- */
+#define SESGD_MAX_WORKERS 64 /* n */
+#define SESGD_MAX_RANKS 8    /* GPUs in one job (one NVLink/NVSwitch domain) */
+
+/* ---- modes (R9) ---- */
+#define SESGD_MODE_PARAM_AVG 0 /* Eq. 6: average locally-stepped parameters (default) */
+#define SESGD_MODE_GRAD_AVG 1  /* Eq. 5 variant: average gradients, then local update */
+
+/* ---- data paths for the intra-group exchange ---- */
+#define SESGD_PATH_AUTO 0     /* resident if all workers are local, else one-shot */
+#define SESGD_PATH_RESIDENT 1 /* all n workers on this GPU (1-GPU "k resident replicas") */
+#define SESGD_PATH_ONESHOT 2  /* NVLink P2P: every member pulls its m-1 peers' chunks */
+
+/* ---- options for sesgd_set_option ---- */
+#define SESGD_OPT_MODE 1       /* SESGD_MODE_*                                   (default 0) */
+#define SESGD_OPT_PATH 2       /* SESGD_PATH_*                                   (default 0) */
+#define SESGD_OPT_TIMEOUT_MS 3 /* flag-wait timeout before SESGD_ETIMEOUT        (default 20000) */
+#define SESGD_OPT_GRID 4       /* CTAs per launch, 0 = auto (SM count x occupancy) */
+#define SESGD_OPT_HOP_DELAY_NS 5 /* injected delay before every flag store (latency sweep) */
+
+/* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
+typedef struct sesgd_cost {
+  double ring_handshakes;  /* 2(n-1)                       per tensor, Ring-AllReduce over n */
+  double sesgd_handshakes; /* 2(m-1)                       per tensor, ring inside a group  */
+  double ring_s;           /* 2(n-1) (G/(n nu) + tau)       seconds                          */
+  double sesgd_s;          /* 2(m-1) (G/(m nu) + tau)       seconds                          */
+  double ratio;            /* ring_s / sesgd_s (1 if both 0, +inf if only sesgd_s is 0)      */
+} sesgd_cost;
+
+/* Per-bucket counters (host-side, exact: the schedule is deterministic). */
+typedef struct sesgd_stats {
+  int64_t sync_calls;        /* sesgd_sync_step calls on this bucket                        */
+  int64_t kernel_launches;   /* kernels this library launched for the bucket                */
+  int64_t handshake_rounds;  /* flag rounds per call on the critical path (0 resident, 1 one-shot) */
+  int64_t flag_messages;     /* cross-GPU flag stores issued by this process, cumulative    */
+  int64_t payload_bytes_in;  /* bytes this process pulled from other GPUs, cumulative       */
+  int64_t hbm_algo_bytes;    /* algorithmic HBM bytes (20 B per worker-element), cumulative */
+} sesgd_stats;
+
+typedef struct sesgd_ctx sesgd_ctx;
+
+/* Create a context for n workers in groups of m = group_size (k = n/m groups).
+ * Host only: no GPU work, no communication.
+ * Errors: SESGD_EINVAL (n < 1, n > SESGD_MAX_WORKERS, group_size < 1, group_size > n,
+ *         out == NULL); SESGD_ENOTDIV (n % group_size != 0); SESGD_ENOMEM. */
+SESGD_API int sesgd_init(int32_t n, int32_t group_size, uint64_t seed, sesgd_ctx **out);
+
+/* Free the context and the library-owned device tables. NULL is a no-op. */
+SESGD_API void sesgd_destroy(sesgd_ctx *ctx);
+
+/* The shuffle-exchange partition of iteration `iter` (A1; Alg.1 lines 1, 9-10;
+ * readings R1-R6).  Pure function of (seed, iter, n, m): random access in iter.
+ * perm_out[n] (required): canonical order -- group j is perm_out[j*m .. j*m+m-1],
+ *   members ascending, groups ordered by smallest member.
+ * group_of_out[n] (may be NULL): group index of each worker in that order.
+ * Caller owns both buffers.  Errors: SESGD_EINVAL (ctx/perm_out NULL, iter < 0). */
+SESGD_API int sesgd_groups(const sesgd_ctx *ctx, int64_t iter, int32_t *perm_out, int32_t *group_of_out);
+
+/* Latency-model query (A6/A7).  Pure, host only.
+ * bytes = G (message bytes per tensor), nu_Bps = bandwidth (B/s), tau_s = per-hop latency.
+ * Errors: SESGD_EINVAL (n < 1, group_size < 1 or > n, nu_Bps <= 0, tau_s < 0, bytes < 0,
+ *         out NULL); SESGD_ENOTDIV (n % group_size != 0). */
+SESGD_API int sesgd_latency_model(int32_t n, int32_t group_size, double bytes, double nu_Bps, double tau_s,
+                        sesgd_cost *out);
+
+/* Set an option (SESGD_OPT_*).  Errors: SESGD_EINVAL (unknown option / bad value). */
+SESGD_API int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value);
+
+/* Bind this process to CUDA `device` and the global worker ids it hosts
+ * (local_workers[n_local], distinct, in [0, n)).  1 GPU: n_local = n (all resident).
+ * Must precede sesgd_register_bucket.  Errors: SESGD_EINVAL (duplicates, out of range,
+ * n_local < 1), SESGD_ESTATE (already attached), SESGD_ECUDA. */
+SESGD_API int sesgd_attach(sesgd_ctx *ctx, int32_t device, int32_t n_local, const int32_t *local_workers);
+
+/* Register bucket `bucket` (0 <= bucket < 4096, ids dense from 0) of `numel` fp32 elements.
+ * x[n_local], v[n_local], g[n_local]: device pointers of each local worker (in the order given
+ * to sesgd_attach), each to numel contiguous floats; 16-byte aligned pointers take the
+ * 128-bit vector path, others a scalar path.  Every worker must register the same
+ * (bucket, numel) list (checked at sesgd_attach_peers on multi-GPU).
+ * Re-registering an id replaces its pointers (numel must not change after attach_peers).
+ * Errors: SESGD_EINVAL (NULL pointers, numel < 0, bad id), SESGD_ESTATE (not attached),
+ *         SESGD_ECUDA / SESGD_ENOMEM (device table allocation). */
+SESGD_API int sesgd_register_bucket(sesgd_ctx *ctx, int32_t bucket, int64_t numel, float *const *x,
+                          float *const *v, const float *const *g);
+
+/* Multi-GPU only.  Bytes of peer-visible workspace each rank must provide for the
+ * registered buckets (stage double buffer + flag words).  Errors: SESGD_ESTATE. */
+SESGD_API int sesgd_workspace_bytes(const sesgd_ctx *ctx, int64_t *bytes_out);
+
+/* Multi-GPU only.  Zero this rank's workspace `local_ws` (device pointer of
+ * sesgd_workspace_bytes bytes) and write its layout header.  Synchronous.
+ * Call on every rank, then barrier, then sesgd_attach_peers. */
+SESGD_API int sesgd_workspace_prepare(sesgd_ctx *ctx, void *local_ws);
+
+/* Multi-GPU only.  rank_ws[n_ranks]: every rank's workspace, mapped into this process
+ * (rank_ws[rank] == local_ws).  worker_rank[n]: the rank hosting each worker.  Reads the
+ * peers' headers (P2P) and returns SESGD_ESTATE if any rank registered different buckets.
+ * Errors: SESGD_EINVAL, SESGD_ESTATE, SESGD_ECUDA. */
+SESGD_API int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, void *const *rank_ws,
+                       const int32_t *worker_rank);
+
+/* Set the current iteration t (any t >= 0: random access / resume).  Computes the
+ * schedule of t (and of t-2, for the stage-reuse guard) on the host.
+ * Errors: SESGD_EINVAL (iter < 0), SESGD_ESTATE (not attached). */
+SESGD_API int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter);
+
+/* The hot path: one SESGD sync+update of bucket `bucket` at the current iteration for all
+ * local workers.  ASYNCHRONOUS: validates, enqueues the fused kernel on `stream`
+ * (a cudaStream_t; NULL = legacy default stream) and returns.  On multi-GPU every rank must
+ * issue the same (iteration, bucket) sequence.  Device-side failures (peer timeout) are
+ * latched and returned by the next call or by sesgd_poll as SESGD_ETIMEOUT.
+ * Errors: SESGD_EINVAL (unregistered bucket, lr/momentum not finite), SESGD_ESTATE
+ *         (begin_iter not called, peers not attached on multi-GPU), SESGD_ECUDA, SESGD_ETIMEOUT. */
+SESGD_API int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, void *stream);
+
+/* End-to-end variant through HOST buffers: for each local worker, copies g_host[w] (numel
+ * floats, pinned for overlap) to the registered device gradient, runs sesgd_sync_step, and
+ * copies the updated device parameters back into x_host_out[w].  Asynchronous on `stream`
+ * like sesgd_sync_step; host buffers must stay valid until the stream is synchronised. */
+SESGD_API int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,
+                         const float *const *g_host, float *const *x_host_out, void *stream);
+
+/* Non-blocking check of the latched device error word: SESGD_OK or SESGD_ETIMEOUT. */
+SESGD_API int sesgd_poll(sesgd_ctx *ctx);
+
+/* Counters of bucket `bucket`.  Errors: SESGD_EINVAL. */
+SESGD_API int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats *out);
+
+/* Number of SMs and CTAs per launch the library uses on the attached device (0 before attach). */
+SESGD_API int sesgd_launch_grid(const sesgd_ctx *ctx, int32_t *ctas_out);
+
+SESGD_API const char *sesgd_strerror(int code);
+SESGD_API const char *sesgd_last_error(const sesgd_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SESGD_H */

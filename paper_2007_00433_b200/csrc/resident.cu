@@ -1,0 +1,241 @@
+// resident.cu -- K6: fused group sync + momentum-SGD update with all n workers
+// resident on one GPU (the 1-GPU configuration: "k simulated workers are resident
+// replicas", BASELINE north star).
+//
+// One launch covers one bucket for every group of the current iteration.  Each
+// CTA row blockIdx.y is one group G = {a_0 < ... < a_{m-1}} of the canonical
+// partition (A1); per element e it computes, entirely in registers
+//   PARAM (Eq. 6; Alg.1 lines 3-11):
+//     v_r = mu (x) v_r (+) g_r ; xh_r = x_r (-) lr (x) v_r      (R8, R11)
+//     x_r = (xh_0 (+) xh_1 (+) ... (+) xh_{m-1}) (/) m           (R7, R10)
+//   GRAD (Eq. 5 variant):
+//     gb = (g_0 (+) ... (+) g_{m-1}) (/) m ; v_r = mu v_r + gb ; x_r = x_r - lr v_r
+// so the HBM traffic is exactly the algorithmic 20 B per worker-element
+// (read g, v, x; write v, x -- DESIGN.md "Algorithmic bytes"): x_hat never leaves
+// registers.  Pure streaming: 128-bit coalesced loads/stores, several independent
+// 16-byte loads in flight per thread, grid = SMs x occupancy (persistent-style
+// grid-stride).  No tensor cores (nothing here is a contraction).
+#include "common.cuh"
+#include "internal.h"
+
+namespace sesgd {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int W>
+__device__ __forceinline__ void load(const float *p, float (&r)[W]) {
+  if constexpr (W == 4) {
+    float4 t = dev::ld4(p);
+    r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
+  } else {
+    r[0] = __ldcs(p);
+  }
+}
+template <int W>
+__device__ __forceinline__ void store(float *p, const float (&r)[W]) {
+  if constexpr (W == 4) {
+    dev::st4(p, make_float4(r[0], r[1], r[2], r[3]));
+  } else {
+    __stcs(p, r[0]);
+  }
+}
+
+// Registers of one W-wide item for a group of compile-time size M.
+template <int M, int W, bool GRAD>
+struct Item {
+  float g[M][W], v[M][W], x[M][W];
+
+  __device__ __forceinline__ void fetch(float *const *xp, float *const *vp,
+                                        const float *const *gp, int64_t e) {
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      load<W>(gp[r] + e, g[r]);
+      load<W>(vp[r] + e, v[r]);
+      load<W>(xp[r] + e, x[r]);
+    }
+  }
+
+  __device__ __forceinline__ void finish(float *const *xp, float *const *vp, int64_t e, float lr,
+                                         float mu) {
+    if constexpr (!GRAD) {
+#pragma unroll
+      for (int r = 0; r < M; ++r)
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          v[r][w] = dev::momentum(mu, v[r][w], g[r][w]);
+          x[r][w] = dev::sgd(x[r][w], lr, v[r][w]);  // x_hat, stays in registers
+        }
+      float mean[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        float s = x[0][w];
+#pragma unroll
+        for (int r = 1; r < M; ++r) s = __fadd_rn(s, x[r][w]);  // ascending member order
+        mean[w] = dev::mean_of<M>(s, M);
+      }
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        store<W>(vp[r] + e, v[r]);
+        store<W>(xp[r] + e, mean);
+      }
+    } else {
+      float gb[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        float s = g[0][w];
+#pragma unroll
+        for (int r = 1; r < M; ++r) s = __fadd_rn(s, g[r][w]);
+        gb[w] = dev::mean_of<M>(s, M);
+      }
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          v[r][w] = dev::momentum(mu, v[r][w], gb[w]);
+          x[r][w] = dev::sgd(x[r][w], lr, v[r][w]);
+        }
+        store<W>(vp[r] + e, v[r]);
+        store<W>(xp[r] + e, x[r]);
+      }
+    }
+  }
+};
+
+// Runtime-m item (any group size): member loop, fold kept in registers.
+template <int W, bool GRAD>
+__device__ __forceinline__ void item_generic(const ResidentArgs &a, const int8_t *mem, int m,
+                                             int64_t e) {
+  float s[W];
+  if constexpr (!GRAD) {
+    for (int r = 0; r < m; ++r) {
+      const int sl = mem[r];
+      float g[W], v[W], x[W];
+      load<W>(a.g[sl] + e, g);
+      load<W>(a.v[sl] + e, v);
+      load<W>(a.x[sl] + e, x);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        v[w] = dev::momentum(a.mu, v[w], g[w]);
+        x[w] = dev::sgd(x[w], a.lr, v[w]);
+        s[w] = (r == 0) ? x[w] : __fadd_rn(s[w], x[w]);
+      }
+      store<W>(a.v[sl] + e, v);
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) s[w] = __fdiv_rn(s[w], (float)m);
+    for (int r = 0; r < m; ++r) store<W>(a.x[mem[r]] + e, s);
+  } else {
+    for (int r = 0; r < m; ++r) {
+      float g[W];
+      load<W>(a.g[mem[r]] + e, g);
+#pragma unroll
+      for (int w = 0; w < W; ++w) s[w] = (r == 0) ? g[w] : __fadd_rn(s[w], g[w]);
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) s[w] = __fdiv_rn(s[w], (float)m);
+    for (int r = 0; r < m; ++r) {
+      const int sl = mem[r];
+      float v[W], x[W];
+      load<W>(a.v[sl] + e, v);
+      load<W>(a.x[sl] + e, x);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        v[w] = dev::momentum(a.mu, v[w], s[w]);
+        x[w] = dev::sgd(x[w], a.lr, v[w]);
+      }
+      store<W>(a.v[sl] + e, v);
+      store<W>(a.x[sl] + e, x);
+    }
+  }
+}
+
+template <int M>
+struct Unroll {
+  static constexpr int value = M == 0 ? 1 : (M <= 2 ? 4 : (M <= 4 ? 2 : 1));
+};
+
+template <int M, int W, bool GRAD>
+__global__ void __launch_bounds__(kThreads) k6_resident(const __grid_constant__ ResidentArgs a) {
+  const int m = M > 0 ? M : a.m;
+  const int8_t *mem = a.member_slot + blockIdx.y * m;
+  const int64_t nfull = a.numel / W;  // complete W-wide items
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+
+  if constexpr (M > 0) {
+    constexpr int U = Unroll<M>::value;
+    float *xp[M], *vp[M];
+    const float *gp[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      xp[r] = a.x[mem[r]];
+      vp[r] = a.v[mem[r]];
+      gp[r] = a.g[mem[r]];
+    }
+    // U independent items per trip: all 3*M*U loads are issued before the first store.
+    for (; i + (U - 1) * stride < nfull; i += U * stride) {
+      Item<M, W, GRAD> it[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) it[u].fetch(xp, vp, gp, (i + u * stride) * W);
+#pragma unroll
+      for (int u = 0; u < U; ++u) it[u].finish(xp, vp, (i + u * stride) * W, a.lr, a.mu);
+    }
+    for (; i < nfull; i += stride) {
+      Item<M, W, GRAD> it;
+      it.fetch(xp, vp, gp, i * W);
+      it.finish(xp, vp, i * W, a.lr, a.mu);
+    }
+  } else {
+    for (; i < nfull; i += stride) item_generic<W, GRAD>(a, mem, m, i * W);
+  }
+  // ragged tail (numel % 4 elements) of the vector path
+  if constexpr (W > 1) {
+    const int64_t tail = a.numel - nfull * W;
+    if (blockIdx.x == 0 && threadIdx.x < tail)
+      item_generic<1, GRAD>(a, mem, m, nfull * W + threadIdx.x);
+  }
+}
+
+template <int M, int W, bool GRAD>
+const void *kernel_ptr() {
+  return reinterpret_cast<const void *>(&k6_resident<M, W, GRAD>);
+}
+
+template <int W, bool GRAD>
+const void *pick_m(int m) {
+  switch (m) {
+    case 1: return kernel_ptr<1, W, GRAD>();
+    case 2: return kernel_ptr<2, W, GRAD>();
+    case 4: return kernel_ptr<4, W, GRAD>();
+    case 8: return kernel_ptr<8, W, GRAD>();
+    default: return kernel_ptr<0, W, GRAD>();
+  }
+}
+
+const void *pick(int mode, bool vec, int m) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (vec) return grad ? pick_m<4, true>(m) : pick_m<4, false>(m);
+  return grad ? pick_m<1, true>(m) : pick_m<1, false>(m);
+}
+
+}  // namespace
+
+int resident_block_threads() { return kThreads; }
+
+int resident_occupancy(int mode, bool vec, int m) {
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode, vec, m), kThreads, 0) !=
+      cudaSuccess)
+    return 1;
+  return blocks > 0 ? blocks : 1;
+}
+
+cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_x,
+                            cudaStream_t stream) {
+  dim3 grid(grid_x, a.k), block(kThreads);
+  void *args[] = {const_cast<ResidentArgs *>(&a)};
+  return cudaLaunchKernel(pick(mode, vec, a.m), grid, block, args, 0, stream);
+}
+
+}  // namespace sesgd

@@ -1,0 +1,513 @@
+// sesgd_capi.cu -- the C ABI of libsesgd.so (declared and documented in include/sesgd.h).
+//
+// Host-side control only: argument validation, the per-iteration schedule
+// (schedule.cpp), device tables, workspace layout, and kernel selection.  Every
+// step of the hot path runs in the kernels of resident.cu (1 GPU) and p2p.cu
+// (NVLink P2P); there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using sesgd::P2PArgs;
+using sesgd::ResidentArgs;
+
+namespace {
+
+constexpr int kMaxBuckets = 4096;
+constexpr uint64_t kMagic = 0x5345534744423230ULL;  // "SESGDB20"
+
+int fail(sesgd_ctx *ctx, int code, const std::string &why) {
+  if (ctx) ctx->last_error = why;
+  return code;
+}
+
+int cuda_fail(sesgd_ctx *ctx, cudaError_t e, const char *what) {
+  std::string s = std::string(what) + ": " + cudaGetErrorString(e);
+  return fail(ctx, SESGD_ECUDA, s);
+}
+
+bool valid_nm(int32_t n, int32_t m) { return n >= 1 && n <= SESGD_MAX_WORKERS && m >= 1 && m <= n; }
+
+uint64_t fnv(uint64_t h, uint64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xff;
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_latched(sesgd_ctx *ctx) {
+  if (ctx->h_err && *reinterpret_cast<volatile unsigned int *>(ctx->h_err) != 0)
+    return fail(ctx, SESGD_ETIMEOUT, "a group peer did not signal before the timeout");
+  return SESGD_OK;
+}
+
+void free_bucket(sesgd_bucket &b) {
+  if (b.d_x) cudaFree(b.d_x);
+  if (b.d_v) cudaFree(b.d_v);
+  if (b.d_g) cudaFree(const_cast<float **>(b.d_g));
+  b.d_x = b.d_v = nullptr;
+  b.d_g = nullptr;
+}
+
+// ---- multi-GPU workspace layout (identical on every rank) ----
+//   [0, 256)            header: magic, layout hash
+//   [ready_off, ...)    u64 ready[r][grid][n]
+//   [done_off, ...)     u64 done [r][grid][n]
+//   [stage_off, ...)    f32 stage[2 parity][r slot][stage_slot_floats]
+void freeze_layout(sesgd_ctx *ctx) {
+  const int chunk = sesgd::p2p_chunk_elems();
+  int occ = sesgd::p2p_occupancy(SESGD_MODE_PARAM_AVG, true);
+  occ = std::min(occ, sesgd::p2p_occupancy(SESGD_MODE_GRAD_AVG, true));
+  occ = std::min(occ, sesgd::p2p_occupancy(SESGD_MODE_PARAM_AVG, false));
+  occ = std::min(occ, sesgd::p2p_occupancy(SESGD_MODE_GRAD_AVG, false));
+  int grid = ctx->sm_count * occ;  // every CTA co-resident: CTA j only waits on CTA j of peers
+  if (ctx->grid_opt > 0 && ctx->grid_opt < grid) grid = int(ctx->grid_opt);
+  ctx->grid = grid;
+  ctx->chunk = chunk;
+  int64_t off = 0, kmax = 1;
+  uint64_t h = 0xcbf29ce484222325ULL;
+  h = fnv(h, uint64_t(ctx->n));
+  h = fnv(h, uint64_t(ctx->m));
+  h = fnv(h, uint64_t(ctx->n_local));
+  h = fnv(h, uint64_t(grid));
+  h = fnv(h, uint64_t(chunk));
+  for (size_t b = 0; b < ctx->buckets.size(); ++b) {
+    sesgd_bucket &bk = ctx->buckets[b];
+    bk.stage_bucket_off = off;
+    bk.nchunks = (bk.numel + chunk - 1) / chunk;
+    kmax = std::max<int64_t>(kmax, (bk.nchunks + grid - 1) / grid);
+    off += round_up(bk.numel, 64);  // 256-byte aligned buckets
+    h = fnv(h, uint64_t(b));
+    h = fnv(h, uint64_t(bk.registered ? bk.numel : -1));
+  }
+  ctx->kmax = kmax;
+  ctx->stage_slot_floats = std::max<int64_t>(off, 64);
+  const int64_t flags = int64_t(ctx->n_local) * grid * ctx->n * 8;
+  ctx->ready_off = 256;
+  ctx->done_off = round_up(ctx->ready_off + flags, 256);
+  ctx->stage_off = round_up(ctx->done_off + flags, 4096);
+  ctx->ws_bytes = ctx->stage_off + 2 * int64_t(ctx->n_local) * ctx->stage_slot_floats * 4;
+  ctx->layout_hash = h;
+  ctx->layout_frozen = true;
+}
+
+uint64_t epoch_of(const sesgd_ctx *ctx, int64_t t, int bucket) {
+  const uint64_t nb = ctx->buckets.size();
+  return (uint64_t(t) * nb + uint64_t(bucket)) * uint64_t(ctx->kmax) + 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sesgd_strerror(int code) {
+  switch (code) {
+    case SESGD_OK: return "ok";
+    case SESGD_EINVAL: return "invalid argument";
+    case SESGD_ENOTDIV: return "group_size does not divide n";
+    case SESGD_ESTATE: return "invalid state for this call";
+    case SESGD_ECUDA: return "CUDA error";
+    case SESGD_ETIMEOUT: return "group peer timed out";
+    case SESGD_ENOMEM: return "out of memory";
+    case SESGD_ENOTSUP: return "not supported";
+    default: return "unknown status";
+  }
+}
+
+const char *sesgd_last_error(const sesgd_ctx *ctx) {
+  return ctx ? ctx->last_error.c_str() : "null context";
+}
+
+int sesgd_init(int32_t n, int32_t group_size, uint64_t seed, sesgd_ctx **out) {
+  if (!out) return SESGD_EINVAL;
+  *out = nullptr;
+  if (!valid_nm(n, group_size)) return SESGD_EINVAL;
+  if (n % group_size != 0) return SESGD_ENOTDIV;
+  sesgd_ctx *ctx = new (std::nothrow) sesgd_ctx();
+  if (!ctx) return SESGD_ENOMEM;
+  ctx->n = n;
+  ctx->m = group_size;
+  ctx->seed = seed;
+  std::memset(ctx->slot_of, -1, sizeof(ctx->slot_of));
+  *out = ctx;
+  return SESGD_OK;
+}
+
+void sesgd_destroy(sesgd_ctx *ctx) {
+  if (!ctx) return;
+  for (auto &b : ctx->buckets) free_bucket(b);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->d_abort) cudaFree(ctx->d_abort);
+  delete ctx;
+}
+
+int sesgd_groups(const sesgd_ctx *ctx, int64_t iter, int32_t *perm_out, int32_t *group_of_out) {
+  if (!ctx || !perm_out || iter < 0) return SESGD_EINVAL;
+  sesgd::shuffle_exchange_groups(ctx->seed, iter, ctx->n, ctx->m, perm_out, group_of_out);
+  return SESGD_OK;
+}
+
+int sesgd_latency_model(int32_t n, int32_t group_size, double bytes, double nu_Bps, double tau_s,
+                        sesgd_cost *out) {
+  if (!out || n < 1 || group_size < 1 || group_size > n) return SESGD_EINVAL;
+  if (n % group_size != 0) return SESGD_ENOTDIV;
+  if (!(nu_Bps > 0.0) || !(tau_s >= 0.0) || !(bytes >= 0.0)) return SESGD_EINVAL;
+  sesgd::latency_model(n, group_size, bytes, nu_Bps, tau_s, out);
+  return SESGD_OK;
+}
+
+int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
+  if (!ctx) return SESGD_EINVAL;
+  switch (option) {
+    case SESGD_OPT_MODE:
+      if (value != SESGD_MODE_PARAM_AVG && value != SESGD_MODE_GRAD_AVG)
+        return fail(ctx, SESGD_EINVAL, "mode must be SESGD_MODE_PARAM_AVG or SESGD_MODE_GRAD_AVG");
+      ctx->mode = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_PATH:
+      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_ONESHOT)
+        return fail(ctx, SESGD_EINVAL, "unknown path");
+      ctx->path = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_TIMEOUT_MS:
+      if (value < 1) return fail(ctx, SESGD_EINVAL, "timeout must be >= 1 ms");
+      ctx->timeout_ms = value;
+      return SESGD_OK;
+    case SESGD_OPT_GRID:
+      if (value < 0) return fail(ctx, SESGD_EINVAL, "grid must be >= 0");
+      if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "grid is fixed once peers attach");
+      ctx->grid_opt = value;
+      return SESGD_OK;
+    case SESGD_OPT_HOP_DELAY_NS:
+      if (value < 0) return fail(ctx, SESGD_EINVAL, "delay must be >= 0");
+      ctx->hop_delay_ns = value;
+      return SESGD_OK;
+    default:
+      return fail(ctx, SESGD_EINVAL, "unknown option");
+  }
+}
+
+int sesgd_attach(sesgd_ctx *ctx, int32_t device, int32_t n_local, const int32_t *local_workers) {
+  if (!ctx) return SESGD_EINVAL;
+  if (ctx->attached) return fail(ctx, SESGD_ESTATE, "already attached");
+  if (n_local < 1 || n_local > ctx->n || !local_workers)
+    return fail(ctx, SESGD_EINVAL, "n_local must be in [1, n] with a worker list");
+  int8_t slot_of[SESGD_MAX_WORKERS];
+  std::memset(slot_of, -1, sizeof(slot_of));
+  for (int s = 0; s < n_local; ++s) {
+    const int w = local_workers[s];
+    if (w < 0 || w >= ctx->n) return fail(ctx, SESGD_EINVAL, "worker id out of range");
+    if (slot_of[w] >= 0) return fail(ctx, SESGD_EINVAL, "duplicate worker id");
+    slot_of[w] = int8_t(s);
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaDeviceGetAttribute");
+  unsigned int *h = nullptr;
+  e = cudaHostAlloc(reinterpret_cast<void **>(&h), sizeof(unsigned int), cudaHostAllocMapped);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaHostAlloc(error word)");
+  *h = 0;
+  unsigned int *d = nullptr;
+  e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&d), h, 0);
+  if (e != cudaSuccess) {
+    cudaFreeHost(h);
+    return cuda_fail(ctx, e, "cudaHostGetDevicePointer");
+  }
+  unsigned int *ab = nullptr;
+  e = cudaMalloc(reinterpret_cast<void **>(&ab), sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(ab, 0, sizeof(unsigned int));
+  if (e != cudaSuccess) {
+    cudaFreeHost(h);
+    return cuda_fail(ctx, e, "cudaMalloc(abort word)");
+  }
+  ctx->h_err = h;
+  ctx->d_err = d;
+  ctx->d_abort = ab;
+  ctx->device = device;
+  ctx->sm_count = sms;
+  ctx->n_local = n_local;
+  ctx->local_workers.assign(local_workers, local_workers + n_local);
+  std::memcpy(ctx->slot_of, slot_of, sizeof(slot_of));
+  ctx->attached = true;
+  return SESGD_OK;
+}
+
+int sesgd_register_bucket(sesgd_ctx *ctx, int32_t bucket, int64_t numel, float *const *x,
+                          float *const *v, const float *const *g) {
+  if (!ctx) return SESGD_EINVAL;
+  if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
+  if (bucket < 0 || bucket >= kMaxBuckets) return fail(ctx, SESGD_EINVAL, "bucket id out of range");
+  if (numel < 0 || !x || !v || !g) return fail(ctx, SESGD_EINVAL, "null pointer table or numel < 0");
+  if (ctx->layout_frozen && (size_t(bucket) >= ctx->buckets.size() ||
+                             ctx->buckets[bucket].numel != numel))
+    return fail(ctx, SESGD_ESTATE, "bucket layout is fixed once peers attach");
+  bool vec = true;
+  for (int s = 0; s < ctx->n_local; ++s) {
+    if (numel > 0 && (!x[s] || !v[s] || !g[s]))
+      return fail(ctx, SESGD_EINVAL, "null device pointer");
+    vec = vec && aligned16(x[s]) && aligned16(v[s]) && aligned16(g[s]);
+  }
+  if (size_t(bucket) >= ctx->buckets.size()) ctx->buckets.resize(size_t(bucket) + 1);
+  sesgd_bucket &b = ctx->buckets[bucket];
+  const size_t bytes = sizeof(float *) * size_t(ctx->n_local);
+  if (!b.d_x) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&b.d_x), bytes);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&b.d_v), bytes);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&b.d_g), bytes);
+    if (e != cudaSuccess) {
+      free_bucket(b);
+      return cuda_fail(ctx, e, "cudaMalloc(pointer tables)");
+    }
+  }
+  b.hx.assign(x, x + ctx->n_local);
+  b.hv.assign(v, v + ctx->n_local);
+  b.hg.assign(g, g + ctx->n_local);
+  cudaError_t e = cudaMemcpy(b.d_x, b.hx.data(), bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(b.d_v, b.hv.data(), bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(const_cast<float **>(b.d_g), b.hg.data(), bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpy(pointer tables)");
+  b.numel = numel;
+  b.vec = vec;
+  b.registered = true;
+  return SESGD_OK;
+}
+
+int sesgd_workspace_bytes(const sesgd_ctx *cctx, int64_t *bytes_out) {
+  sesgd_ctx *ctx = const_cast<sesgd_ctx *>(cctx);
+  if (!ctx || !bytes_out) return SESGD_EINVAL;
+  if (!ctx->attached || ctx->buckets.empty())
+    return fail(ctx, SESGD_ESTATE, "attach and register buckets first");
+  for (auto &b : ctx->buckets)
+    if (!b.registered) return fail(ctx, SESGD_ESTATE, "bucket ids must be dense from 0");
+  if (!ctx->layout_frozen) freeze_layout(ctx);
+  *bytes_out = ctx->ws_bytes;
+  return SESGD_OK;
+}
+
+int sesgd_workspace_prepare(sesgd_ctx *ctx, void *local_ws) {
+  if (!ctx || !local_ws) return SESGD_EINVAL;
+  int64_t bytes = 0;
+  int rc = sesgd_workspace_bytes(ctx, &bytes);
+  if (rc != SESGD_OK) return rc;
+  // zero flags (stage contents are don't-care), then the header
+  cudaError_t e = cudaMemset(local_ws, 0, size_t(ctx->stage_off));
+  uint64_t hdr[2] = {kMagic, ctx->layout_hash};
+  if (e == cudaSuccess) e = cudaMemcpy(local_ws, hdr, sizeof(hdr), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "workspace prepare");
+  return SESGD_OK;
+}
+
+int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, void *const *rank_ws,
+                       const int32_t *worker_rank) {
+  if (!ctx || !rank_ws || !worker_rank) return SESGD_EINVAL;
+  if (n_ranks < 1 || n_ranks > SESGD_MAX_RANKS || rank < 0 || rank >= n_ranks)
+    return fail(ctx, SESGD_EINVAL, "rank / n_ranks out of range");
+  if (!ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "sesgd_workspace_prepare first");
+  // worker -> (rank, slot): slot = position among the rank's workers in ascending id
+  int count[SESGD_MAX_RANKS] = {0};
+  for (int w = 0; w < ctx->n; ++w) {
+    const int r = worker_rank[w];
+    if (r < 0 || r >= n_ranks) return fail(ctx, SESGD_EINVAL, "worker_rank out of range");
+    ctx->worker_rank[w] = int8_t(r);
+    ctx->worker_slot[w] = int8_t(count[r]++);
+  }
+  for (int r = 0; r < n_ranks; ++r)
+    if (count[r] != ctx->n_local)
+      return fail(ctx, SESGD_EINVAL, "every rank must host the same number of workers");
+  for (int s = 0; s < ctx->n_local; ++s) {
+    const int w = ctx->local_workers[s];
+    if (ctx->worker_rank[w] != rank || ctx->worker_slot[w] != s)
+      return fail(ctx, SESGD_EINVAL, "local workers must be this rank's workers in ascending order");
+  }
+  for (int r = 0; r < n_ranks; ++r) {
+    if (!rank_ws[r]) return fail(ctx, SESGD_EINVAL, "null workspace pointer");
+    uint64_t hdr[2] = {0, 0};
+    cudaError_t e = cudaMemcpy(hdr, rank_ws[r], sizeof(hdr), cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "reading a peer workspace header");
+    if (hdr[0] != kMagic || hdr[1] != ctx->layout_hash) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "rank %d workspace layout differs (magic %llx hash %llx vs %llx)",
+                    r, (unsigned long long)hdr[0], (unsigned long long)hdr[1],
+                    (unsigned long long)ctx->layout_hash);
+      return fail(ctx, SESGD_ESTATE, buf);
+    }
+    ctx->ws[r] = static_cast<char *>(rank_ws[r]);
+  }
+  ctx->n_ranks = n_ranks;
+  ctx->rank = rank;
+  ctx->peers = true;
+  return SESGD_OK;
+}
+
+int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter) {
+  if (!ctx) return SESGD_EINVAL;
+  if (iter < 0) return fail(ctx, SESGD_EINVAL, "iteration must be >= 0");
+  if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
+  sesgd::shuffle_exchange_groups(ctx->seed, iter, ctx->n, ctx->m, ctx->canon, ctx->group_of);
+  if (iter >= 2)
+    sesgd::shuffle_exchange_groups(ctx->seed, iter - 2, ctx->n, ctx->m, ctx->canon_prev,
+                                   ctx->group_of_prev);
+  ctx->t = iter;
+  ctx->iter_set = true;
+  return SESGD_OK;
+}
+
+int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  int rc = check_latched(ctx);
+  if (rc != SESGD_OK) return rc;
+  if (!ctx->attached || !ctx->iter_set) return fail(ctx, SESGD_ESTATE, "attach and begin_iter first");
+  if (bucket < 0 || size_t(bucket) >= ctx->buckets.size() || !ctx->buckets[bucket].registered)
+    return fail(ctx, SESGD_EINVAL, "bucket not registered");
+  if (!std::isfinite(lr) || !std::isfinite(momentum))
+    return fail(ctx, SESGD_EINVAL, "lr and momentum must be finite");
+  sesgd_bucket &b = ctx->buckets[bucket];
+  b.stats.sync_calls++;
+  if (b.numel == 0) return SESGD_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool all_local = (ctx->n_local == ctx->n);
+  int path = ctx->path;
+  if (path == SESGD_PATH_AUTO) path = all_local ? SESGD_PATH_RESIDENT : SESGD_PATH_ONESHOT;
+
+  if (path == SESGD_PATH_RESIDENT) {
+    if (!all_local) return fail(ctx, SESGD_ESTATE, "resident path needs all n workers on this GPU");
+    ResidentArgs a{};
+    a.x = b.d_x;
+    a.v = b.d_v;
+    a.g = b.d_g;
+    a.numel = b.numel;
+    a.lr = lr;
+    a.mu = momentum;
+    a.m = ctx->m;
+    a.k = ctx->n / ctx->m;
+    for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
+    const int threads = sesgd::resident_block_threads();
+    int target = ctx->sm_count * sesgd::resident_occupancy(ctx->mode, b.vec, ctx->m);
+    if (ctx->grid_opt > 0) target = int(ctx->grid_opt);
+    int gx = (target + a.k - 1) / a.k;
+    const int64_t items = b.vec ? b.numel / 4 : b.numel;
+    const int64_t need = (items + threads - 1) / threads;
+    if (need < gx) gx = int(need > 0 ? need : 1);
+    cudaError_t e = sesgd::launch_resident(a, ctx->mode, b.vec, gx, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel");
+    b.stats.kernel_launches++;
+    b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n;
+    return SESGD_OK;
+  }
+
+  // one-shot NVLink P2P
+  if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
+  P2PArgs a{};
+  a.x = b.d_x;
+  a.v = b.d_v;
+  a.g = b.d_g;
+  for (int r = 0; r < ctx->n_ranks; ++r) a.ws[r] = ctx->ws[r];
+  a.numel = b.numel;
+  a.chunk = ctx->chunk;
+  a.nchunks = b.nchunks;
+  a.stage_off = ctx->stage_off;
+  a.stage_slot_floats = ctx->stage_slot_floats;
+  a.stage_bucket_off = b.stage_bucket_off;
+  a.ready_off = ctx->ready_off;
+  a.done_off = ctx->done_off;
+  a.epoch0 = epoch_of(ctx, ctx->t, bucket);
+  a.epoch_prev0 = ctx->t >= 2 ? epoch_of(ctx, ctx->t - 2, bucket) : 0;
+  a.timeout_ns = uint64_t(ctx->timeout_ms) * 1000000ULL;
+  a.hop_delay_ns = uint64_t(ctx->hop_delay_ns);
+  a.err_host = ctx->d_err;
+  a.abort_dev = ctx->d_abort;
+  a.lr = lr;
+  a.mu = momentum;
+  a.n = ctx->n;
+  a.m = ctx->m;
+  a.r = ctx->n_local;
+  a.grid = ctx->grid;
+  a.parity = int(ctx->t & 1);
+  a.my_rank = ctx->rank;
+  for (int s = 0; s < ctx->n_local; ++s) a.my_workers[s] = int8_t(ctx->local_workers[s]);
+  for (int i = 0; i < ctx->n; ++i) {
+    a.worker_rank[i] = ctx->worker_rank[i];
+    a.worker_slot[i] = ctx->worker_slot[i];
+    a.canon[i] = int8_t(ctx->canon[i]);
+    a.group_of[i] = int8_t(ctx->group_of[i]);
+    a.canon_prev[i] = int8_t(ctx->t >= 2 ? ctx->canon_prev[i] : 0);
+    a.group_of_prev[i] = int8_t(ctx->t >= 2 ? ctx->group_of_prev[i] : 0);
+  }
+  cudaError_t e = sesgd::launch_p2p_oneshot(a, ctx->mode, b.vec, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch one-shot kernel");
+  b.stats.kernel_launches++;
+  b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n_local;
+  if (ctx->m > 1) {
+    b.stats.handshake_rounds = 1;
+    int remote_peers = 0;
+    for (int s = 0; s < ctx->n_local; ++s) {
+      const int me = ctx->local_workers[s];
+      const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
+      for (int r = 0; r < ctx->m; ++r)
+        if (G[r] != me && ctx->worker_rank[G[r]] != ctx->rank) remote_peers++;
+    }
+    b.stats.flag_messages += 2 * int64_t(remote_peers) * b.nchunks;  // ready + done per chunk
+    b.stats.payload_bytes_in += int64_t(remote_peers) * b.numel * 4;
+  }
+  return SESGD_OK;
+}
+
+int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,
+                         const float *const *g_host, float *const *x_host_out, void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  if (!g_host || !x_host_out) return fail(ctx, SESGD_EINVAL, "null host buffer table");
+  if (bucket < 0 || size_t(bucket) >= ctx->buckets.size() || !ctx->buckets[bucket].registered)
+    return fail(ctx, SESGD_EINVAL, "bucket not registered");
+  sesgd_bucket &b = ctx->buckets[bucket];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = size_t(b.numel) * sizeof(float);
+  for (int s = 0; s < ctx->n_local; ++s) {
+    if (!g_host[s] || !x_host_out[s]) return fail(ctx, SESGD_EINVAL, "null host buffer");
+    cudaError_t e = cudaMemcpyAsync(const_cast<float *>(b.hg[s]), g_host[s], bytes,
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D gradient copy");
+  }
+  int rc = sesgd_sync_step(ctx, bucket, lr, momentum, stream);
+  if (rc != SESGD_OK) return rc;
+  for (int s = 0; s < ctx->n_local; ++s) {
+    cudaError_t e = cudaMemcpyAsync(x_host_out[s], b.hx[s], bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H parameter copy");
+  }
+  return SESGD_OK;
+}
+
+int sesgd_poll(sesgd_ctx *ctx) {
+  if (!ctx) return SESGD_EINVAL;
+  return check_latched(ctx);
+}
+
+int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats *out) {
+  if (!ctx || !out || bucket < 0 || size_t(bucket) >= ctx->buckets.size()) return SESGD_EINVAL;
+  *out = ctx->buckets[bucket].stats;
+  return SESGD_OK;
+}
+
+int sesgd_launch_grid(const sesgd_ctx *ctx, int32_t *ctas_out) {
+  if (!ctx || !ctas_out) return SESGD_EINVAL;
+  *ctas_out = ctx->peers ? ctx->grid : ctx->sm_count;
+  return SESGD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+"""SESGDEngine: owns the per-worker fp32 buckets as torch tensors and drives libsesgd.
+
+PyTorch is used only for device memory, streams and process groups (symmetric
+memory for the peer-visible workspace); all arithmetic runs in libsesgd's kernels.
+
+Layout in HBM: per local worker one flat tensor per
+array (x, v, g), buckets packed back to back at 64-float (256 B) aligned offsets,
+so every bucket is a 16-byte-aligned view (128-bit vector path) and a model's
+parameters/gradients can be views into the same storage (fusion buffer, no pack copy).
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+
+from . import sesgd as C
+
+
+def _aligned_offsets(sizes: Sequence[int], align: int = 64):
+    offs, o = [], 0
+    for s in sizes:
+        offs.append(o)
+        o += (int(s) + align - 1) // align * align
+    return offs, max(o, align)
+
+
+class SESGDEngine:
+    def __init__(self, n: int, group_size: int, bucket_sizes: Sequence[int], *, seed: int = 42,
+                 device: Optional[int] = None, mode: int = C.MODE_PARAM_AVG,
+                 rank: int = 0, world: int = 1, process_group=None, path: int = C.PATH_AUTO,
+                 grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0):
+        if n % world != 0:
+            raise ValueError("n must be a multiple of the number of ranks")
+        self.n, self.m, self.seed = n, group_size, seed
+        self.rank, self.world = rank, world
+        self.r = n // world
+        self.local_workers = list(range(rank * self.r, (rank + 1) * self.r))
+        self.worker_rank = [i // self.r for i in range(n)]
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.bucket_sizes = [int(s) for s in bucket_sizes]
+        self.ctx = C.sesgd_init(n, group_size, seed)
+        C.sesgd_set_option(self.ctx, C.OPT_MODE, mode)
+        C.sesgd_set_option(self.ctx, C.OPT_PATH, path)
+        C.sesgd_set_option(self.ctx, C.OPT_TIMEOUT_MS, timeout_ms)
+        C.sesgd_set_option(self.ctx, C.OPT_HOP_DELAY_NS, hop_delay_ns)
+        if grid:
+            C.sesgd_set_option(self.ctx, C.OPT_GRID, grid)
+        C.sesgd_attach(self.ctx, self.device.index, self.local_workers)
+
+        self.offsets, total = _aligned_offsets(self.bucket_sizes)
+        mk = lambda: torch.zeros(total, dtype=torch.float32, device=self.device)  # noqa: E731
+        self.x_flat = [mk() for _ in range(self.r)]
+        self.v_flat = [mk() for _ in range(self.r)]
+        self.g_flat = [mk() for _ in range(self.r)]
+        for b, numel in enumerate(self.bucket_sizes):
+            C.sesgd_register_bucket(self.ctx, b, numel,
+                                    [t.data_ptr() + 4 * self.offsets[b] for t in self.x_flat],
+                                    [t.data_ptr() + 4 * self.offsets[b] for t in self.v_flat],
+                                    [t.data_ptr() + 4 * self.offsets[b] for t in self.g_flat])
+        self.workspace = None
+        if world > 1:
+            self._attach_peers(process_group)
+
+    # -------------------------------------------------------------- multi-GPU
+    def _attach_peers(self, process_group):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        group = process_group or dist.group.WORLD
+        nbytes = C.sesgd_workspace_bytes(self.ctx)
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            try:
+                symm_mem.enable_symm_mem_for_group(group.group_name)
+            except Exception:  # already enabled / not needed in this torch
+                pass
+        self.workspace = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
+        C.sesgd_workspace_prepare(self.ctx, self.workspace.data_ptr())
+        self._symm = symm_mem.rendezvous(self.workspace, group)
+        dist.barrier(group=group)
+        ptrs = list(self._symm.buffer_ptrs)
+        C.sesgd_attach_peers(self.ctx, self.world, self.rank, ptrs, self.worker_rank)
+        dist.barrier(group=group)
+
+    # -------------------------------------------------------------- views
+    def view(self, flat: torch.Tensor, b: int) -> torch.Tensor:
+        o = self.offsets[b]
+        return flat[o:o + self.bucket_sizes[b]]
+
+    def x(self, slot: int, b: int) -> torch.Tensor:
+        return self.view(self.x_flat[slot], b)
+
+    def v(self, slot: int, b: int) -> torch.Tensor:
+        return self.view(self.v_flat[slot], b)
+
+    def g(self, slot: int, b: int) -> torch.Tensor:
+        return self.view(self.g_flat[slot], b)
+
+    # -------------------------------------------------------------- hot path
+    def begin_iter(self, t: int) -> None:
+        C.sesgd_begin_iter(self.ctx, t)
+
+    def sync_step(self, b: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        C.sesgd_sync_step(self.ctx, b, lr, momentum, s.cuda_stream)
+
+    def step(self, t: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
+        """One SESGD iteration over every bucket (Alg.1 lines 3-11 for all local workers)."""
+        self.begin_iter(t)
+        for b in range(len(self.bucket_sizes)):
+            self.sync_step(b, lr, momentum, stream)
+
+    def step_host(self, t: int, lr: float, momentum: float, g_host, x_host,
+                  stream: Optional[torch.cuda.Stream] = None):
+        """End-to-end through host buffers: g_host[b][slot] -> device, sync, device x -> x_host[b][slot]."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.begin_iter(t)
+        for b in range(len(self.bucket_sizes)):
+            C.sesgd_sync_step_host(self.ctx, b, lr, momentum, [h.data_ptr() for h in g_host[b]],
+                                   [h.data_ptr() for h in x_host[b]], s.cuda_stream)
+
+    def groups(self, t: int):
+        return C.sesgd_groups(self.ctx, t, self.n)
+
+    def stats(self, b: int) -> dict:
+        return C.sesgd_get_stats(self.ctx, b)
+
+    def poll(self) -> None:
+        C.sesgd_poll(self.ctx)
+
+    def close(self) -> None:
+        if self.ctx is not None:
+            C.sesgd_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

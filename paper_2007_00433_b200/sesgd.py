@@ -1,0 +1,182 @@
+"""Thin ctypes binding of libsesgd.so (include/sesgd.h), same names as the C ABI.
+
+Argument marshalling only: every step of the SESGD hot path runs in the CUDA
+kernels behind these calls.  There is no Python or CPU fallback -- importing
+this module fails loudly if the in-tree ``libsesgd.so`` is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsesgd.so")
+
+OK, EINVAL, ENOTDIV, ESTATE, ECUDA, ETIMEOUT, ENOMEM, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7
+MAX_WORKERS, MAX_RANKS = 64, 8
+MODE_PARAM_AVG, MODE_GRAD_AVG = 0, 1
+PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT = 0, 1, 2
+OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS = 1, 2, 3, 4, 5
+
+# every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
+EXPORTED = (
+    "sesgd_init", "sesgd_destroy", "sesgd_groups", "sesgd_latency_model", "sesgd_set_option",
+    "sesgd_attach", "sesgd_register_bucket", "sesgd_workspace_bytes", "sesgd_workspace_prepare",
+    "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
+    "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
+)
+
+
+class sesgd_cost(ctypes.Structure):
+    _fields_ = [("ring_handshakes", ctypes.c_double), ("sesgd_handshakes", ctypes.c_double),
+                ("ring_s", ctypes.c_double), ("sesgd_s", ctypes.c_double), ("ratio", ctypes.c_double)]
+
+
+class sesgd_stats(ctypes.Structure):
+    _fields_ = [("sync_calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("handshake_rounds", ctypes.c_int64), ("flag_messages", ctypes.c_int64),
+                ("payload_bytes_in", ctypes.c_int64), ("hbm_algo_bytes", ctypes.c_int64)]
+
+
+class SesgdError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        super().__init__(f"{lib().sesgd_strerror(code).decode()} ({code}){': ' + what if what else ''}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, u64, f32, f64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                      ctypes.c_uint64, ctypes.c_float, ctypes.c_double)
+        sig = {
+            "sesgd_init": ([i32, i32, u64, ctypes.POINTER(P)], ctypes.c_int),
+            "sesgd_destroy": ([P], None),
+            "sesgd_groups": ([P, i64, P, P], ctypes.c_int),
+            "sesgd_latency_model": ([i32, i32, f64, f64, f64, ctypes.POINTER(sesgd_cost)], ctypes.c_int),
+            "sesgd_set_option": ([P, i32, i64], ctypes.c_int),
+            "sesgd_attach": ([P, i32, i32, P], ctypes.c_int),
+            "sesgd_register_bucket": ([P, i32, i64, P, P, P], ctypes.c_int),
+            "sesgd_workspace_bytes": ([P, ctypes.POINTER(i64)], ctypes.c_int),
+            "sesgd_workspace_prepare": ([P, P], ctypes.c_int),
+            "sesgd_attach_peers": ([P, i32, i32, P, P], ctypes.c_int),
+            "sesgd_begin_iter": ([P, i64], ctypes.c_int),
+            "sesgd_sync_step": ([P, i32, f32, f32, P], ctypes.c_int),
+            "sesgd_sync_step_host": ([P, i32, f32, f32, P, P, P], ctypes.c_int),
+            "sesgd_poll": ([P], ctypes.c_int),
+            "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
+            "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
+            "sesgd_strerror": ([ctypes.c_int], ctypes.c_char_p),
+            "sesgd_last_error": ([P], ctypes.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, ctx=None) -> None:
+    if rc != OK:
+        what = lib().sesgd_last_error(ctx).decode() if ctx else ""
+        raise SesgdError(rc, what)
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+    return arr
+
+
+# ------------------------------------------------------------------ C-ABI calls
+def sesgd_init(n: int, group_size: int, seed: int):
+    ctx = ctypes.c_void_p()
+    _check(lib().sesgd_init(n, group_size, seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(ctx)))
+    return ctx
+
+
+def sesgd_destroy(ctx) -> None:
+    lib().sesgd_destroy(ctx)
+
+
+def sesgd_groups(ctx, it: int, n: int):
+    perm = np.empty(n, np.int32)
+    gof = np.empty(n, np.int32)
+    _check(lib().sesgd_groups(ctx, it, perm.ctypes.data_as(ctypes.c_void_p),
+                              gof.ctypes.data_as(ctypes.c_void_p)), ctx)
+    return perm, gof
+
+
+def sesgd_latency_model(n: int, group_size: int, nbytes: float, nu_Bps: float, tau_s: float) -> dict:
+    out = sesgd_cost()
+    _check(lib().sesgd_latency_model(n, group_size, float(nbytes), float(nu_Bps), float(tau_s),
+                                     ctypes.byref(out)))
+    return {f: getattr(out, f) for f, _ in sesgd_cost._fields_}
+
+
+def sesgd_set_option(ctx, option: int, value: int) -> None:
+    _check(lib().sesgd_set_option(ctx, option, int(value)), ctx)
+
+
+def sesgd_attach(ctx, device: int, local_workers) -> None:
+    lw = np.ascontiguousarray(local_workers, np.int32)
+    _check(lib().sesgd_attach(ctx, device, len(lw), lw.ctypes.data_as(ctypes.c_void_p)), ctx)
+
+
+def sesgd_register_bucket(ctx, bucket: int, numel: int, x_ptrs, v_ptrs, g_ptrs) -> None:
+    _check(lib().sesgd_register_bucket(ctx, bucket, numel, _ptr_array(x_ptrs), _ptr_array(v_ptrs),
+                                       _ptr_array(g_ptrs)), ctx)
+
+
+def sesgd_workspace_bytes(ctx) -> int:
+    out = ctypes.c_int64()
+    _check(lib().sesgd_workspace_bytes(ctx, ctypes.byref(out)), ctx)
+    return out.value
+
+
+def sesgd_workspace_prepare(ctx, local_ws_ptr: int) -> None:
+    _check(lib().sesgd_workspace_prepare(ctx, ctypes.c_void_p(int(local_ws_ptr))), ctx)
+
+
+def sesgd_attach_peers(ctx, n_ranks: int, rank: int, rank_ws_ptrs, worker_rank) -> None:
+    wr = np.ascontiguousarray(worker_rank, np.int32)
+    _check(lib().sesgd_attach_peers(ctx, n_ranks, rank, _ptr_array(rank_ws_ptrs),
+                                    wr.ctypes.data_as(ctypes.c_void_p)), ctx)
+
+
+def sesgd_begin_iter(ctx, it: int) -> None:
+    _check(lib().sesgd_begin_iter(ctx, it), ctx)
+
+
+def sesgd_sync_step(ctx, bucket: int, lr: float, momentum: float, stream: int = 0) -> None:
+    _check(lib().sesgd_sync_step(ctx, bucket, lr, momentum, ctypes.c_void_p(int(stream))), ctx)
+
+
+def sesgd_sync_step_host(ctx, bucket: int, lr: float, momentum: float, g_host_ptrs, x_host_ptrs,
+                         stream: int = 0) -> None:
+    _check(lib().sesgd_sync_step_host(ctx, bucket, lr, momentum, _ptr_array(g_host_ptrs),
+                                      _ptr_array(x_host_ptrs), ctypes.c_void_p(int(stream))), ctx)
+
+
+def sesgd_poll(ctx) -> None:
+    _check(lib().sesgd_poll(ctx), ctx)
+
+
+def sesgd_get_stats(ctx, bucket: int) -> dict:
+    out = sesgd_stats()
+    _check(lib().sesgd_get_stats(ctx, bucket, ctypes.byref(out)), ctx)
+    return {f: getattr(out, f) for f, _ in sesgd_stats._fields_}
+
+
+def sesgd_launch_grid(ctx) -> int:
+    out = ctypes.c_int32()
+    _check(lib().sesgd_launch_grid(ctx, ctypes.byref(out)), ctx)
+    return out.value

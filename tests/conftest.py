@@ -16,3 +16,17 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+def _build_all():
+    """Compile the oracle (gcc), the input generator and libsesgd (nvcc, sm_100a) in-tree
+    if they are missing or stale, so a fresh checkout can run the suite."""
+    import oracle
+    import synth
+    from paper_2007_00433_b200 import _build
+    oracle.build()
+    synth.build()
+    _build.build()
+
+
+_build_all()

@@ -1,0 +1,61 @@
+"""Per-rank body of the multi-GPU parity test (launched by tests/test_gpu_multigpu.py via
+torch.distributed.run).  Runs T SESGD iterations through the one-shot NVLink P2P path
+and saves every local worker's x and v for the parent to compare with the oracle."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import synth  # noqa: E402
+from paper_2007_00433_b200 import sesgd as C  # noqa: E402
+from paper_2007_00433_b200.engine import SESGDEngine  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--n", type=int, required=True)
+    p.add_argument("--m", type=int, required=True)
+    p.add_argument("--T", type=int, required=True)
+    p.add_argument("--buckets", required=True)
+    p.add_argument("--mode", type=int, default=0)
+    p.add_argument("--t0", type=int, default=0)
+    p.add_argument("--grid", type=int, default=0)
+    p.add_argument("--out", required=True)
+    a = p.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    buckets = [int(b) for b in a.buckets.split(",")]
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    eng = SESGDEngine(a.n, a.m, buckets, seed=42, mode=a.mode, rank=rank, world=world,
+                      grid=a.grid, timeout_ms=10000)
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(eng.r):
+        for b, L in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st)
+    for t in range(a.t0, a.t0 + a.T):
+        for s, w in enumerate(eng.local_workers):
+            for b, L in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
+        eng.step(t, 0.1, 0.9)
+    torch.cuda.synchronize()
+    eng.poll()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    stats = eng.stats(0)
+    np.savez(f"{a.out}.rank{rank}.npz", X=X, V=V, workers=np.array(eng.local_workers),
+             flag_messages=stats["flag_messages"], payload=stats["payload_bytes_in"])
+    dist.barrier()
+    eng.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

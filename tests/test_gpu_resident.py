@@ -1,0 +1,179 @@
+"""GPU parity of the 1-GPU path (K6, all n workers resident) against the CPU oracle.
+
+Every test drives the C ABI (through SESGDEngine / the ctypes binding), fills the
+seeded synthetic inputs on the device (synth/), runs T iterations and compares
+element by element with oracle.run on the same inputs.  Bar (BASELINE north star):
+<= 1e-5 relative with atol 1e-7 (fp32); the kernels use the oracle's binary32 op
+order, so the comparison is additionally asserted bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-7
+LR, MU = 0.1, 0.9
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2007_00433_b200.engine import SESGDEngine
+    return SESGDEngine
+
+
+def _run_gpu(n, m, buckets, T, mode, seed=42, slot_misalign=False):
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    eng = SESGDEngine(n, m, buckets, seed=seed, mode=mode)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    stream = torch.cuda.current_stream()
+    for s in range(eng.r):
+        for b, L in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), stream.cuda_stream)
+    for t in range(T):
+        for s, w in enumerate(eng.local_workers):
+            for b, L in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, stream.cuda_stream)
+        eng.step(t, LR, MU)
+    torch.cuda.synchronize()
+    eng.poll()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    stats = [eng.stats(b) for b in range(len(buckets))]
+    eng.close()
+    return X, V, stats
+
+
+def _run_oracle(n, m, L, T, mode, seed=42, coords=None):
+    S = L if coords is None else len(coords)
+    x = np.tile(synth.x0_host(S, coords=coords), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run(n, m, seed, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=mode, coords=coords)
+    return x, v
+
+
+def _compare(got, want):
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    mism = int(np.count_nonzero(got.view(np.uint32) != want.view(np.uint32)))
+    assert mism == 0, f"{mism} elements differ in bits (within tolerance)"
+
+
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+def test_config1_full_parity(mode):
+    """BASELINE configs[0]: n=4, group_size=2, 3 odd-sized buckets totalling 2^20, T=8."""
+    from paper_2007_00433_b200.workloads import CONFIG1_BUCKETS
+    n, m, T = 4, 2, 8
+    X, V, stats = _run_gpu(n, m, CONFIG1_BUCKETS, T, mode)
+    x, v = _run_oracle(n, m, sum(CONFIG1_BUCKETS), T, mode)
+    _compare(X, x)
+    _compare(V, v)
+    assert all(s["sync_calls"] == T and s["kernel_launches"] == T for s in stats)
+
+
+@pytest.mark.parametrize("n,m", [(4, 1), (4, 4), (8, 2), (8, 4), (8, 8), (6, 3), (16, 4), (12, 6)])
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+def test_group_sizes_and_ragged_tails(n, m, mode):
+    """m in {1, n, 2, 4, 8} (templated kernels) and 3, 6 (runtime-m kernel); bucket sizes that
+    span several CTAs, ragged tails of 1-3 elements, an empty bucket and a 1-element bucket."""
+    buckets = [70001, 0, 1, 4099, 12345]
+    T = 5
+    X, V, _ = _run_gpu(n, m, buckets, T, mode)
+    x, v = _run_oracle(n, m, sum(buckets), T, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_unaligned_pointers_take_scalar_path():
+    """Pointers not 16-byte aligned: the scalar kernel gives the same bits."""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    n, m, L, T = 4, 2, 10007, 4
+    dev = torch.device("cuda", 0)
+    xs = [torch.zeros(L + 1, device=dev) for _ in range(n)]
+    vs = [torch.zeros(L + 1, device=dev) for _ in range(n)]
+    gs = [torch.zeros(L + 1, device=dev) for _ in range(n)]
+    ctx = C.sesgd_init(n, m, 42)
+    C.sesgd_attach(ctx, 0, list(range(n)))
+    ptr = lambda t: t.data_ptr() + 4  # noqa: E731  (offset by one float: 4-byte aligned only)
+    C.sesgd_register_bucket(ctx, 0, L, [ptr(t) for t in xs], [ptr(t) for t in vs], [ptr(t) for t in gs])
+    st = torch.cuda.current_stream().cuda_stream
+    for i in range(n):
+        synth.fill_x0_device(ptr(xs[i]), L, 0, st)
+    for t in range(T):
+        for i in range(n):
+            synth.fill_grad_device(ptr(gs[i]), L, 0, i, t, st)
+        C.sesgd_begin_iter(ctx, t)
+        C.sesgd_sync_step(ctx, 0, LR, MU, st)
+    torch.cuda.synchronize()
+    X = np.stack([t[1:].cpu().numpy() for t in xs])
+    C.sesgd_destroy(ctx)
+    x, _ = _run_oracle(n, m, L, T, oracle.MODE_PARAM)
+    _compare(X, x)
+
+
+def test_random_access_iterations_and_resume():
+    """sesgd_begin_iter(t) at arbitrary t (S:152 restart): iterations t0..t0+T-1 equal the
+    oracle started at t0."""
+    SESGDEngine = _cuda()
+    n, m, L, t0, T = 8, 2, 30000, 1000, 3
+    eng = SESGDEngine(n, m, [L])
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(n):
+        synth.fill_x0_device(eng.x(s, 0).data_ptr(), L, 0, st)
+    for t in range(t0, t0 + T):
+        for s in range(n):
+            synth.fill_grad_device(eng.g(s, 0).data_ptr(), L, 0, s, t, st)
+        eng.step(t, LR, MU)
+    torch.cuda.synchronize()
+    X = np.stack([eng.x(s, 0).cpu().numpy() for s in range(n)])
+    eng.close()
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, t0=t0)
+    _compare(X, x)
+
+
+def test_resnet50_full_size_sampled():
+    """BASELINE configs[1] at full size on one GPU (8 resident workers, group_size 2, the five
+    ResNet-50 DDP buckets, 25,557,032 fp32 each) for T=100 iterations, in the launch
+    configuration bench.py times; the oracle replays 3000 sampled coordinates (bucket edges,
+    ragged tails, random interior) of the same run."""
+    from paper_2007_00433_b200.workloads import RESNET50_BUCKETS
+    SESGDEngine = _cuda()
+    n, m, T = 8, 2, 100
+    buckets = list(RESNET50_BUCKETS)
+    L = sum(buckets)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    rng = np.random.default_rng(11)
+    edges = np.concatenate([[o, o + 1, o + s - 1, o + s - 2] for o, s in zip(offs, buckets)])
+    coords = np.unique(np.concatenate([edges, rng.integers(0, L, 3000 - len(edges))])).astype(np.int64)
+    eng = SESGDEngine(n, m, buckets)
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(n):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), st)
+    for t in range(T):
+        for s in range(n):
+            for b, Lb in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), s, t, st)
+        eng.step(t, LR, MU)
+    torch.cuda.synchronize()
+    idx = torch.from_numpy(coords).cuda()
+    X = np.stack([eng.x_flat[s][_padded(idx, buckets, eng.offsets)].cpu().numpy() for s in range(n)])
+    V = np.stack([eng.v_flat[s][_padded(idx, buckets, eng.offsets)].cpu().numpy() for s in range(n)])
+    eng.close()
+    x, v = _run_oracle(n, m, L, T, oracle.MODE_PARAM, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def _padded(idx, buckets, offsets):
+    """map global (unpadded) element indices to the engine's aligned flat layout"""
+    starts = torch.tensor(np.concatenate([[0], np.cumsum(buckets)[:-1]]), device=idx.device)
+    b = torch.searchsorted(starts, idx, right=True) - 1
+    return idx - starts[b] + torch.tensor(offsets, device=idx.device)[b]
