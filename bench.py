@@ -147,8 +147,8 @@ def cpu_oracle_rate(n, m, budget_s, mode):
     probe_S, probe_T = 20000, 2
     dt = run(probe_S, probe_T)
     rate = n * probe_S * probe_T / dt  # worker-elements / s
-    T = 4
-    S = int(max(1000, min(25557032, rate * budget_s / (n * T))))
+    S = int(max(1000, min(25557032, rate * budget_s / (n * 4))))
+    T = int(max(4, min(100, rate * budget_s / (n * S))))
     dt = run(S, T)
     gbs = BYTES_PER_WORKER_ELEM * n * S * T / dt / 1e9
     sample = (f"n={n}, m={m}: {S} of 25,557,032 coordinates x {T} iterations "

@@ -18,9 +18,9 @@ from paper_2007_00433_b200.engine import SESGDEngine  # noqa: E402
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--n", type=int, required=True)
-    p.add_argument("--m", type=int, required=True)
-    p.add_argument("--T", type=int, required=True)
+    p.add_argument("--workers", type=int, required=True)
+    p.add_argument("--gsize", type=int, required=True)
+    p.add_argument("--iters", type=int, required=True)
     p.add_argument("--buckets", required=True)
     p.add_argument("--mode", type=int, default=0)
     p.add_argument("--t0", type=int, default=0)
@@ -34,13 +34,13 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     buckets = [int(b) for b in a.buckets.split(",")]
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
-    eng = SESGDEngine(a.n, a.m, buckets, seed=42, mode=a.mode, rank=rank, world=world,
+    eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
                       grid=a.grid, timeout_ms=10000)
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):
             synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st)
-    for t in range(a.t0, a.t0 + a.T):
+    for t in range(a.t0, a.t0 + a.iters):
         for s, w in enumerate(eng.local_workers):
             for b, L in enumerate(buckets):
                 synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)

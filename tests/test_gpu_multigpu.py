@@ -34,7 +34,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0):
     out = str(tmp_path / "res")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "tests", "mgpu_worker.py"), "--n", str(n), "--m", str(m), "--T", str(T),
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), "--workers", str(n), "--gsize", str(m), "--iters", str(T),
            "--buckets", ",".join(map(str, buckets)), "--mode", str(mode), "--t0", str(t0),
            "--grid", str(grid), "--out", out]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
