@@ -42,12 +42,15 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="sesgd", choices=["sesgd", "reference"])
     p.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16", "config1"])
-    p.add_argument("--n", type=int, default=N_WORKERS)
+    p.add_argument("--workers", dest="n", type=int, default=N_WORKERS)  # (--n clashes with torchrun)
     p.add_argument("--group-size", type=int, default=GROUP_SIZE)
     p.add_argument("--mode", default="param", choices=["param", "grad"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--p2p-variant", type=int, default=-1)
+    p.add_argument("--discard", type=int, default=1)
+    p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot"])
     return p.parse_args()
 
 
@@ -225,7 +228,10 @@ def run_sesgd(args):
     buckets = list(WORKLOADS[args.workload])
     L = sum(buckets)
     mode = C.MODE_PARAM_AVG if args.mode == "param" else C.MODE_GRAD_AVG
-    eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world)
+    eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world,
+                      p2p_variant=args.p2p_variant, discard=args.discard,
+                      path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT,
+                            "oneshot": C.PATH_ONESHOT}[args.path])
     r = eng.r
     stream = torch.cuda.current_stream(dev)
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
@@ -280,7 +286,8 @@ def run_sesgd(args):
     # dominant kernel roofline (all timed launches are the one fused kernel)
     hbm_peak, peak_src = measured_peaks()
     algo_bytes_per_step_gpu = BYTES_PER_WORKER_ELEM * L * r
-    if world == 1:
+    resident = (world == 1 and args.path != "oneshot")
+    if resident:
         kernel = "k6_resident"
         achieved = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -288,15 +295,28 @@ def run_sesgd(args):
                 "algo_bytes_per_launch": [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets],
                 "kernel": kernel}
     else:
-        kernel = "k3_oneshot"
-        # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction
-        s_span = min(m, world)  # groups of m workers, 1 per GPU when r == 1
-        nvl_bytes = 2 * (s_span - 1) / s_span * 4 * L * r if s_span > 1 else 0.0
+        kernel = "k3_push"
+        # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
+        # actual schedule of the timed iterations: a group spanning s GPUs costs every one
+        # of them 2(s-1)/s * 4 B per element (co-resident members pre-combine); max over
+        # GPUs, mean over the timed iterations.
+        worker_rank = [i // r for i in range(n)]
+        nvl_steps = []
+        for t in range(t_next - K, t_next):
+            perm, _ = eng.groups(t)
+            per_gpu_b = [0.0] * world
+            for j in range(n // m):
+                ranks = {worker_rank[int(w)] for w in perm[j * m:(j + 1) * m]}
+                s_span = len(ranks)
+                for rk in ranks:
+                    per_gpu_b[rk] += 2 * (s_span - 1) / s_span * 4 * L
+            nvl_steps.append(max(per_gpu_b))
+        nvl_bytes = sum(nvl_steps) / len(nvl_steps)
         achieved_nvl = nvl_bytes * K / (kern_ms_total * 1e-3) / 1e9
         achieved_hbm = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
         t_hbm = algo_bytes_per_step_gpu / (hbm_peak * 1e9)
         t_nvl = nvl_bytes / (NVLINK_PEER_GBS * 1e9)
-        if t_nvl >= t_hbm:
+        if t_nvl >= t_hbm and nvl_bytes > 0:
             roof = {"bound": "nvlink", "achieved": achieved_nvl, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                     "frac": achieved_nvl / NVLINK_PEER_GBS,
                     "peak_source": "measured peer copy per direction, B200_PROFILING.md (nominal 900)"}
@@ -351,7 +371,7 @@ def run_sesgd(args):
                              f"({nb} buckets, {L:,} fp32 per worker), {args.mode.upper()} mode, "
                              f"lr {LR}, momentum {MU}; {r} worker(s) resident per GPU"),
                 "n": n, "group_size": m, "workers_per_gpu": r,
-                "path": "resident (K6)" if world == 1 else "one-shot NVLink P2P (K3)",
+                "path": "resident (K6)" if resident else "one-shot push over NVLink P2P (K3)",
                 "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush",
                 "parallelism": f"sesgd groups over {world} GPU(s)",
             },

@@ -69,6 +69,18 @@ extern "C" {
 #define SESGD_OPT_TIMEOUT_MS 3 /* flag-wait timeout before SESGD_ETIMEOUT        (default 20000) */
 #define SESGD_OPT_GRID 4       /* CTAs per launch, 0 = auto (SM count x occupancy) */
 #define SESGD_OPT_HOP_DELAY_NS 5 /* injected delay before every flag store (latency sweep) */
+#define SESGD_OPT_P2P_VARIANT 6  /* one-shot kernel: CTAs dedicated to NVLink pushes (1..148,
+                                    default 32; the other CTAs stream HBM); fixed once peers
+                                    attach (it sets the workspace layout) */
+#define SESGD_OPT_DISCARD 7      /* 1 (default): drop consumed receive lines from L2 without
+                                    write-back (discard.global.L2); 0: leave them to be evicted */
+#define SESGD_OPT_PROFILE 8      /* 1: the one-shot kernel accumulates per-CTA phase times
+                                    (%globaltimer ns) readable with sesgd_profile_read; 0 (default) */
+#define SESGD_OPT_COMM_BATCH 9   /* chunks (16 KiB each) a COMM CTA pushes per flag release:
+                                    amortises the system-scope release (default 16); fixed once
+                                    peers attach */
+#define SESGD_OPT_FOLD_LAG 10    /* chunk steps a COMPUTE CTA stages ahead of its fold (1..64,
+                                    default 4): covers the push + release latency */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {
@@ -180,6 +192,31 @@ SESGD_API int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats 
 
 /* Number of SMs and CTAs per launch the library uses on the attached device (0 before attach). */
 SESGD_API int sesgd_launch_grid(const sesgd_ctx *ctx, int32_t *ctas_out);
+
+/* Copy and reset the one-shot kernel's per-CTA phase timers (SESGD_OPT_PROFILE = 1).
+ * out[words] receives up to grid*8 u64: for CTA j, words [8j, 8j+8).  COMM CTAs (j <
+ * *comm_ctas_out): 0 waiting for staged chunks, 1 pushing, 2 releasing flags, 3 total,
+ * 7 launches.  COMPUTE CTAs: 0 staging, 1 folding (incl. waits), 2 total, 7 launches.
+ * Errors: SESGD_EINVAL, SESGD_ESTATE (nothing recorded), SESGD_ECUDA. */
+SESGD_API int sesgd_profile_read(sesgd_ctx *ctx, uint64_t *out, int64_t words, int32_t *comm_ctas_out);
+
+/* ---- K7 probes (diagnostics; not part of an iteration) ---- */
+
+/* Streaming 128-bit copy of `bytes` (multiple of 16, 16-byte aligned pointers) from `src` to
+ * `dst`, any device-visible addresses: local->local (HBM), peer->local (NVLink pull) or
+ * local->peer (NVLink push).  `ctas` CTAs of 512 threads, enqueued on `stream`; the caller
+ * times it (bandwidth bound of the exchange, row a5).  Errors: SESGD_EINVAL, SESGD_ECUDA. */
+SESGD_API int sesgd_probe_copy(void *dst, const void *src, int64_t bytes, int32_t ctas, void *stream);
+
+/* Flag ping-pong between two GPUs (per-hop handshake latency t_tau of Eq. 2).
+ * Both ranks launch it concurrently on peer-mapped u64 flags: my_flag (local), peer_flag
+ * (the other rank's my_flag).  The initiator stores base+2i+1 and waits for base+2i+2; the
+ * responder mirrors it.  Writes the elapsed ns of `iters` round trips (or ~0 on a 10 s
+ * timeout) to the device word out_ns_device.  `base` must exceed every earlier value written
+ * to the flags.  Errors: SESGD_EINVAL, SESGD_ECUDA. */
+SESGD_API int sesgd_probe_pingpong(uint64_t *my_flag, uint64_t *peer_flag, int32_t iters,
+                                   int32_t initiator, uint64_t base, uint64_t *out_ns_device,
+                                   void *stream);
 
 SESGD_API const char *sesgd_strerror(int code);
 SESGD_API const char *sesgd_last_error(const sesgd_ctx *ctx);

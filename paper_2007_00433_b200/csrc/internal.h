@@ -40,41 +40,48 @@ cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_
 int resident_block_threads();
 int resident_occupancy(int mode, bool vec, int m);
 
-// K3: one-shot NVLink P2P group exchange (worker(s) on several GPUs).
+// K3: one-shot push over NVLink, SM-specialised (COMM CTAs + COMPUTE CTAs), see p2p.cu.
 struct P2PArgs {
   float *const *x;        // [r] local workers' buffers
   float *const *v;
   const float *const *g;
   char *ws[SESGD_MAX_RANKS];        // every rank's workspace, mapped here
   int64_t numel;                    // bucket elements
-  int64_t chunk;                    // elements per chunk (multiple of 4 * threads)
-  int64_t nchunks;
-  int64_t stage_off;                // byte offset of the stage area in a workspace
-  int64_t stage_slot_floats;        // floats of one (parity, slot) stage region
+  int64_t nchunks;                  // chunks of this bucket
+  int64_t total_chunks;             // chunks of all buckets (flag array stride)
+  int64_t chunk_base;               // first global chunk index of this bucket
+  int64_t stage_slot_floats;        // floats of one stage / receive region
   int64_t stage_bucket_off;         // float offset of this bucket inside a region
-  int64_t ready_off, done_off;      // byte offsets of the flag arrays
-  uint64_t epoch0;                  // epoch of (t, bucket, k=0)
-  uint64_t epoch_prev0;             // epoch of (t-2, bucket, k=0), 0 if t < 2
+  int64_t ready_off, sent_off, staged_off, done_off, stage_off, recv_off;  // byte offsets
+  uint64_t seq_epoch0;              // staged-flag epoch of chunk step k = 0 of this launch
+  int64_t call;                     // index of this sync_step call on this bucket (all ranks equal)
   uint64_t timeout_ns;
   uint64_t hop_delay_ns;
-  unsigned int *err_host;           // mapped host word (latched error)
+  unsigned long long *err_host;     // mapped host block: [code, kind, cta, seen, target, worker, pos, rank]
   unsigned int *abort_dev;          // device word: set on timeout, skips further waits
+  uint64_t *prof;                   // optional per-CTA phase timers [grid][8] (SESGD_OPT_PROFILE)
   float lr, mu;
   int n, m, r, grid;
-  int parity;
+  int comm_ctas, comm_batch;        // COMM CTAs (blockIdx < comm_ctas) and chunks per release
+  int lag;                          // COMPUTE folds chunk step k - lag after staging step k
+  int parity;                       // call & 1: receive slots / ready flags double buffer
   int my_rank;
+  int bucket, nbuckets;
+  int discard;                      // drop dead stage / receive lines from L2 (no write-back)
   int8_t my_workers[SESGD_MAX_WORKERS];      // global ids of local slots
+  int8_t my_pos[SESGD_MAX_WORKERS];          // position of each local slot in its group
   int8_t worker_rank[SESGD_MAX_WORKERS];
   int8_t worker_slot[SESGD_MAX_WORKERS];
-  int8_t canon[SESGD_MAX_WORKERS];           // iteration t
+  int8_t canon[SESGD_MAX_WORKERS];           // canonical groups of the iteration
   int8_t group_of[SESGD_MAX_WORKERS];
-  int8_t canon_prev[SESGD_MAX_WORKERS];      // iteration t-2 (valid if epoch_prev0)
-  int8_t group_of_prev[SESGD_MAX_WORKERS];
 };
-cudaError_t launch_p2p_oneshot(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
-int p2p_block_threads();
-int p2p_chunk_elems();
-int p2p_occupancy(int mode, bool vec);
+// variant = COMM CTAs per launch (1..148)
+cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec,
+                               cudaStream_t stream);
+bool p2p_variant_valid(int variant);
+int p2p_block_threads(int variant);
+int p2p_chunk_elems(int variant);
+int p2p_occupancy(int variant, int r, int mode, bool vec);
 
 }  // namespace sesgd
 
@@ -89,7 +96,8 @@ struct sesgd_bucket {
   std::vector<const float *> hg;
   sesgd_stats stats{};
   int64_t stage_bucket_off = 0;  // multi-GPU layout
-  int64_t nchunks = 0;
+  int64_t nchunks = 0, chunk_base = 0;
+  int64_t calls = 0;             // sync_step calls on this bucket (flag epochs, parity)
 };
 
 struct sesgd_ctx {
@@ -100,6 +108,10 @@ struct sesgd_ctx {
   int64_t timeout_ms = 20000;
   int64_t grid_opt = 0;
   int64_t hop_delay_ns = 0;
+  int p2p_variant = 32;  // COMM CTAs per launch (SESGD_OPT_P2P_VARIANT)
+  int comm_batch = 16;   // chunks per COMM release (SESGD_OPT_COMM_BATCH)
+  int fold_lag = 4;      // SESGD_OPT_FOLD_LAG
+  int discard = 1;      // SESGD_OPT_DISCARD
   // attach
   bool attached = false;
   int device = -1;
@@ -117,7 +129,9 @@ struct sesgd_ctx {
   int8_t worker_slot[SESGD_MAX_WORKERS];
   int grid = 0;
   int64_t chunk = 0, kmax = 0;
-  int64_t ws_bytes = 0, ready_off = 0, done_off = 0, stage_off = 0, stage_slot_floats = 0;
+  int64_t ws_bytes = 0, ready_off = 0, sent_off = 0, staged_off = 0, done_off = 0, stage_off = 0,
+          recv_off = 0, stage_slot_floats = 0, total_chunks = 0;
+  int64_t seq = 0;  // sync_step calls on all buckets so far (staged-flag epochs)
   uint64_t layout_hash = 0;
   // iteration
   bool iter_set = false;
@@ -125,8 +139,10 @@ struct sesgd_ctx {
   int32_t canon[SESGD_MAX_WORKERS], group_of[SESGD_MAX_WORKERS];
   int32_t canon_prev[SESGD_MAX_WORKERS], group_of_prev[SESGD_MAX_WORKERS];
   // errors
-  unsigned int *h_err = nullptr;  // pinned mapped
-  unsigned int *d_err = nullptr;  // device alias of h_err
+  unsigned long long *h_err = nullptr;  // pinned mapped error block (8 words)
+  unsigned long long *d_err = nullptr;  // device alias of h_err
   unsigned int *d_abort = nullptr;
+  uint64_t *d_prof = nullptr;     // SESGD_OPT_PROFILE timers
+  int profile = 0;
   std::string last_error;
 };

@@ -49,9 +49,14 @@ int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int check_latched(sesgd_ctx *ctx) {
-  if (ctx->h_err && *reinterpret_cast<volatile unsigned int *>(ctx->h_err) != 0)
-    return fail(ctx, SESGD_ETIMEOUT, "a group peer did not signal before the timeout");
-  return SESGD_OK;
+  volatile unsigned long long *e = ctx->h_err;
+  if (!e || e[0] == 0) return SESGD_OK;
+  char buf[256];
+  std::snprintf(buf, sizeof buf,
+                "a group peer did not signal before the timeout: rank %llu CTA %llu waited for "
+                "%s flag of worker %llu (position %lld): saw epoch %llu, needed %llu",
+                e[7], e[2], e[1] == 1 ? "consumed" : "ready", e[5], (long long)e[6], e[3], e[4]);
+  return fail(ctx, SESGD_ETIMEOUT, buf);
 }
 
 void free_bucket(sesgd_bucket &b) {
@@ -63,50 +68,61 @@ void free_bucket(sesgd_bucket &b) {
 }
 
 // ---- multi-GPU workspace layout (identical on every rank) ----
-//   [0, 256)            header: magic, layout hash
-//   [ready_off, ...)    u64 ready[r][grid][n]
-//   [done_off, ...)     u64 done [r][grid][n]
-//   [stage_off, ...)    f32 stage[2 parity][r slot][stage_slot_floats]
+//   [0, 256)          header: magic, layout hash
+//   [ready_off, ..)   u64 ready [2 parity][r slot][total_chunks][m position]  (written by peers)
+//   [sent_off, ..)    u64 sent  [r slot][total_chunks]          (local: COMM -> COMPUTE)
+//   [staged_off, ..)  u64 staged[r slot][compute CTAs]          (local: COMPUTE -> COMM)
+//   [done_off, ..)    u64 done  [r slot][NB]                    (read by peers: consumption)
+//   [stage_off, ..)   f32 stage [r slot][stage_slot_floats]     (own x_hat, L2-resident)
+//   [recv_off, ..)    f32 recv  [2 parity][r slot][m position][stage_slot_floats]
 void freeze_layout(sesgd_ctx *ctx) {
-  const int chunk = sesgd::p2p_chunk_elems();
-  int occ = sesgd::p2p_occupancy(SESGD_MODE_PARAM_AVG, true);
-  occ = std::min(occ, sesgd::p2p_occupancy(SESGD_MODE_GRAD_AVG, true));
-  occ = std::min(occ, sesgd::p2p_occupancy(SESGD_MODE_PARAM_AVG, false));
-  occ = std::min(occ, sesgd::p2p_occupancy(SESGD_MODE_GRAD_AVG, false));
-  int grid = ctx->sm_count * occ;  // every CTA co-resident: CTA j only waits on CTA j of peers
+  const int var = ctx->p2p_variant;
+  const int chunk = sesgd::p2p_chunk_elems(var);
+  const int r = ctx->n_local;
+  int occ = sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, true);
+  occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, true));
+  occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, false));
+  occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, false));
+  int grid = ctx->sm_count * occ;  // every CTA co-resident (COMM and COMPUTE wait on each other)
   if (ctx->grid_opt > 0 && ctx->grid_opt < grid) grid = int(ctx->grid_opt);
+  const int comm = std::min(var, std::max(1, grid / 2));
   ctx->grid = grid;
   ctx->chunk = chunk;
-  int64_t off = 0, kmax = 1;
+  const int gc = grid - comm;
+  int64_t off = 0, kmax = 1, chunks = 0;
   uint64_t h = 0xcbf29ce484222325ULL;
   h = fnv(h, uint64_t(ctx->n));
   h = fnv(h, uint64_t(ctx->m));
   h = fnv(h, uint64_t(ctx->n_local));
   h = fnv(h, uint64_t(grid));
   h = fnv(h, uint64_t(chunk));
+  h = fnv(h, uint64_t(comm));
+  h = fnv(h, uint64_t(ctx->comm_batch));
   for (size_t b = 0; b < ctx->buckets.size(); ++b) {
     sesgd_bucket &bk = ctx->buckets[b];
     bk.stage_bucket_off = off;
     bk.nchunks = (bk.numel + chunk - 1) / chunk;
-    kmax = std::max<int64_t>(kmax, (bk.nchunks + grid - 1) / grid);
+    bk.chunk_base = chunks;
+    chunks += bk.nchunks;
+    kmax = std::max<int64_t>(kmax, (bk.nchunks + gc - 1) / gc);
     off += round_up(bk.numel, 64);  // 256-byte aligned buckets
     h = fnv(h, uint64_t(b));
     h = fnv(h, uint64_t(bk.registered ? bk.numel : -1));
   }
+  ctx->p2p_variant = comm;
   ctx->kmax = kmax;
+  ctx->total_chunks = std::max<int64_t>(chunks, 1);
   ctx->stage_slot_floats = std::max<int64_t>(off, 64);
-  const int64_t flags = int64_t(ctx->n_local) * grid * ctx->n * 8;
+  const int64_t nb = int64_t(ctx->buckets.size());
   ctx->ready_off = 256;
-  ctx->done_off = round_up(ctx->ready_off + flags, 256);
-  ctx->stage_off = round_up(ctx->done_off + flags, 4096);
-  ctx->ws_bytes = ctx->stage_off + 2 * int64_t(ctx->n_local) * ctx->stage_slot_floats * 4;
+  ctx->sent_off = round_up(ctx->ready_off + 2 * int64_t(r) * ctx->total_chunks * ctx->m * 8, 256);
+  ctx->staged_off = round_up(ctx->sent_off + int64_t(r) * ctx->total_chunks * 8, 256);
+  ctx->done_off = round_up(ctx->staged_off + int64_t(r) * gc * 8, 256);
+  ctx->stage_off = round_up(ctx->done_off + int64_t(r) * nb * 8, 4096);
+  ctx->recv_off = ctx->stage_off + int64_t(r) * ctx->stage_slot_floats * 4;
+  ctx->ws_bytes = ctx->recv_off + 2 * int64_t(r) * ctx->m * ctx->stage_slot_floats * 4;
   ctx->layout_hash = h;
   ctx->layout_frozen = true;
-}
-
-uint64_t epoch_of(const sesgd_ctx *ctx, int64_t t, int bucket) {
-  const uint64_t nb = ctx->buckets.size();
-  return (uint64_t(t) * nb + uint64_t(bucket)) * uint64_t(ctx->kmax) + 1;
 }
 
 }  // namespace
@@ -151,6 +167,7 @@ void sesgd_destroy(sesgd_ctx *ctx) {
   for (auto &b : ctx->buckets) free_bucket(b);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->d_abort) cudaFree(ctx->d_abort);
+  if (ctx->d_prof) cudaFree(ctx->d_prof);
   delete ctx;
 }
 
@@ -191,6 +208,28 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "grid is fixed once peers attach");
       ctx->grid_opt = value;
       return SESGD_OK;
+    case SESGD_OPT_P2P_VARIANT:
+      if (!sesgd::p2p_variant_valid(int(value))) return fail(ctx, SESGD_EINVAL, "unknown P2P variant");
+      if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "variant is fixed once peers attach");
+      ctx->p2p_variant = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_COMM_BATCH:
+      if (value < 1 || value > 1024) return fail(ctx, SESGD_EINVAL, "comm batch must be in [1, 1024]");
+      if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "comm batch is fixed once peers attach");
+      ctx->comm_batch = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_FOLD_LAG:
+      if (value < 1 || value > 64) return fail(ctx, SESGD_EINVAL, "fold lag must be in [1, 64]");
+      ctx->fold_lag = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_PROFILE:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");
+      ctx->profile = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_DISCARD:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "discard must be 0 or 1");
+      ctx->discard = int(value);
+      return SESGD_OK;
     case SESGD_OPT_HOP_DELAY_NS:
       if (value < 0) return fail(ctx, SESGD_EINVAL, "delay must be >= 0");
       ctx->hop_delay_ns = value;
@@ -218,11 +257,11 @@ int sesgd_attach(sesgd_ctx *ctx, int32_t device, int32_t n_local, const int32_t 
   int sms = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaDeviceGetAttribute");
-  unsigned int *h = nullptr;
-  e = cudaHostAlloc(reinterpret_cast<void **>(&h), sizeof(unsigned int), cudaHostAllocMapped);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaHostAlloc(error word)");
-  *h = 0;
-  unsigned int *d = nullptr;
+  unsigned long long *h = nullptr;
+  e = cudaHostAlloc(reinterpret_cast<void **>(&h), 8 * sizeof(unsigned long long), cudaHostAllocMapped);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaHostAlloc(error block)");
+  std::memset(h, 0, 8 * sizeof(unsigned long long));
+  unsigned long long *d = nullptr;
   e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&d), h, 0);
   if (e != cudaSuccess) {
     cudaFreeHost(h);
@@ -412,7 +451,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     return SESGD_OK;
   }
 
-  // one-shot NVLink P2P
+  // one-shot push over NVLink P2P
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
   P2PArgs a{};
   a.x = b.d_x;
@@ -420,38 +459,60 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
   a.g = b.d_g;
   for (int r = 0; r < ctx->n_ranks; ++r) a.ws[r] = ctx->ws[r];
   a.numel = b.numel;
-  a.chunk = ctx->chunk;
   a.nchunks = b.nchunks;
-  a.stage_off = ctx->stage_off;
+  a.total_chunks = ctx->total_chunks;
+  a.chunk_base = b.chunk_base;
   a.stage_slot_floats = ctx->stage_slot_floats;
   a.stage_bucket_off = b.stage_bucket_off;
   a.ready_off = ctx->ready_off;
+  a.sent_off = ctx->sent_off;
+  a.staged_off = ctx->staged_off;
   a.done_off = ctx->done_off;
-  a.epoch0 = epoch_of(ctx, ctx->t, bucket);
-  a.epoch_prev0 = ctx->t >= 2 ? epoch_of(ctx, ctx->t - 2, bucket) : 0;
+  a.stage_off = ctx->stage_off;
+  a.recv_off = ctx->recv_off;
+  a.seq_epoch0 = uint64_t(ctx->seq) * uint64_t(ctx->kmax) + 1;
+  a.call = b.calls;
   a.timeout_ns = uint64_t(ctx->timeout_ms) * 1000000ULL;
   a.hop_delay_ns = uint64_t(ctx->hop_delay_ns);
   a.err_host = ctx->d_err;
   a.abort_dev = ctx->d_abort;
+  if (ctx->profile && !ctx->d_prof) {
+    cudaError_t pe = cudaMalloc(reinterpret_cast<void **>(&ctx->d_prof), size_t(ctx->grid) * 64);
+    if (pe == cudaSuccess) pe = cudaMemset(ctx->d_prof, 0, size_t(ctx->grid) * 64);
+    if (pe != cudaSuccess) return cuda_fail(ctx, pe, "profile buffer");
+  }
+  a.prof = ctx->profile ? ctx->d_prof : nullptr;
   a.lr = lr;
   a.mu = momentum;
   a.n = ctx->n;
   a.m = ctx->m;
   a.r = ctx->n_local;
   a.grid = ctx->grid;
-  a.parity = int(ctx->t & 1);
+  a.comm_ctas = ctx->p2p_variant;
+  a.comm_batch = ctx->comm_batch;
+  a.lag = ctx->fold_lag;
+  a.parity = int(b.calls & 1);
   a.my_rank = ctx->rank;
-  for (int s = 0; s < ctx->n_local; ++s) a.my_workers[s] = int8_t(ctx->local_workers[s]);
+  a.bucket = bucket;
+  a.nbuckets = int(ctx->buckets.size());
+  a.discard = ctx->discard;
+  for (int s = 0; s < ctx->n_local; ++s) {
+    const int me = ctx->local_workers[s];
+    a.my_workers[s] = int8_t(me);
+    const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
+    for (int p = 0; p < ctx->m; ++p)
+      if (G[p] == me) a.my_pos[s] = int8_t(p);
+  }
   for (int i = 0; i < ctx->n; ++i) {
     a.worker_rank[i] = ctx->worker_rank[i];
     a.worker_slot[i] = ctx->worker_slot[i];
     a.canon[i] = int8_t(ctx->canon[i]);
     a.group_of[i] = int8_t(ctx->group_of[i]);
-    a.canon_prev[i] = int8_t(ctx->t >= 2 ? ctx->canon_prev[i] : 0);
-    a.group_of_prev[i] = int8_t(ctx->t >= 2 ? ctx->group_of_prev[i] : 0);
   }
-  cudaError_t e = sesgd::launch_p2p_oneshot(a, ctx->mode, b.vec, st);
+  cudaError_t e = sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, b.vec, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "launch one-shot kernel");
+  b.calls++;
+  ctx->seq++;
   b.stats.kernel_launches++;
   b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n_local;
   if (ctx->m > 1) {
@@ -463,7 +524,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
       for (int r = 0; r < ctx->m; ++r)
         if (G[r] != me && ctx->worker_rank[G[r]] != ctx->rank) remote_peers++;
     }
-    b.stats.flag_messages += 2 * int64_t(remote_peers) * b.nchunks;  // ready + done per chunk
+    b.stats.flag_messages += int64_t(remote_peers) * b.nchunks;  // one ready flag per chunk
     b.stats.payload_bytes_in += int64_t(remote_peers) * b.numel * 4;
   }
   return SESGD_OK;
@@ -501,6 +562,17 @@ int sesgd_poll(sesgd_ctx *ctx) {
 int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats *out) {
   if (!ctx || !out || bucket < 0 || size_t(bucket) >= ctx->buckets.size()) return SESGD_EINVAL;
   *out = ctx->buckets[bucket].stats;
+  return SESGD_OK;
+}
+
+int sesgd_profile_read(sesgd_ctx *ctx, uint64_t *out, int64_t words, int32_t *comm_ctas_out) {
+  if (!ctx || !out || words < 0) return SESGD_EINVAL;
+  if (!ctx->d_prof) return fail(ctx, SESGD_ESTATE, "no profile recorded (SESGD_OPT_PROFILE, multi-GPU path)");
+  const int64_t n = std::min<int64_t>(words, int64_t(ctx->grid) * 8);
+  cudaError_t e = cudaMemcpy(out, ctx->d_prof, size_t(n) * 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_prof, 0, size_t(ctx->grid) * 64);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "profile read");
+  if (comm_ctas_out) *comm_ctas_out = ctx->p2p_variant;
   return SESGD_OK;
 }
 

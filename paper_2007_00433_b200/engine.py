@@ -29,7 +29,8 @@ class SESGDEngine:
     def __init__(self, n: int, group_size: int, bucket_sizes: Sequence[int], *, seed: int = 42,
                  device: Optional[int] = None, mode: int = C.MODE_PARAM_AVG,
                  rank: int = 0, world: int = 1, process_group=None, path: int = C.PATH_AUTO,
-                 grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0):
+                 grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0,
+                 p2p_variant: int = -1, discard: int = 1, options: Optional[dict] = None):
         if n % world != 0:
             raise ValueError("n must be a multiple of the number of ranks")
         self.n, self.m, self.seed = n, group_size, seed
@@ -46,6 +47,11 @@ class SESGDEngine:
         C.sesgd_set_option(self.ctx, C.OPT_HOP_DELAY_NS, hop_delay_ns)
         if grid:
             C.sesgd_set_option(self.ctx, C.OPT_GRID, grid)
+        if p2p_variant >= 0:
+            C.sesgd_set_option(self.ctx, C.OPT_P2P_VARIANT, p2p_variant)
+        C.sesgd_set_option(self.ctx, C.OPT_DISCARD, discard)
+        for opt, val in (options or {}).items():  # extra SESGD_OPT_* (before the layout freezes)
+            C.sesgd_set_option(self.ctx, opt, val)
         C.sesgd_attach(self.ctx, self.device.index, self.local_workers)
 
         self.offsets, total = _aligned_offsets(self.bucket_sizes)
@@ -61,6 +67,12 @@ class SESGDEngine:
         self.workspace = None
         if world > 1:
             self._attach_peers(process_group)
+        elif path == C.PATH_ONESHOT:
+            # single GPU through the one-shot kernel (profiling / tests): a private workspace
+            nbytes = C.sesgd_workspace_bytes(self.ctx)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            C.sesgd_workspace_prepare(self.ctx, self.workspace.data_ptr())
+            C.sesgd_attach_peers(self.ctx, 1, 0, [self.workspace.data_ptr()], self.worker_rank)
 
     # -------------------------------------------------------------- multi-GPU
     def _attach_peers(self, process_group):

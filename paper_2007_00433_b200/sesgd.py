@@ -18,7 +18,9 @@ OK, EINVAL, ENOTDIV, ESTATE, ECUDA, ETIMEOUT, ENOMEM, ENOTSUP = 0, -1, -2, -3, -
 MAX_WORKERS, MAX_RANKS = 64, 8
 MODE_PARAM_AVG, MODE_GRAD_AVG = 0, 1
 PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT = 0, 1, 2
-OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS = 1, 2, 3, 4, 5
+OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS, OPT_P2P_VARIANT, OPT_DISCARD = (
+    1, 2, 3, 4, 5, 6, 7)
+OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG = 8, 9, 10
 
 # every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
 EXPORTED = (
@@ -26,6 +28,7 @@ EXPORTED = (
     "sesgd_attach", "sesgd_register_bucket", "sesgd_workspace_bytes", "sesgd_workspace_prepare",
     "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
+    "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read",
 )
 
 
@@ -76,6 +79,9 @@ def lib():
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
             "sesgd_strerror": ([ctypes.c_int], ctypes.c_char_p),
             "sesgd_last_error": ([P], ctypes.c_char_p),
+            "sesgd_probe_copy": ([P, P, i64, i32, P], ctypes.c_int),
+            "sesgd_profile_read": ([P, P, i64, ctypes.POINTER(i32)], ctypes.c_int),
+            "sesgd_probe_pingpong": ([P, P, i32, i32, u64, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -174,6 +180,27 @@ def sesgd_get_stats(ctx, bucket: int) -> dict:
     out = sesgd_stats()
     _check(lib().sesgd_get_stats(ctx, bucket, ctypes.byref(out)), ctx)
     return {f: getattr(out, f) for f, _ in sesgd_stats._fields_}
+
+
+def sesgd_probe_copy(dst: int, src: int, nbytes: int, ctas: int, stream: int = 0) -> None:
+    _check(lib().sesgd_probe_copy(ctypes.c_void_p(int(dst)), ctypes.c_void_p(int(src)), nbytes, ctas,
+                                  ctypes.c_void_p(int(stream))))
+
+
+def sesgd_probe_pingpong(my_flag: int, peer_flag: int, iters: int, initiator: bool, base: int,
+                         out_ns_dev: int, stream: int = 0) -> None:
+    _check(lib().sesgd_probe_pingpong(ctypes.c_void_p(int(my_flag)), ctypes.c_void_p(int(peer_flag)),
+                                      iters, int(bool(initiator)), base,
+                                      ctypes.c_void_p(int(out_ns_dev)), ctypes.c_void_p(int(stream))))
+
+
+def sesgd_profile_read(ctx, grid: int):
+    """-> (timers uint64[grid, 8], comm_ctas); see include/sesgd.h."""
+    out = np.zeros((grid, 8), np.uint64)
+    comm = ctypes.c_int32()
+    _check(lib().sesgd_profile_read(ctx, out.ctypes.data_as(ctypes.c_void_p), out.size,
+                                    ctypes.byref(comm)), ctx)
+    return out, comm.value
 
 
 def sesgd_launch_grid(ctx) -> int:

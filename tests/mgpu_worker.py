@@ -25,6 +25,7 @@ def main():
     p.add_argument("--mode", type=int, default=0)
     p.add_argument("--t0", type=int, default=0)
     p.add_argument("--grid", type=int, default=0)
+    p.add_argument("--variant", type=int, default=-1)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -35,7 +36,7 @@ def main():
     buckets = [int(b) for b in a.buckets.split(",")]
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
-                      grid=a.grid, timeout_ms=10000)
+                      grid=a.grid, timeout_ms=10000, p2p_variant=a.variant)
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):

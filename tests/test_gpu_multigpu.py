@@ -28,16 +28,19 @@ def _free_port():
     return p
 
 
-def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0):
+def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "tests", "mgpu_worker.py"), "--workers", str(n), "--gsize", str(m), "--iters", str(T),
-           "--buckets", ",".join(map(str, buckets)), "--mode", str(mode), "--t0", str(t0),
-           "--grid", str(grid), "--out", out]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    for _attempt in range(3):  # the rendezvous port can be taken between probe and bind
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+               os.path.join(ROOT, "tests", "mgpu_worker.py"), "--workers", str(n), "--gsize", str(m),
+               "--iters", str(T), "--buckets", ",".join(map(str, buckets)), "--mode", str(mode),
+               "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--out", out]
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        if "EADDRINUSE" not in res.stderr:
+            break
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     X = np.zeros((n, sum(buckets)), np.float32)
     V = np.zeros_like(X)
@@ -88,6 +91,17 @@ def test_two_gpus_small_grid_many_chunks(tmp_path):
     X, V = _launch(tmp_path, 2, 4, 2, 5, buckets, grid=8)
     x, v = _oracle(4, 2, sum(buckets), 5, 0)
     _compare(X, x)
+
+
+@pytest.mark.parametrize("variant", [1, 8, 32, 64])
+def test_two_gpus_kernel_variants(tmp_path, variant):
+    """Every one-shot kernel shape (threads per CTA x lookahead) gives the oracle's bits,
+    with a small grid so each CTA pipelines several chunks."""
+    buckets = [250001, 13]
+    X, V = _launch(tmp_path, 2, 4, 2, 5, buckets, grid=20, variant=variant)
+    x, v = _oracle(4, 2, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
 
 
 def test_four_gpus(tmp_path):
