@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--p2p-variant", type=int, default=-1)
     p.add_argument("--discard", type=int, default=1)
     p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot"])
+    p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
+    p.add_argument("--comm-batch", type=int, default=0)
+    p.add_argument("--fold-lag", type=int, default=0)
     return p.parse_args()
 
 
@@ -230,6 +233,8 @@ def run_sesgd(args):
     mode = C.MODE_PARAM_AVG if args.mode == "param" else C.MODE_GRAD_AVG
     eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world,
                       p2p_variant=args.p2p_variant, discard=args.discard,
+                      options={k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch),
+                                                 (C.OPT_FOLD_LAG, args.fold_lag)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT,
                             "oneshot": C.PATH_ONESHOT}[args.path])
     r = eng.r
@@ -254,31 +259,39 @@ def run_sesgd(args):
         return float(t.item())
 
     nb = len(buckets)
+    # one-shot path: one fused launch per step (sesgd_sync_all); resident: one launch per bucket
+    fused = (world > 1 or args.path == "oneshot") and args.fused
+    launches_per_step = 1 if fused else nb
     t_next = 0
     for _ in range(args.warmup):
-        eng.step(t_next, LR, MU, stream)
+        eng.step(t_next, LR, MU, stream, fused=fused)
         t_next += 1
     eng.poll()
     K = args.steps
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nb)]
-          for _ in range(K)]
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(launches_per_step)] for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(local) as clk:
         start.record(stream)
         for k in range(K):
             eng.begin_iter(t_next)
-            for b in range(nb):
-                ev[k][b][0].record(stream)
-                eng.sync_step(b, LR, MU, stream)
-                ev[k][b][1].record(stream)
+            if fused:
+                ev[k][0][0].record(stream)
+                eng.sync_all(LR, MU, stream)
+                ev[k][0][1].record(stream)
+            else:
+                for b in range(nb):
+                    ev[k][b][0].record(stream)
+                    eng.sync_step(b, LR, MU, stream)
+                    ev[k][b][1].record(stream)
             t_next += 1
         end.record(stream)
         barrier()
     eng.poll()
     ms_total = max_over_ranks(start.elapsed_time(end))
     ms_step = ms_total / K
-    launch_ms = [[ev[k][b][0].elapsed_time(ev[k][b][1]) for b in range(nb)] for k in range(K)]
+    launch_ms = [[e0.elapsed_time(e1) for (e0, e1) in ev[k]] for k in range(K)]
     kern_ms_total = max_over_ranks(sum(map(sum, launch_ms)))
     total_bytes = BYTES_PER_WORKER_ELEM * L * n  # whole job, per step
     value = total_bytes / (ms_step * 1e-3) / 1e9
@@ -380,7 +393,7 @@ def run_sesgd(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * nb,
+            "gpu_launches": K * launches_per_step,
             "clocks": clocks,
             "handshakes": {
                 "sesgd_per_tensor": lat["sesgd_handshakes"], "ring_per_tensor": lat["ring_handshakes"],

@@ -69,9 +69,10 @@ extern "C" {
 #define SESGD_OPT_TIMEOUT_MS 3 /* flag-wait timeout before SESGD_ETIMEOUT        (default 20000) */
 #define SESGD_OPT_GRID 4       /* CTAs per launch, 0 = auto (SM count x occupancy) */
 #define SESGD_OPT_HOP_DELAY_NS 5 /* injected delay before every flag store (latency sweep) */
-#define SESGD_OPT_P2P_VARIANT 6  /* one-shot kernel: CTAs dedicated to NVLink pushes (1..148,
-                                    default 32; the other CTAs stream HBM); fixed once peers
-                                    attach (it sets the workspace layout) */
+#define SESGD_OPT_P2P_VARIANT 6  /* one-shot kernel shape: 0 (default) = every CTA pushes its own
+                                    x_hat to remote members from registers; 1..148 = that many
+                                    CTAs dedicated to NVLink pushes out of an L2 stage while the
+                                    others stream HBM; fixed once peers attach (sets the layout) */
 #define SESGD_OPT_DISCARD 7      /* 1 (default): drop consumed receive lines from L2 without
                                     write-back (discard.global.L2); 0: leave them to be evicted */
 #define SESGD_OPT_PROFILE 8      /* 1: the one-shot kernel accumulates per-CTA phase times
@@ -177,6 +178,14 @@ SESGD_API int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter);
  *         (begin_iter not called, peers not attached on multi-GPU), SESGD_ECUDA, SESGD_ETIMEOUT. */
 SESGD_API int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, void *stream);
 
+/* sesgd_sync_step for EVERY registered bucket of the current iteration.  On the multi-GPU
+ * one-shot path, when all buckets share their call history (always the case if they are only
+ * ever synced together), this is ONE fused launch over all buckets' chunks: the NVLink / HBM
+ * pipeline fills and drains once per iteration instead of once per bucket.  Otherwise (and on
+ * the resident path) it enqueues one launch per bucket in id order.  Asynchronous on `stream`.
+ * Errors: as sesgd_sync_step; SESGD_ESTATE if no bucket is registered. */
+SESGD_API int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream);
+
 /* End-to-end variant through HOST buffers: for each local worker, copies g_host[w] (numel
  * floats, pinned for overlap) to the registered device gradient, runs sesgd_sync_step, and
  * copies the updated device parameters back into x_host_out[w].  Asynchronous on `stream`
@@ -204,7 +213,8 @@ SESGD_API int sesgd_profile_read(sesgd_ctx *ctx, uint64_t *out, int64_t words, i
 
 /* Streaming 128-bit copy of `bytes` (multiple of 16, 16-byte aligned pointers) from `src` to
  * `dst`, any device-visible addresses: local->local (HBM), peer->local (NVLink pull) or
- * local->peer (NVLink push).  `ctas` CTAs of 512 threads, enqueued on `stream`; the caller
+ * local->peer (NVLink push).  `ctas` CTAs (low 16 bits) of 512 threads (or, if bits 16..21
+ * are non-zero, that many warps per CTA), enqueued on `stream`; the caller
  * times it (bandwidth bound of the exchange, row a5).  Errors: SESGD_EINVAL, SESGD_ECUDA. */
 SESGD_API int sesgd_probe_copy(void *dst, const void *src, int64_t bytes, int32_t ctas, void *stream);
 

@@ -41,20 +41,25 @@ int resident_block_threads();
 int resident_occupancy(int mode, bool vec, int m);
 
 // K3: one-shot push over NVLink, SM-specialised (COMM CTAs + COMPUTE CTAs), see p2p.cu.
+struct BucketMeta {
+  int64_t numel;       // elements
+  int64_t stage_off;   // float offset inside a stage / receive region
+  int64_t chunk_base;  // first global chunk index
+  int64_t nchunks;
+};
 struct P2PArgs {
-  float *const *x;        // [r] local workers' buffers
-  float *const *v;
-  const float *const *g;
+  const BucketMeta *meta;           // [NB] device table
+  float *const *bx;                 // [NB * r] device tables: bucket b, local slot s -> b*r + s
+  float *const *bv;
+  const float *const *bg;
   char *ws[SESGD_MAX_RANKS];        // every rank's workspace, mapped here
-  int64_t numel;                    // bucket elements
-  int64_t nchunks;                  // chunks of this bucket
+  int64_t g0, g1;                   // global chunk range of this launch
   int64_t total_chunks;             // chunks of all buckets (flag array stride)
-  int64_t chunk_base;               // first global chunk index of this bucket
-  int64_t stage_slot_floats;        // floats of one stage / receive region
-  int64_t stage_bucket_off;         // float offset of this bucket inside a region
-  int64_t ready_off, sent_off, staged_off, done_off, stage_off, recv_off;  // byte offsets
-  uint64_t seq_epoch0;              // staged-flag epoch of chunk step k = 0 of this launch
-  int64_t call;                     // index of this sync_step call on this bucket (all ranks equal)
+  int64_t region_floats;            // floats of one stage / receive region (all buckets)
+  int64_t ready_off, sent_off, staged_off, consumed_off, stage_off, recv_off;  // byte offsets
+  uint64_t seq_epoch0;              // S(seq, g) = seq_epoch0 + g / Gc for this launch
+  uint64_t prev2_epoch0;            // the same for the launch that made call - 2 (guard)
+  int64_t call;                     // call index of the bucket(s) (identical on every rank)
   uint64_t timeout_ns;
   uint64_t hop_delay_ns;
   unsigned long long *err_host;     // mapped host block: [code, kind, cta, seen, target, worker, pos, rank]
@@ -66,7 +71,7 @@ struct P2PArgs {
   int lag;                          // COMPUTE folds chunk step k - lag after staging step k
   int parity;                       // call & 1: receive slots / ready flags double buffer
   int my_rank;
-  int bucket, nbuckets;
+  int bucket, nbuckets;             // bucket of a single-bucket launch, -1 for all buckets
   int discard;                      // drop dead stage / receive lines from L2 (no write-back)
   int8_t my_workers[SESGD_MAX_WORKERS];      // global ids of local slots
   int8_t my_pos[SESGD_MAX_WORKERS];          // position of each local slot in its group
@@ -75,13 +80,15 @@ struct P2PArgs {
   int8_t canon[SESGD_MAX_WORKERS];           // canonical groups of the iteration
   int8_t group_of[SESGD_MAX_WORKERS];
 };
-// variant = COMM CTAs per launch (1..148)
-cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec,
+// variant = COMM CTAs per launch (1..148); smem = guard cache bytes
+cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec, size_t smem,
                                cudaStream_t stream);
 bool p2p_variant_valid(int variant);
 int p2p_block_threads(int variant);
 int p2p_chunk_elems(int variant);
-int p2p_occupancy(int variant, int r, int mode, bool vec);
+int p2p_guard_pairs_max();
+size_t p2p_smem_bytes(int variant, int guard_pairs, int grid);  // COMM ring + mbarriers + guard cache
+int p2p_occupancy(int variant, int r, int mode, bool vec, size_t smem);
 
 }  // namespace sesgd
 
@@ -98,6 +105,7 @@ struct sesgd_bucket {
   int64_t stage_bucket_off = 0;  // multi-GPU layout
   int64_t nchunks = 0, chunk_base = 0;
   int64_t calls = 0;             // sync_step calls on this bucket (flag epochs, parity)
+  int64_t seq_hist[2] = {0, 0};  // launch sequence numbers of the last two calls (by call parity)
 };
 
 struct sesgd_ctx {
@@ -108,7 +116,7 @@ struct sesgd_ctx {
   int64_t timeout_ms = 20000;
   int64_t grid_opt = 0;
   int64_t hop_delay_ns = 0;
-  int p2p_variant = 32;  // COMM CTAs per launch (SESGD_OPT_P2P_VARIANT)
+  int p2p_variant = 0;   // SESGD_OPT_P2P_VARIANT: 0 = DIRECT push, n = n COMM CTAs
   int comm_batch = 16;   // chunks per COMM release (SESGD_OPT_COMM_BATCH)
   int fold_lag = 4;      // SESGD_OPT_FOLD_LAG
   int discard = 1;      // SESGD_OPT_DISCARD
@@ -129,9 +137,13 @@ struct sesgd_ctx {
   int8_t worker_slot[SESGD_MAX_WORKERS];
   int grid = 0;
   int64_t chunk = 0, kmax = 0;
-  int64_t ws_bytes = 0, ready_off = 0, sent_off = 0, staged_off = 0, done_off = 0, stage_off = 0,
-          recv_off = 0, stage_slot_floats = 0, total_chunks = 0;
-  int64_t seq = 0;  // sync_step calls on all buckets so far (staged-flag epochs)
+  int64_t ws_bytes = 0, ready_off = 0, sent_off = 0, staged_off = 0, consumed_off = 0,
+          stage_off = 0, recv_off = 0, stage_slot_floats = 0, total_chunks = 0;
+  int64_t seq = 0;  // one-shot launches so far (staged / consumed epochs)
+  size_t guard_smem = 0;
+  sesgd::BucketMeta *d_meta = nullptr;  // device bucket tables (multi-GPU path)
+  float **d_bx = nullptr, **d_bv = nullptr;
+  const float **d_bg = nullptr;
   uint64_t layout_hash = 0;
   // iteration
   bool iter_set = false;

@@ -1,6 +1,7 @@
 // p2p.cu -- K3: fused local update + ONE-SHOT PUSH intra-group exchange over NVLink,
 // SM-specialised: a few COMM CTAs move data over NVLink while the COMPUTE CTAs
-// stream HBM, in one persistent kernel per bucket.
+// stream HBM, in one persistent kernel over a range of chunks (one bucket, or every
+// bucket of the iteration at once with sesgd_sync_all).
 //
 // Each iteration every group G = {a_0 < ... < a_{m-1}} of the shuffle-exchange
 // partition (A1) averages its members' locally-stepped parameters (Eq. 6,
@@ -8,33 +9,39 @@
 // Ethernet is prior art: on NVSwitch every peer is one hop at full bandwidth, so one
 // handshake round suffices (instead of the ring's 2(m-1)).
 //
-// Why this shape (measured on B200, profiles/r01_nvlink_probe_2gpu*.json):
+// Why this shape (measured on B200; profiles/r01_nvlink_probe_2gpu*.json,
+// profiles/r01_k3_phases*.json):
 //  * remote loads hold an SM's request slots for ~2.5 us and starve a local HBM
 //    stream; remote STORES do not, and both-direction push keeps 705 GB/s/dir;
-//  * 32 CTAs of pushes already reach 698 GB/s/dir and leave the other SMs free to
-//    stream HBM concurrently (805 us vs 956 us serial); pushing from >= 64 CTAs
-//    starves the local stream;
-//  * a system-scope release stalls its warp until the CTA's remote stores drain,
-//    so releases are batched (one per COMM batch of chunks).
+//  * 32 CTAs of pushes reach 698 GB/s/dir and leave the other SMs free to stream
+//    HBM concurrently; pushing from >= 64 CTAs starves the local stream;
+//  * a system-scope release stalls until the CTA's remote stores drain, so flags
+//    are released once per COMM batch of chunks;
+//  * every launch pays a pipeline fill and drain, so one launch covers as many
+//    chunks as possible (all buckets of the iteration with sesgd_sync_all).
 //
-// Roles (blockIdx < Q: COMM, else COMPUTE; all CTAs co-resident):
-//  COMPUTE CTA i, chunks c = i, i+Gc, ... (chunk = 4096 floats):
-//    stage(c):  load g, v, x ; v <- mu v + g ; x_hat <- x - lr v ; store v ;
-//               x_hat -> own stage (L2) ; st.release staged[s][i] = E(seq, k)
-//               (GRAD: g -> stage, v and x untouched)
-//    fold(c) two chunks later: wait sent[s][c] (own COMM pushed it) and every peer's
-//               ready[par][s][c][pos] ; fold the m contributions in ascending position
-//               (= ascending worker id; own from the stage) ; (/) m ; store x
-//               (GRAD: v, x update) ; discard the dead stage / receive lines from L2
-//    end:       red.release.sys done[s][b] += 1   (consumption counter for senders)
+// Chunks (4096 floats) are numbered globally over the concatenated buckets; a launch
+// covers [g0, g1).  Roles (blockIdx < Q: COMM, else COMPUTE; all CTAs co-resident):
+//  COMPUTE CTA i (i = g mod Gc for its chunks g):
+//    stage(g):  load g, v, x ; v <- mu v + g ; x_hat <- x - lr v ; store v ;
+//               x_hat -> own stage (L2) ; staged[s][i] = S(seq, g)
+//               (GRAD: g -> stage; v and x are updated at fold time)
+//    fold(g)  `lag` chunk steps later: wait sent[s][g] (own COMM pushed it) and the
+//               ready flags of remote members ; fold the m contributions in ascending
+//               position (= ascending worker id): own / co-resident members from
+//               their stages, remote members from the receive slots ; (/) m ; store x ;
+//               discard the dead lines from L2
+//    end:       consumed[s][i] = S(seq, last g)  (one system-scope release per launch)
 //  COMM CTA q, batches of B chunks (batch j = q, q+Q, ...):
-//    guard once per launch: every peer finished folding this bucket two calls ago
-//               (done counter, read over NVLink)
-//    wait staged for the batch ; copy own stage -> every peer's receive slot (NVLink
-//    stores) ; one st.release.sys per (chunk, peer) ready flag + local sent flags
-// All waits point to a strictly smaller chunk index (or an earlier step of the same
-// chunk), so the smallest unfinished step can always progress: no deadlock.  Flags
-// are keyed by the per-bucket call index (identical on every rank) and never reset.
+//    guard: every remote member consumed its receive slot of the call two back
+//               (consumed counters bulk-read once per launch into shared memory)
+//    wait staged ; copy own stage -> remote members' receive slots (NVLink stores) ;
+//    one st.release.sys per (chunk, remote member) ready flag ; sent flags
+// S(seq, g) = seq * KMAX + floor(g / Gc) + 1 is strictly increasing in every compute
+// CTA's processing order across launches; ready / sent flags hold the bucket's call
+// index + 1, with ready and receive slots double-buffered by call parity.  All waits
+// point to a strictly smaller chunk (or an earlier step of the same chunk), so the
+// smallest unfinished step can always progress: no deadlock.  Flags are never reset.
 // Every spin has a %globaltimer timeout that latches SESGD_ETIMEOUT.
 #include "common.cuh"
 #include "internal.h"
@@ -43,9 +50,11 @@ namespace sesgd {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kVec = 4;                                 // float4 items per thread per chunk
+constexpr int kVec = 4;                                   // float4 items per thread per chunk
 constexpr int64_t kChunk = int64_t(kThreads) * 4 * kVec;  // 4096 floats = 16 KiB
-// fold(c) runs a.lag chunk steps after stage(c) (SESGD_OPT_FOLD_LAG)
+constexpr int kMaxGuardPairs = 8;                         // (slot, remote member) pairs cached in smem
+constexpr int kRing = 3;                                  // COMM TMA ring: chunks in flight
+constexpr int kRingBytes = kRing * int(kChunk) * 4;       // 48 KiB
 
 // ---- element access with a per-component mask on the ragged last vector ----
 template <int W>
@@ -110,32 +119,24 @@ __device__ __forceinline__ void ld_slot(const float *p, float (&r)[W], int nvali
 __device__ __forceinline__ void discard_l2(const void *p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
-__device__ __forceinline__ void red_add_release_sys(uint64_t *p, uint64_t v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t *p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_release_gpu(uint64_t *p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // what a timed-out wait was waiting for (reported through sesgd_last_error)
-enum WaitKind : int { kWaitDone = 1, kWaitReady = 2, kWaitStaged = 3, kWaitSent = 4 };
+enum WaitKind : int { kWaitConsumed = 1, kWaitReady = 2, kWaitStaged = 3, kWaitSent = 4 };
 
 // spin until *p >= target (sys-scope acquire); on timeout the first CTA to give up
 // latches SESGD_ETIMEOUT plus a description of the flag in the host-mapped block
-__device__ bool wait_geq(const P2PArgs &a, const uint64_t *p, uint64_t target, int kind,
-                         int worker, int pos) {
+__device__ uint64_t wait_geq(const P2PArgs &a, const uint64_t *p, uint64_t target, int kind,
+                             int worker, int pos) {
   uint64_t v = dev::ld_acquire_sys(p);
-  if (v >= target) return true;
+  if (v >= target) return v;
   const uint64_t t0 = dev::globaltimer();
   for (;;) {
     v = dev::ld_acquire_sys(p);
-    if (v >= target) return true;
-    if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) return false;
+    if (v >= target) return v;
+    if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) return target;
     if (dev::globaltimer() - t0 > a.timeout_ns) {
       if (atomicExch(a.abort_dev, 1u) == 0u) {
         unsigned long long *e = a.err_host;
@@ -150,7 +151,7 @@ __device__ bool wait_geq(const P2PArgs &a, const uint64_t *p, uint64_t target, i
         atomicExch(e, (unsigned long long)(-SESGD_ETIMEOUT));
         __threadfence_system();
       }
-      return false;
+      return target;
     }
   }
 }
@@ -162,6 +163,12 @@ __device__ __forceinline__ void hop_delay(const P2PArgs &a) {
   }
 }
 
+struct ChunkRef {
+  int b;           // bucket
+  int64_t e0, e1;  // element range inside the bucket
+  int64_t soff;    // float offset of the bucket inside a stage / receive region
+};
+
 template <int W, bool GRAD>
 struct Split {
   static constexpr int kItems = int(kChunk / W) / kThreads;  // W-wide items per thread per chunk
@@ -170,108 +177,139 @@ struct Split {
   int gc;  // compute CTAs
   __device__ explicit Split(const P2PArgs &args) : a(args) { gc = a.grid - a.comm_ctas; }
 
+  // ---- chunk -> bucket ----
+  __device__ __forceinline__ ChunkRef locate(int64_t g) const {
+    int b = a.bucket;
+    if (b < 0) {  // multi-bucket launch: last bucket whose chunk_base <= g
+      int lo = 0, hi = a.nbuckets - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.meta[mid].chunk_base <= g) lo = mid; else hi = mid - 1;
+      }
+      b = lo;
+    }
+    const BucketMeta &mb = a.meta[b];
+    ChunkRef c;
+    c.b = b;
+    c.e0 = (g - mb.chunk_base) * kChunk;
+    c.e1 = min(c.e0 + kChunk, mb.numel);
+    c.soff = mb.stage_off;
+    return c;
+  }
+
   // ---- addressing (workspace layout: see sesgd_capi.cu freeze_layout) ----
   __device__ __forceinline__ const int8_t *group(int me) const {
     return a.canon + a.group_of[me] * a.m;
   }
-  __device__ __forceinline__ float *stage(int s) const {
-    return reinterpret_cast<float *>(a.ws[a.my_rank] + a.stage_off) + int64_t(s) * a.stage_slot_floats +
-           a.stage_bucket_off;
+  __device__ __forceinline__ bool remote(int w) const { return a.worker_rank[w] != a.my_rank; }
+  __device__ __forceinline__ float *stage(int slot) const {  // my rank's stage of a local slot
+    return reinterpret_cast<float *>(a.ws[a.my_rank] + a.stage_off) + int64_t(slot) * a.region_floats;
   }
-  __device__ __forceinline__ float *recv(int worker, int pos) const {
+  __device__ __forceinline__ float *recv(int worker, int pos) const {  // worker's receive slot
     char *base = a.ws[a.worker_rank[worker]] + a.recv_off;
     const int64_t region = (int64_t(a.parity) * a.r + a.worker_slot[worker]) * a.m + pos;
-    return reinterpret_cast<float *>(base) + region * a.stage_slot_floats + a.stage_bucket_off;
+    return reinterpret_cast<float *>(base) + region * a.region_floats;
   }
-  __device__ __forceinline__ uint64_t *ready(int worker, int64_t c, int pos) const {
+  __device__ __forceinline__ uint64_t *ready(int worker, int64_t g, int pos) const {
     uint64_t *f = reinterpret_cast<uint64_t *>(a.ws[a.worker_rank[worker]] + a.ready_off);
-    const int64_t row = (int64_t(a.parity) * a.r + a.worker_slot[worker]) * a.total_chunks +
-                        a.chunk_base + c;
-    return f + row * a.m + pos;
+    return f + ((int64_t(a.parity) * a.r + a.worker_slot[worker]) * a.total_chunks + g) * a.m + pos;
   }
-  __device__ __forceinline__ uint64_t *sent(int s, int64_t c) const {
-    return reinterpret_cast<uint64_t *>(a.ws[a.my_rank] + a.sent_off) + int64_t(s) * a.total_chunks +
-           a.chunk_base + c;
+  __device__ __forceinline__ uint64_t *sent(int s, int64_t g) const {
+    return reinterpret_cast<uint64_t *>(a.ws[a.my_rank] + a.sent_off) + int64_t(s) * a.total_chunks + g;
   }
   __device__ __forceinline__ uint64_t *staged(int s, int i) const {
     return reinterpret_cast<uint64_t *>(a.ws[a.my_rank] + a.staged_off) + int64_t(s) * gc + i;
   }
-  __device__ __forceinline__ uint64_t *done(int worker) const {
-    return reinterpret_cast<uint64_t *>(a.ws[a.worker_rank[worker]] + a.done_off) +
-           int64_t(a.worker_slot[worker]) * a.nbuckets + a.bucket;
+  __device__ __forceinline__ uint64_t *consumed(int worker, int i) const {
+    return reinterpret_cast<uint64_t *>(a.ws[a.worker_rank[worker]] + a.consumed_off) +
+           int64_t(a.worker_slot[worker]) * gc + i;
+  }
+  __device__ __forceinline__ uint64_t step_epoch(uint64_t base, int64_t g) const {
+    return base + uint64_t(g / gc);
+  }
+  // the pi-th (slot, remote member) pair of this rank's groups
+  __device__ __forceinline__ int remote_pair_member(int pi) const {
+    int seen = -1;
+    for (int p = 0; p < a.r * a.m; ++p) {
+      const int s = p / a.m, rr = p % a.m;
+      const int me = a.my_workers[s];
+      const int w = group(me)[rr];
+      if (w != me && remote(w) && ++seen == pi) return w;
+    }
+    return -1;
   }
 
   // ---------------------------------------------------------------- COMPUTE
-  __device__ void stage_chunk(int i, int64_t k) const {
-    const int64_t c = i + k * gc;
-    const int64_t e0 = c * kChunk, e1 = min(e0 + kChunk, a.numel);
+  __device__ void stage_chunk(int i, int64_t g) const {
+    const ChunkRef c = locate(g);
     for (int s = 0; s < a.r; ++s) {
-      float *xs = a.x[s], *vs = a.v[s];
-      const float *gs = a.g[s];
-      float *st = stage(s);
+      float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
+      const float *gs = a.bg[c.b * a.r + s];
+      float *st = stage(s) + c.soff;
 #pragma unroll
       for (int it = 0; it < kItems; ++it) {
-        const int64_t e = e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
-        const int nv = (int)min(int64_t(W), e1 - e);
+        const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+        const int nv = (int)min(int64_t(W), c.e1 - e);
         if (nv <= 0) continue;
-        float g[W];
-        load_m<W>(gs + e, g, nv);
+        float gr[W];
+        load_m<W>(gs + e, gr, nv);
         if constexpr (!GRAD) {
           float v[W], x[W];
           load_m<W>(vs + e, v, nv);
           load_m<W>(xs + e, x, nv);
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            v[w] = dev::momentum(a.mu, v[w], g[w]);
-            x[w] = dev::sgd(x[w], a.lr, v[w]);  // x_hat
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            x[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
           }
           store_m<W>(vs + e, v, nv);
           st_slot<W>(st + e, x, nv);
         } else {
-          st_slot<W>(st + e, g, nv);
+          st_slot<W>(st + e, gr, nv);
         }
       }
     }
-    __syncthreads();  // every stage store of chunk c precedes the release
-    if (threadIdx.x < a.r) st_release_gpu(staged(threadIdx.x, i), a.seq_epoch0 + uint64_t(k));
+    __syncthreads();  // every stage store of chunk g precedes the release
+    if (threadIdx.x < a.r) st_release_gpu(staged(threadIdx.x, i), step_epoch(a.seq_epoch0, g));
   }
 
-  __device__ void fold_chunk(int i, int64_t k) const {
-    const int64_t c = i + k * gc;
-    const int64_t e0 = c * kChunk, e1 = min(e0 + kChunk, a.numel);
-    const uint64_t call = a.call + 1;
-    // warp 0: my COMM pushed chunk c (stage no longer needed by it) and all peers' arrived
+  __device__ void fold_chunk(int i, int64_t g) const {
+    const ChunkRef c = locate(g);
+    const uint64_t call = uint64_t(a.call) + 1;
+    // warp 0: my COMM pushed chunk g of every slot, and every remote member's chunk arrived
     if (threadIdx.x < 32) {
       const int pairs = a.r * a.m;
       for (int p = threadIdx.x; p < pairs; p += 32) {
         const int s = p / a.m, rr = p % a.m;
         const int me = a.my_workers[s];
-        if (rr == a.my_pos[s])
-          wait_geq(a, sent(s, c), call, kWaitSent, me, rr);
-        else
-          wait_geq(a, ready(me, c, rr), call, kWaitReady, me, rr);
+        const int w = group(me)[rr];
+        if (w == me)
+          wait_geq(a, sent(s, g), call, kWaitSent, me, rr);
+        else if (remote(w))
+          wait_geq(a, ready(me, g, rr), call, kWaitReady, me, rr);
       }
     }
     __syncthreads();
     for (int s = 0; s < a.r; ++s) {
       const int me = a.my_workers[s];
-      const int mypos = a.my_pos[s];
-      float *xs = a.x[s], *vs = a.v[s];
-      const float *st = stage(s);
+      const int8_t *G = group(me);
+      float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
 #pragma unroll
       for (int it = 0; it < kItems; ++it) {
-        const int64_t e = e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
-        const int nv = (int)min(int64_t(W), e1 - e);
+        const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+        const int nv = (int)min(int64_t(W), c.e1 - e);
         if (nv <= 0) continue;
         float acc[W];
         for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
+          const int w = G[rr];
+          const float *src = remote(w) ? recv(me, rr) : stage(a.worker_slot[w]);
           float y[W];
-          ld_slot<W>((rr == mypos ? st : recv(me, rr)) + e, y, nv);
+          ld_slot<W>(src + c.soff + e, y, nv);
 #pragma unroll
-          for (int w = 0; w < W; ++w) acc[w] = (rr == 0) ? y[w] : __fadd_rn(acc[w], y[w]);
+          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
         }
 #pragma unroll
-        for (int w = 0; w < W; ++w) acc[w] = __fdiv_rn(acc[w], (float)a.m);
+        for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
         if constexpr (!GRAD) {
           store_m<W>(xs + e, acc, nv);
         } else {
@@ -279,52 +317,62 @@ struct Split {
           load_m<W>(vs + e, v, nv);
           load_m<W>(xs + e, x, nv);
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            v[w] = dev::momentum(a.mu, v[w], acc[w]);
-            x[w] = dev::sgd(x[w], a.lr, v[w]);
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], acc[q]);
+            x[q] = dev::sgd(x[q], a.lr, v[q]);
           }
           store_m<W>(vs + e, v, nv);
           store_m<W>(xs + e, x, nv);
         }
       }
-      // the stage and receive lines of this chunk are dead: drop them from L2 without
-      // write-back.  A 128-byte line is read by 8 consecutive lanes of one warp.
-      if constexpr (W == 4) {
-        if (a.discard) {
-          __syncwarp();
-          if ((threadIdx.x & 7) == 0) {
+    }
+    __syncthreads();  // every slot's fold has read the co-resident stages
+    // The stage and receive lines of chunk g are dead: drop them from L2 without
+    // write-back (a discard is a write, so it precedes the `consumed` release below).
+    if constexpr (W == 4) {
+      if (a.discard && (threadIdx.x & 7) == 0) {
+        for (int s = 0; s < a.r; ++s) {
+          const int me = a.my_workers[s];
+          const int8_t *G = group(me);
 #pragma unroll
-            for (int it = 0; it < kItems; ++it) {
-              const int64_t e = e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
-              if (e + 32 > e1) continue;
-              for (int rr = 0; rr < a.m; ++rr) discard_l2((rr == mypos ? st : recv(me, rr)) + e);
-            }
+          for (int it = 0; it < kItems; ++it) {
+            const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+            if (e + 32 > c.e1) continue;
+            discard_l2(stage(s) + c.soff + e);
+            for (int rr = 0; rr < a.m; ++rr)
+              if (remote(G[rr])) discard_l2(recv(me, rr) + c.soff + e);
           }
         }
       }
     }
+    __syncthreads();  // this chunk's reads and discards precede the next stage / final release
   }
 
   __device__ void compute(int i) const {
-    const int64_t nk = (a.nchunks > i) ? (a.nchunks - i + gc - 1) / gc : 0;
+    // my chunks: g = first, first + gc, ... in [g0, g1)
+    const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
+    const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
     uint64_t t_stage = 0, t_fold = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
     for (int64_t k = 0; k < nk + a.lag; ++k) {
-      if (k < nk) stage_chunk(i, k);
+      if (k < nk) stage_chunk(i, first + k * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_stage += t1 - t0;
         t0 = t1;
       }
-      if (k >= a.lag) {
-        fold_chunk(i, k - a.lag);
-        __syncthreads();  // the fold's reads are complete before the next stage / done
-      }
+      if (k >= a.lag) fold_chunk(i, first + (k - a.lag) * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_fold += t1 - t0;
         t0 = t1;
       }
     }
+    // One system-scope release per launch (not per chunk: a sys fence per chunk stalls the
+    // SM's pushes): my receive slots of every chunk of this launch may be overwritten by
+    // senders two calls later.  Monotone, so it covers every chunk g of mine in [g0, g1).
+    if (nk > 0 && threadIdx.x < a.r)
+      dev::st_release_sys(consumed(a.my_workers[threadIdx.x], i),
+                          step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
     if (a.prof && threadIdx.x == 0) {
       uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
       pr[0] += t_stage;
@@ -332,92 +380,168 @@ struct Split {
       pr[2] += t0 - tstart;
       pr[7] += 1;
     }
-    // consumption counter (senders of call+2 wait for it); every compute CTA counts
-    if (threadIdx.x < a.r) red_add_release_sys(done(a.my_workers[threadIdx.x]), 1);
   }
 
   // ---------------------------------------------------------------- COMM
-  __device__ void comm(int q) const {
-    // guard: every peer I push to has folded this bucket's call-2 data (one remote read
-    // per peer per launch; normally long satisfied)
-    if (a.call >= 2 && threadIdx.x < 32) {
-      const uint64_t need = uint64_t(a.call - 1) * uint64_t(gc);
-      const int pairs = a.r * a.m;
-      for (int p = threadIdx.x; p < pairs; p += 32) {
-        const int s = p / a.m, rr = p % a.m;
-        const int me = a.my_workers[s];
-        const int qw = group(me)[rr];
-        if (qw != me) wait_geq(a, done(qw), need, kWaitDone, qw, rr);
-      }
+  __device__ void comm(int q, unsigned char *smem) const {
+    // dynamic smem: [TMA ring: kRing chunks][kRing mbarriers][guard cache: pairs x Gc u64]
+    float *ring = reinterpret_cast<float *>(smem);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + kRingBytes);
+    uint64_t *cache = mbar + kRing;
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kRing; ++s) dev::mbar_init(&mbar[s], 1);
+      dev::fence_mbar_init();
+    }
+    // (slot, remote member) pairs of this rank; their consumed counters cached in smem
+    int npairs = 0;
+    for (int p = 0; p < a.r * a.m; ++p) {
+      const int s = p / a.m, rr = p % a.m;
+      const int me = a.my_workers[s];
+      const int w = group(me)[rr];
+      if (w != me && remote(w)) ++npairs;
+    }
+    const bool guard = a.call >= 2 && npairs > 0;
+    const bool cached = guard && npairs <= kMaxGuardPairs;
+    if (cached) {  // one bulk remote read of every counter (one round trip per CTA)
+      for (int idx = threadIdx.x; idx < npairs * gc; idx += kThreads)
+        cache[idx] = dev::ld_acquire_sys(consumed(remote_pair_member(idx / gc), idx % gc));
     }
     __syncthreads();
+    // Per batch of B chunks: warp 0 waits (lane-parallel) for the guard and the staged flags;
+    // then every (slot, chunk) item with remote members streams through a kRing-deep smem
+    // ring: thread 0 prefetches the staged chunk with a TMA bulk load (stage in L2 -> smem,
+    // mbarrier completion), and all threads copy it out with 128-bit stores into every remote
+    // member's receive slot (NVLink; LSU stores keep ~22 GB/s per SM, a TMA bulk store to a
+    // peer only ~6 GB/s per SM).  One system-scope release per (chunk, member) ends the batch.
     const int B = a.comm_batch;
-    const int64_t nbatches = (a.nchunks + B - 1) / B;
-    uint64_t t_staged = 0, t_push = 0, t_rel = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
+    const int64_t nbatches = (a.g1 - a.g0 + B - 1) / B;
+    const int ns = a.r;
+    const uint64_t call1 = uint64_t(a.call) + 1;
+    uint64_t t_wait = 0, t_push = 0, t_rel = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
+    auto has_remote = [&](int s) {
+      const int me = a.my_workers[s];
+      for (int rr = 0; rr < a.m; ++rr) {
+        const int w = group(me)[rr];
+        if (w != me && remote(w)) return true;
+      }
+      return false;
+    };
+    uint32_t ring_uses = 0;  // items streamed so far (all threads agree): slot = uses % kRing
     for (int64_t j = q; j < nbatches; j += a.comm_ctas) {
-      const int64_t c0 = j * B, c1 = min(c0 + B, a.nchunks);
-      // wait until the compute CTAs staged every chunk of the batch
+      const int64_t c0 = a.g0 + j * B, c1 = min(c0 + B, a.g1);
+      const int nb = int(c1 - c0);
       if (threadIdx.x < 32) {
-        const int n = int(c1 - c0) * a.r;
-        for (int p = threadIdx.x; p < n; p += 32) {
-          const int s = p % a.r;
-          const int64_t c = c0 + p / a.r;
-          wait_geq(a, staged(s, int(c % gc)), a.seq_epoch0 + uint64_t(c / gc), kWaitStaged,
-                   a.my_workers[s], -1);
+        const int lane = threadIdx.x;
+        if (guard) {  // receivers consumed their call-2 slots
+          for (int idx = lane; idx < nb * npairs; idx += 32) {
+            const int pi = idx % npairs;
+            const int64_t g = c0 + idx / npairs;
+            const int i = int(g % gc);
+            const uint64_t need = step_epoch(a.prev2_epoch0, g);
+            if (cached && cache[pi * gc + i] >= need) continue;
+            const int w = remote_pair_member(pi);
+            const uint64_t got = wait_geq(a, consumed(w, i), need, kWaitConsumed, w, pi);
+            if (cached) cache[pi * gc + i] = got;
+          }
         }
+        for (int idx = lane; idx < nb * ns; idx += 32)  // my compute CTAs staged the batch
+          wait_geq(a, staged(idx % ns, int((c0 + idx / ns) % gc)),
+                   step_epoch(a.seq_epoch0, c0 + idx / ns), kWaitStaged, a.my_workers[idx % ns], -1);
       }
       __syncthreads();
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
-        t_staged += t1 - t0;
+        t_wait += t1 - t0;
         t0 = t1;
       }
-      // copy own stage -> every peer's receive slot (NVLink or local stores)
-      for (int s = 0; s < a.r; ++s) {
-        const int me = a.my_workers[s];
-        const int8_t *G = group(me);
-        const int mypos = a.my_pos[s];
-        const float *st = stage(s);
-        for (int64_t c = c0; c < c1; ++c) {
-          const int64_t e0 = c * kChunk, e1 = min(e0 + kChunk, a.numel);
-          float val[kItems][W];
-          int nvs[kItems];
-#pragma unroll
-          for (int it = 0; it < kItems; ++it) {
-            const int64_t e = e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
-            nvs[it] = (int)min(int64_t(W), e1 - e);
-            if (nvs[it] > 0) ld_slot<W>(st + e, val[it], nvs[it]);
+      // items of the batch that have a remote member: (s, g) in batch order
+      const int total = nb * ns;
+      auto item_live = [&](int idx) { return has_remote(idx % ns); };
+      auto issue_load = [&](int idx, uint32_t use) {
+        const int s = idx % ns;
+        const ChunkRef c = locate(c0 + idx / ns);
+        const uint32_t bytes = uint32_t(((c.e1 - c.e0) & ~int64_t(3)) * 4);
+        const int slot = use % kRing;
+        dev::mbar_arrive_expect_tx(&mbar[slot], bytes);
+        if (bytes > 0) dev::bulk_g2s(ring + slot * kChunk, stage(s) + c.soff + c.e0, bytes, &mbar[slot]);
+      };
+      // prefetch the first kRing live items
+      if (threadIdx.x == 0) {
+        dev::fence_proxy_async_global();  // the stage was written by other CTAs (generic proxy)
+        uint32_t u = ring_uses;
+        for (int idx = 0, k = 0; idx < total && k < kRing; ++idx)
+          if (item_live(idx)) issue_load(idx, u++), ++k;
+      }
+      int next_load = 0;  // thread 0: index of the next live item to prefetch (after the first kRing)
+      if (threadIdx.x == 0) {
+        int k = 0;
+        for (; next_load < total && k < kRing; ++next_load)
+          if (item_live(next_load)) ++k;
+      }
+      for (int idx = 0; idx < total; ++idx) {
+        if (!item_live(idx)) continue;
+        const int s = idx % ns;
+        const int64_t g = c0 + idx / ns;
+        const ChunkRef c = locate(g);
+        const int slot = ring_uses % kRing;
+        if (!dev::mbar_wait(&mbar[slot], (ring_uses / kRing) & 1, a.timeout_ns) && threadIdx.x == 0) {
+          if (atomicExch(a.abort_dev, 1u) == 0u) {  // a TMA load never landed: latch, don't hang
+            a.err_host[1] = 5;
+            a.err_host[2] = blockIdx.x;
+            a.err_host[7] = (unsigned long long)a.my_rank;
+            __threadfence_system();
+            atomicExch(a.err_host, (unsigned long long)(-SESGD_ETIMEOUT));
           }
-          for (int rr = 0; rr < a.m; ++rr) {
-            if (rr == mypos) continue;
-            float *dst = recv(G[rr], mypos);
+        }
+        const float *src = ring + slot * kChunk;
+        const int me = a.my_workers[s];
+        const int mypos = a.my_pos[s];
+        const int64_t len = c.e1 - c.e0;
+        float4 val[kVec];
 #pragma unroll
-            for (int it = 0; it < kItems; ++it) {
-              if (nvs[it] <= 0) continue;
-              const int64_t e = e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
-              st_slot<W>(dst + e, val[it], nvs[it]);
+        for (int it = 0; it < kVec; ++it) {
+          const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * 4;
+          if (o + 4 <= len) val[it] = *reinterpret_cast<const float4 *>(src + o);
+        }
+        for (int rr = 0; rr < a.m; ++rr) {
+          const int w = group(me)[rr];
+          if (w == me || !remote(w)) continue;
+          float *dst = recv(w, mypos) + c.soff + c.e0;
+#pragma unroll
+          for (int it = 0; it < kVec; ++it) {
+            const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * 4;
+            if (o + 4 <= len) {
+              *reinterpret_cast<float4 *>(dst + o) = val[it];
+            } else if (o < len) {  // ragged 1..3-float tail (not covered by the bulk load)
+              for (int64_t e = o; e < len; ++e) dst[e] = __ldcg(stage(s) + c.soff + c.e0 + e);
             }
           }
         }
+        ++ring_uses;
+        __syncthreads();  // every thread has read the slot: refill it
+        if (threadIdx.x == 0) {
+          while (next_load < total && !item_live(next_load)) ++next_load;
+          if (next_load < total) issue_load(next_load++, ring_uses + kRing - 1);
+        }
       }
-      __syncthreads();  // all stores of the batch precede the releases (cumulativity)
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_push += t1 - t0;
         t0 = t1;
       }
+      __syncthreads();  // every store of the batch precedes the releases (cumulativity)
       if (threadIdx.x < 32) {
         hop_delay(a);
-        const uint64_t call = a.call + 1;
-        const int n = int(c1 - c0) * a.r * a.m;
+        const int n = nb * ns * a.m;
         for (int p = threadIdx.x; p < n; p += 32) {
-          const int rr = p % a.m, s = (p / a.m) % a.r;
-          const int64_t c = c0 + p / (a.m * a.r);
+          const int rr = p % a.m, s = (p / a.m) % ns;
+          const int64_t g = c0 + p / (a.m * ns);
           const int me = a.my_workers[s];
-          if (rr == a.my_pos[s])
-            st_release_gpu(sent(s, c), call);
-          else
-            dev::st_release_sys(ready(group(me)[rr], c, a.my_pos[s]), call);
+          const int w = group(me)[rr];
+          if (w == me)
+            st_release_gpu(sent(s, g), call1);
+          else if (remote(w))
+            dev::st_release_sys(ready(w, g, a.my_pos[s]), call1);
         }
       }
       if (a.prof) {
@@ -428,7 +552,7 @@ struct Split {
     }
     if (a.prof && threadIdx.x == 0) {
       uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
-      pr[0] += t_staged;
+      pr[0] += t_wait;
       pr[1] += t_push;
       pr[2] += t_rel;
       pr[3] += t0 - tstart;
@@ -436,44 +560,240 @@ struct Split {
     }
   }
 
+  // ---------------------------------------------------------------- DIRECT (no COMM CTAs)
+  // Every CTA is a compute CTA that pushes its own x_hat to the remote members straight from
+  // registers (remote stores are fire-and-forget), so nothing is ever re-read from the stage
+  // for sending.  The ready flags of chunk k are released at the start of chunk k+1's stage,
+  // when those stores have long drained, so the system-scope release costs little.
+
+  // release the ready flags of chunk g (warp 0, lane-parallel); every thread's stores of
+  // chunk g precede this call through the __syncthreads that ends stage_push(g)
+  __device__ __forceinline__ void release_ready(int64_t g) const {
+    if (threadIdx.x >= 32) return;
+    hop_delay(a);
+    const uint64_t call1 = uint64_t(a.call) + 1;
+    for (int p = threadIdx.x; p < a.r * a.m; p += 32) {
+      const int s = p / a.m, rr = p % a.m;
+      const int me = a.my_workers[s];
+      const int w = group(me)[rr];
+      if (w != me && remote(w)) dev::st_release_sys(ready(w, g, a.my_pos[s]), call1);
+    }
+  }
+
+  __device__ void stage_push(int64_t g) const {
+    const ChunkRef c = locate(g);
+    for (int s = 0; s < a.r; ++s) {
+      float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
+      const float *gs = a.bg[c.b * a.r + s];
+      const int me = a.my_workers[s];
+      const int8_t *G = group(me);
+      const int mypos = a.my_pos[s];
+      float *st = stage(s) + c.soff;
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+        const int nv = (int)min(int64_t(W), c.e1 - e);
+        if (nv <= 0) continue;
+        float gr[W], val[W];
+        load_m<W>(gs + e, gr, nv);
+        if constexpr (!GRAD) {
+          float v[W], x[W];
+          load_m<W>(vs + e, v, nv);
+          load_m<W>(xs + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
+          }
+          store_m<W>(vs + e, v, nv);
+        } else {
+#pragma unroll
+          for (int q = 0; q < W; ++q) val[q] = gr[q];
+        }
+        st_slot<W>(st + e, val, nv);  // own copy, read by my fold (and co-resident members')
+        for (int rr = 0; rr < a.m; ++rr) {
+          const int w = G[rr];
+          if (w != me && remote(w)) st_slot<W>(recv(w, mypos) + c.soff + e, val, nv);  // NVLink
+        }
+      }
+    }
+    __syncthreads();  // every store of chunk g precedes its (deferred) flag release
+  }
+
+  __device__ void fold_direct(int64_t g) const {
+    const ChunkRef c = locate(g);
+    const uint64_t call1 = uint64_t(a.call) + 1;
+    if (threadIdx.x < 32) {  // every remote member's chunk g arrived
+      for (int p = threadIdx.x; p < a.r * a.m; p += 32) {
+        const int s = p / a.m, rr = p % a.m;
+        const int me = a.my_workers[s];
+        const int w = group(me)[rr];
+        if (w != me && remote(w)) wait_geq(a, ready(me, g, rr), call1, kWaitReady, me, rr);
+      }
+    }
+    __syncthreads();
+    for (int s = 0; s < a.r; ++s) {
+      const int me = a.my_workers[s];
+      const int8_t *G = group(me);
+      float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+        const int nv = (int)min(int64_t(W), c.e1 - e);
+        if (nv <= 0) continue;
+        float acc[W];
+        for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
+          const int w = G[rr];
+          const float *src = remote(w) ? recv(me, rr) : stage(a.worker_slot[w]);
+          float y[W];
+          ld_slot<W>(src + c.soff + e, y, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
+        if constexpr (!GRAD) {
+          store_m<W>(xs + e, acc, nv);
+        } else {
+          float v[W], x[W];
+          load_m<W>(vs + e, v, nv);
+          load_m<W>(xs + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], acc[q]);
+            x[q] = dev::sgd(x[q], a.lr, v[q]);
+          }
+          store_m<W>(vs + e, v, nv);
+          store_m<W>(xs + e, x, nv);
+        }
+      }
+    }
+    __syncthreads();  // all slots folded (co-resident stages read)
+    if constexpr (W == 4) {
+      if (a.discard && (threadIdx.x & 7) == 0) {
+        for (int s = 0; s < a.r; ++s) {
+          const int me = a.my_workers[s];
+          const int8_t *G = group(me);
+#pragma unroll
+          for (int it = 0; it < kItems; ++it) {
+            const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+            if (e + 32 > c.e1) continue;
+            discard_l2(stage(s) + c.soff + e);
+            for (int rr = 0; rr < a.m; ++rr)
+              if (remote(G[rr])) discard_l2(recv(me, rr) + c.soff + e);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void compute_direct(int i) const {
+    const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
+    const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
+    if (nk == 0) return;
+    // guard, once: every remote member consumed its receive slots of call-2 for my chunks
+    // (its CTA i folds exactly my chunks, so one remote counter per member)
+    if (a.call >= 2 && threadIdx.x < 32) {
+      const uint64_t need = step_epoch(a.prev2_epoch0, first + (nk - 1) * gc);
+      for (int p = threadIdx.x; p < a.r * a.m; p += 32) {
+        const int s = p / a.m, rr = p % a.m;
+        const int me = a.my_workers[s];
+        const int w = group(me)[rr];
+        if (w != me && remote(w)) wait_geq(a, consumed(w, i), need, kWaitConsumed, w, rr);
+      }
+    }
+    __syncthreads();
+    uint64_t t_stage = 0, t_fold = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
+    for (int64_t k = 0; k < nk + a.lag; ++k) {
+      if (k >= 1 && k <= nk) release_ready(first + (k - 1) * gc);
+      if (k < nk) stage_push(first + k * gc);
+      if (a.prof) {
+        const uint64_t t1 = dev::globaltimer();
+        t_stage += t1 - t0;
+        t0 = t1;
+      }
+      if (k >= a.lag) fold_direct(first + (k - a.lag) * gc);
+      if (a.prof) {
+        const uint64_t t1 = dev::globaltimer();
+        t_fold += t1 - t0;
+        t0 = t1;
+      }
+    }
+    if (a.lag == 0) release_ready(first + (nk - 1) * gc);  // (lag >= 1 releases it in the loop)
+    if (threadIdx.x < a.r)
+      dev::st_release_sys(consumed(a.my_workers[threadIdx.x], i),
+                          step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
+    if (a.prof && threadIdx.x == 0) {
+      uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
+      pr[0] += t_stage;
+      pr[1] += t_fold;
+      pr[2] += t0 - tstart;
+      pr[7] += 1;
+    }
+  }
+
   // m == 1: no exchange, the local step is the whole update (x / 1 = x)
   __device__ void local_only() const {
-    const int64_t stride = int64_t(a.grid) * kThreads * W;
-    for (int s = 0; s < a.r; ++s) {
-      float *xs = a.x[s], *vs = a.v[s];
-      const float *gs = a.g[s];
-      for (int64_t e = (int64_t(blockIdx.x) * kThreads + threadIdx.x) * W; e < a.numel; e += stride) {
-        const int nv = (int)min(int64_t(W), a.numel - e);
-        float g[W], v[W], x[W];
-        load_m<W>(gs + e, g, nv);
-        load_m<W>(vs + e, v, nv);
-        load_m<W>(xs + e, x, nv);
+    for (int64_t g = a.g0 + blockIdx.x; g < a.g1; g += a.grid) {
+      const ChunkRef c = locate(g);
+      for (int s = 0; s < a.r; ++s) {
+        float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
+        const float *gs = a.bg[c.b * a.r + s];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          v[w] = dev::momentum(a.mu, v[w], g[w]);
-          x[w] = dev::sgd(x[w], a.lr, v[w]);
+        for (int it = 0; it < kItems; ++it) {
+          const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+          const int nv = (int)min(int64_t(W), c.e1 - e);
+          if (nv <= 0) continue;
+          float gr[W], v[W], x[W];
+          load_m<W>(gs + e, gr, nv);
+          load_m<W>(vs + e, v, nv);
+          load_m<W>(xs + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            x[q] = dev::sgd(x[q], a.lr, v[q]);
+          }
+          store_m<W>(vs + e, v, nv);
+          store_m<W>(xs + e, x, nv);
         }
-        store_m<W>(vs + e, v, nv);
-        store_m<W>(xs + e, x, nv);
       }
     }
   }
 };
 
 template <int W, bool GRAD>
-__global__ void __launch_bounds__(kThreads) k3_split(const __grid_constant__ P2PArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k3_split(const __grid_constant__ P2PArgs a) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
   const Split<W, GRAD> p(a);
   if (a.m == 1) {
     p.local_only();
   } else if (int(blockIdx.x) < a.comm_ctas) {
-    p.comm(blockIdx.x);
+    p.comm(blockIdx.x, dsmem);
   } else {
     p.compute(blockIdx.x - a.comm_ctas);
   }
 }
 
-const void *pick(int mode, bool vec) {
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__ P2PArgs a) {
+  const Split<W, GRAD> p(a);
+  if (a.m == 1)
+    p.local_only();
+  else
+    p.compute_direct(blockIdx.x);
+}
+
+// variant 0: DIRECT push from the compute CTAs; variant >= 1: that many COMM CTAs
+const void *pick(int variant, int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (variant == 0) {
+    if (vec)
+      return grad ? reinterpret_cast<const void *>(&k3_direct<4, true>)
+                  : reinterpret_cast<const void *>(&k3_direct<4, false>);
+    return grad ? reinterpret_cast<const void *>(&k3_direct<1, true>)
+                : reinterpret_cast<const void *>(&k3_direct<1, false>);
+  }
   if (vec)
     return grad ? reinterpret_cast<const void *>(&k3_split<4, true>)
                 : reinterpret_cast<const void *>(&k3_split<4, false>);
@@ -483,24 +803,33 @@ const void *pick(int mode, bool vec) {
 
 }  // namespace
 
-bool p2p_variant_valid(int variant) { return variant >= 1 && variant <= 148; }
+bool p2p_variant_valid(int variant) { return variant >= 0 && variant <= 148; }
 int p2p_block_threads(int) { return kThreads; }
 int p2p_chunk_elems(int) { return int(kChunk); }
+int p2p_guard_pairs_max() { return kMaxGuardPairs; }
+size_t p2p_smem_bytes(int variant, int pairs, int grid) {
+  if (variant == 0) return 0;  // DIRECT: no COMM ring, no guard cache
+  return size_t(kRingBytes) + size_t(kRing) * 8 + size_t(pairs > 0 ? pairs : 0) * size_t(grid) * 8;
+}
 
-int p2p_occupancy(int variant, int r, int mode, bool vec) {
-  (void)variant;
+int p2p_occupancy(int variant, int r, int mode, bool vec, size_t smem) {
   (void)r;
+  const void *k = pick(variant, mode, vec);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode, vec), kThreads, 0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, smem) != cudaSuccess)
     return 1;
   return blocks > 0 ? blocks : 1;
 }
 
-cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec,
+cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec, size_t smem,
                                cudaStream_t stream) {
-  (void)variant;
+  const void *k = pick(variant, mode, vec);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
-  return cudaLaunchKernel(pick(mode, vec), dim3(a.grid), dim3(kThreads), args, 0, stream);
+  return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
 }
 
 }  // namespace sesgd

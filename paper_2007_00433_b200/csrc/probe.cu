@@ -57,7 +57,11 @@ SESGD_API int sesgd_probe_copy(void *dst, const void *src, int64_t bytes, int32_
                                void *stream) {
   if (!dst || !src || bytes < 0 || (bytes & 15) || ctas < 1) return SESGD_EINVAL;
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return SESGD_EINVAL;
-  sesgd::copy_kernel<<<ctas, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+  // ctas = CTA count | (threads per CTA / 32) << 16; threads default 512
+  const int warps = (ctas >> 16) & 0x3f;
+  ctas &= 0xffff;
+  if (ctas < 1) return SESGD_EINVAL;
+  sesgd::copy_kernel<<<ctas, warps ? warps * 32 : 512, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<float4 *>(dst), static_cast<const float4 *>(src), bytes / 16);
   return cudaGetLastError() == cudaSuccess ? SESGD_OK : SESGD_ECUDA;
 }

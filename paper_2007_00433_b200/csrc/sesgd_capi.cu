@@ -51,11 +51,12 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 int check_latched(sesgd_ctx *ctx) {
   volatile unsigned long long *e = ctx->h_err;
   if (!e || e[0] == 0) return SESGD_OK;
+  static const char *kinds[] = {"?", "consumed", "ready", "staged", "sent", "TMA-load"};
   char buf[256];
   std::snprintf(buf, sizeof buf,
                 "a group peer did not signal before the timeout: rank %llu CTA %llu waited for "
                 "%s flag of worker %llu (position %lld): saw epoch %llu, needed %llu",
-                e[7], e[2], e[1] == 1 ? "consumed" : "ready", e[5], (long long)e[6], e[3], e[4]);
+                e[7], e[2], kinds[e[1] < 6 ? e[1] : 0], e[5], (long long)e[6], e[3], e[4]);
   return fail(ctx, SESGD_ETIMEOUT, buf);
 }
 
@@ -68,28 +69,42 @@ void free_bucket(sesgd_bucket &b) {
 }
 
 // ---- multi-GPU workspace layout (identical on every rank) ----
-//   [0, 256)          header: magic, layout hash
-//   [ready_off, ..)   u64 ready [2 parity][r slot][total_chunks][m position]  (written by peers)
-//   [sent_off, ..)    u64 sent  [r slot][total_chunks]          (local: COMM -> COMPUTE)
-//   [staged_off, ..)  u64 staged[r slot][compute CTAs]          (local: COMPUTE -> COMM)
-//   [done_off, ..)    u64 done  [r slot][NB]                    (read by peers: consumption)
-//   [stage_off, ..)   f32 stage [r slot][stage_slot_floats]     (own x_hat, L2-resident)
-//   [recv_off, ..)    f32 recv  [2 parity][r slot][m position][stage_slot_floats]
+//   [0, 256)            header: magic, layout hash
+//   [ready_off, ..)     u64 ready   [2 parity][r slot][total_chunks][m position] (written by peers)
+//   [sent_off, ..)      u64 sent    [r slot][total_chunks]        (local: COMM -> COMPUTE)
+//   [staged_off, ..)    u64 staged  [r slot][Gc]                  (local: COMPUTE -> COMM)
+//   [consumed_off, ..)  u64 consumed[r slot][Gc]                  (read by peers' COMM: guard)
+//   [stage_off, ..)     f32 stage   [r slot][region]              (own x_hat, L2-resident)
+//   [recv_off, ..)      f32 recv    [2 parity][r slot][m position][region]
+// region = stage_slot_floats = sum over buckets of round_up(numel, 64).
 void freeze_layout(sesgd_ctx *ctx) {
   const int var = ctx->p2p_variant;
   const int chunk = sesgd::p2p_chunk_elems(var);
   const int r = ctx->n_local;
-  int occ = sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, true);
-  occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, true));
-  occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, false));
-  occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, false));
-  int grid = ctx->sm_count * occ;  // every CTA co-resident (COMM and COMPUTE wait on each other)
+  const int pairs = std::min(sesgd::p2p_guard_pairs_max(), r * (ctx->m - 1));
+  auto occupancy = [&](size_t smem) {
+    int occ = sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, true, smem);
+    occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, true, smem));
+    occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, false, smem));
+    occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, false, smem));
+    return occ;
+  };
+  // every CTA must be co-resident (COMM and COMPUTE wait on each other): grid = SMs x
+  // occupancy, with the COMM guard cache (pairs x Gc u64) in dynamic shared memory
+  int grid = ctx->sm_count * occupancy(sesgd::p2p_smem_bytes(var, 0, 0));
   if (ctx->grid_opt > 0 && ctx->grid_opt < grid) grid = int(ctx->grid_opt);
-  const int comm = std::min(var, std::max(1, grid / 2));
+  size_t smem = sesgd::p2p_smem_bytes(var, pairs, grid);
+  const int grid2 = ctx->sm_count * occupancy(smem);
+  if (grid2 < grid) {
+    grid = grid2;
+    smem = sesgd::p2p_smem_bytes(var, pairs, grid);
+  }
+  const int comm = std::min(var, std::max(1, grid / 2));  // 0 = DIRECT push (no COMM CTAs)
+  const int gc = grid - comm;
   ctx->grid = grid;
   ctx->chunk = chunk;
-  const int gc = grid - comm;
-  int64_t off = 0, kmax = 1, chunks = 0;
+  ctx->guard_smem = smem;
+  int64_t off = 0, chunks = 0;
   uint64_t h = 0xcbf29ce484222325ULL;
   h = fnv(h, uint64_t(ctx->n));
   h = fnv(h, uint64_t(ctx->m));
@@ -104,25 +119,152 @@ void freeze_layout(sesgd_ctx *ctx) {
     bk.nchunks = (bk.numel + chunk - 1) / chunk;
     bk.chunk_base = chunks;
     chunks += bk.nchunks;
-    kmax = std::max<int64_t>(kmax, (bk.nchunks + gc - 1) / gc);
     off += round_up(bk.numel, 64);  // 256-byte aligned buckets
     h = fnv(h, uint64_t(b));
     h = fnv(h, uint64_t(bk.registered ? bk.numel : -1));
   }
   ctx->p2p_variant = comm;
-  ctx->kmax = kmax;
   ctx->total_chunks = std::max<int64_t>(chunks, 1);
+  ctx->kmax = (ctx->total_chunks + gc - 1) / gc + 1;  // > any floor(g / Gc)
   ctx->stage_slot_floats = std::max<int64_t>(off, 64);
-  const int64_t nb = int64_t(ctx->buckets.size());
   ctx->ready_off = 256;
   ctx->sent_off = round_up(ctx->ready_off + 2 * int64_t(r) * ctx->total_chunks * ctx->m * 8, 256);
   ctx->staged_off = round_up(ctx->sent_off + int64_t(r) * ctx->total_chunks * 8, 256);
-  ctx->done_off = round_up(ctx->staged_off + int64_t(r) * gc * 8, 256);
-  ctx->stage_off = round_up(ctx->done_off + int64_t(r) * nb * 8, 4096);
+  ctx->consumed_off = round_up(ctx->staged_off + int64_t(r) * gc * 8, 256);
+  ctx->stage_off = round_up(ctx->consumed_off + int64_t(r) * gc * 8, 4096);
   ctx->recv_off = ctx->stage_off + int64_t(r) * ctx->stage_slot_floats * 4;
   ctx->ws_bytes = ctx->recv_off + 2 * int64_t(r) * ctx->m * ctx->stage_slot_floats * 4;
   ctx->layout_hash = h;
   ctx->layout_frozen = true;
+}
+
+// device bucket tables of the one-shot kernel: meta[NB], x/v/g pointers [NB * r]
+int upload_tables(sesgd_ctx *ctx) {
+  const size_t nb = ctx->buckets.size();
+  const int r = ctx->n_local;
+  std::vector<sesgd::BucketMeta> meta(nb);
+  std::vector<float *> bx(nb * r), bv(nb * r);
+  std::vector<const float *> bg(nb * r);
+  for (size_t b = 0; b < nb; ++b) {
+    const sesgd_bucket &bk = ctx->buckets[b];
+    meta[b] = {bk.numel, bk.stage_bucket_off, bk.chunk_base, bk.nchunks};
+    for (int s = 0; s < r; ++s) {
+      bx[b * r + s] = bk.hx[s];
+      bv[b * r + s] = bk.hv[s];
+      bg[b * r + s] = bk.hg[s];
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!ctx->d_meta) {
+    e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_meta), std::max<size_t>(nb, 1) * sizeof(sesgd::BucketMeta));
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bx), std::max<size_t>(nb * r, 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bv), std::max<size_t>(nb * r, 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bg), std::max<size_t>(nb * r, 1) * 8);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(bucket tables)");
+  }
+  e = cudaMemcpy(ctx->d_meta, meta.data(), nb * sizeof(sesgd::BucketMeta), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bx, bx.data(), nb * r * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bv, bv.data(), nb * r * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(const_cast<float **>(ctx->d_bg), bg.data(), nb * r * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpy(bucket tables)");
+  return SESGD_OK;
+}
+
+// One one-shot launch over bucket `bucket` (>= 0) or over every bucket (-1, all buckets
+// share the same call history).  Host bookkeeping of calls / launch sequence follows.
+int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st) {
+  const sesgd_bucket &ref = ctx->buckets[bucket >= 0 ? bucket : 0];
+  P2PArgs a{};
+  a.meta = ctx->d_meta;
+  a.bx = ctx->d_bx;
+  a.bv = ctx->d_bv;
+  a.bg = ctx->d_bg;
+  for (int r = 0; r < ctx->n_ranks; ++r) a.ws[r] = ctx->ws[r];
+  if (bucket >= 0) {
+    a.g0 = ref.chunk_base;
+    a.g1 = ref.chunk_base + ref.nchunks;
+  } else {
+    a.g0 = 0;
+    a.g1 = ctx->total_chunks;
+  }
+  a.total_chunks = ctx->total_chunks;
+  a.region_floats = ctx->stage_slot_floats;
+  a.ready_off = ctx->ready_off;
+  a.sent_off = ctx->sent_off;
+  a.staged_off = ctx->staged_off;
+  a.consumed_off = ctx->consumed_off;
+  a.stage_off = ctx->stage_off;
+  a.recv_off = ctx->recv_off;
+  const int64_t call = ref.calls;
+  a.call = call;
+  a.seq_epoch0 = uint64_t(ctx->seq) * uint64_t(ctx->kmax) + 1;
+  a.prev2_epoch0 = call >= 2 ? uint64_t(ref.seq_hist[call & 1]) * uint64_t(ctx->kmax) + 1 : 0;
+  a.timeout_ns = uint64_t(ctx->timeout_ms) * 1000000ULL;
+  a.hop_delay_ns = uint64_t(ctx->hop_delay_ns);
+  a.err_host = ctx->d_err;
+  a.abort_dev = ctx->d_abort;
+  if (ctx->profile && !ctx->d_prof) {
+    cudaError_t pe = cudaMalloc(reinterpret_cast<void **>(&ctx->d_prof), size_t(ctx->grid) * 64);
+    if (pe == cudaSuccess) pe = cudaMemset(ctx->d_prof, 0, size_t(ctx->grid) * 64);
+    if (pe != cudaSuccess) return cuda_fail(ctx, pe, "profile buffer");
+  }
+  a.prof = ctx->profile ? ctx->d_prof : nullptr;
+  a.lr = lr;
+  a.mu = momentum;
+  a.n = ctx->n;
+  a.m = ctx->m;
+  a.r = ctx->n_local;
+  a.grid = ctx->grid;
+  a.comm_ctas = ctx->p2p_variant;
+  a.comm_batch = ctx->comm_batch;
+  a.lag = ctx->fold_lag;
+  a.parity = int(call & 1);
+  a.my_rank = ctx->rank;
+  a.bucket = bucket;
+  a.nbuckets = int(ctx->buckets.size());
+  a.discard = ctx->discard;
+  for (int s = 0; s < ctx->n_local; ++s) {
+    const int me = ctx->local_workers[s];
+    a.my_workers[s] = int8_t(me);
+    const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
+    for (int p = 0; p < ctx->m; ++p)
+      if (G[p] == me) a.my_pos[s] = int8_t(p);
+  }
+  for (int i = 0; i < ctx->n; ++i) {
+    a.worker_rank[i] = ctx->worker_rank[i];
+    a.worker_slot[i] = ctx->worker_slot[i];
+    a.canon[i] = int8_t(ctx->canon[i]);
+    a.group_of[i] = int8_t(ctx->group_of[i]);
+  }
+  bool vec = true;
+  for (size_t b = 0; b < ctx->buckets.size(); ++b)
+    if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
+  cudaError_t e = sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec, ctx->guard_smem, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch one-shot kernel");
+  // bookkeeping
+  int remote_peers = 0;
+  for (int s = 0; s < ctx->n_local; ++s) {
+    const int me = ctx->local_workers[s];
+    const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
+    for (int r = 0; r < ctx->m; ++r)
+      if (G[r] != me && ctx->worker_rank[G[r]] != ctx->rank) remote_peers++;
+  }
+  for (size_t b = 0; b < ctx->buckets.size(); ++b) {
+    if (bucket >= 0 && int(b) != bucket) continue;
+    sesgd_bucket &bk = ctx->buckets[b];
+    bk.seq_hist[bk.calls & 1] = ctx->seq;
+    bk.calls++;
+    bk.stats.kernel_launches += (bucket >= 0 || b == 0) ? 1 : 0;
+    bk.stats.hbm_algo_bytes += 20 * bk.numel * ctx->n_local;
+    if (ctx->m > 1) {
+      bk.stats.handshake_rounds = 1;
+      bk.stats.flag_messages += int64_t(remote_peers) * bk.nchunks;  // one ready flag per chunk
+      bk.stats.payload_bytes_in += int64_t(remote_peers) * bk.numel * 4;
+    }
+  }
+  ctx->seq++;
+  return SESGD_OK;
 }
 
 }  // namespace
@@ -168,6 +310,10 @@ void sesgd_destroy(sesgd_ctx *ctx) {
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->d_abort) cudaFree(ctx->d_abort);
   if (ctx->d_prof) cudaFree(ctx->d_prof);
+  if (ctx->d_meta) cudaFree(ctx->d_meta);
+  if (ctx->d_bx) cudaFree(ctx->d_bx);
+  if (ctx->d_bv) cudaFree(ctx->d_bv);
+  if (ctx->d_bg) cudaFree(const_cast<float **>(ctx->d_bg));
   delete ctx;
 }
 
@@ -324,6 +470,7 @@ int sesgd_register_bucket(sesgd_ctx *ctx, int32_t bucket, int64_t numel, float *
   b.numel = numel;
   b.vec = vec;
   b.registered = true;
+  if (ctx->layout_frozen) return upload_tables(ctx);  // re-registration after the layout froze
   return SESGD_OK;
 }
 
@@ -391,6 +538,8 @@ int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, void *cons
   }
   ctx->n_ranks = n_ranks;
   ctx->rank = rank;
+  int rc = upload_tables(ctx);
+  if (rc != SESGD_OK) return rc;
   ctx->peers = true;
   return SESGD_OK;
 }
@@ -453,81 +602,35 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
 
   // one-shot push over NVLink P2P
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
-  P2PArgs a{};
-  a.x = b.d_x;
-  a.v = b.d_v;
-  a.g = b.d_g;
-  for (int r = 0; r < ctx->n_ranks; ++r) a.ws[r] = ctx->ws[r];
-  a.numel = b.numel;
-  a.nchunks = b.nchunks;
-  a.total_chunks = ctx->total_chunks;
-  a.chunk_base = b.chunk_base;
-  a.stage_slot_floats = ctx->stage_slot_floats;
-  a.stage_bucket_off = b.stage_bucket_off;
-  a.ready_off = ctx->ready_off;
-  a.sent_off = ctx->sent_off;
-  a.staged_off = ctx->staged_off;
-  a.done_off = ctx->done_off;
-  a.stage_off = ctx->stage_off;
-  a.recv_off = ctx->recv_off;
-  a.seq_epoch0 = uint64_t(ctx->seq) * uint64_t(ctx->kmax) + 1;
-  a.call = b.calls;
-  a.timeout_ns = uint64_t(ctx->timeout_ms) * 1000000ULL;
-  a.hop_delay_ns = uint64_t(ctx->hop_delay_ns);
-  a.err_host = ctx->d_err;
-  a.abort_dev = ctx->d_abort;
-  if (ctx->profile && !ctx->d_prof) {
-    cudaError_t pe = cudaMalloc(reinterpret_cast<void **>(&ctx->d_prof), size_t(ctx->grid) * 64);
-    if (pe == cudaSuccess) pe = cudaMemset(ctx->d_prof, 0, size_t(ctx->grid) * 64);
-    if (pe != cudaSuccess) return cuda_fail(ctx, pe, "profile buffer");
-  }
-  a.prof = ctx->profile ? ctx->d_prof : nullptr;
-  a.lr = lr;
-  a.mu = momentum;
-  a.n = ctx->n;
-  a.m = ctx->m;
-  a.r = ctx->n_local;
-  a.grid = ctx->grid;
-  a.comm_ctas = ctx->p2p_variant;
-  a.comm_batch = ctx->comm_batch;
-  a.lag = ctx->fold_lag;
-  a.parity = int(b.calls & 1);
-  a.my_rank = ctx->rank;
-  a.bucket = bucket;
-  a.nbuckets = int(ctx->buckets.size());
-  a.discard = ctx->discard;
-  for (int s = 0; s < ctx->n_local; ++s) {
-    const int me = ctx->local_workers[s];
-    a.my_workers[s] = int8_t(me);
-    const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
-    for (int p = 0; p < ctx->m; ++p)
-      if (G[p] == me) a.my_pos[s] = int8_t(p);
-  }
-  for (int i = 0; i < ctx->n; ++i) {
-    a.worker_rank[i] = ctx->worker_rank[i];
-    a.worker_slot[i] = ctx->worker_slot[i];
-    a.canon[i] = int8_t(ctx->canon[i]);
-    a.group_of[i] = int8_t(ctx->group_of[i]);
-  }
-  cudaError_t e = sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, b.vec, st);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch one-shot kernel");
-  b.calls++;
-  ctx->seq++;
-  b.stats.kernel_launches++;
-  b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n_local;
-  if (ctx->m > 1) {
-    b.stats.handshake_rounds = 1;
-    int remote_peers = 0;
-    for (int s = 0; s < ctx->n_local; ++s) {
-      const int me = ctx->local_workers[s];
-      const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
-      for (int r = 0; r < ctx->m; ++r)
-        if (G[r] != me && ctx->worker_rank[G[r]] != ctx->rank) remote_peers++;
+  return launch_oneshot(ctx, bucket, lr, momentum, st);
+}
+
+int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  int rc = check_latched(ctx);
+  if (rc != SESGD_OK) return rc;
+  if (!ctx->attached || !ctx->iter_set) return fail(ctx, SESGD_ESTATE, "attach and begin_iter first");
+  if (ctx->buckets.empty()) return fail(ctx, SESGD_ESTATE, "no bucket registered");
+  for (auto &b : ctx->buckets)
+    if (!b.registered) return fail(ctx, SESGD_ESTATE, "bucket ids must be dense from 0");
+  if (!std::isfinite(lr) || !std::isfinite(momentum))
+    return fail(ctx, SESGD_EINVAL, "lr and momentum must be finite");
+  const bool all_local = (ctx->n_local == ctx->n);
+  int path = ctx->path;
+  if (path == SESGD_PATH_AUTO) path = all_local ? SESGD_PATH_RESIDENT : SESGD_PATH_ONESHOT;
+  bool fuse = (path == SESGD_PATH_ONESHOT) && ctx->peers;
+  for (auto &b : ctx->buckets)  // one launch needs one shared call history
+    fuse = fuse && b.calls == ctx->buckets[0].calls && b.seq_hist[0] == ctx->buckets[0].seq_hist[0] &&
+           b.seq_hist[1] == ctx->buckets[0].seq_hist[1];
+  if (!fuse) {
+    for (size_t b = 0; b < ctx->buckets.size(); ++b) {
+      rc = sesgd_sync_step(ctx, int32_t(b), lr, momentum, stream);
+      if (rc != SESGD_OK) return rc;
     }
-    b.stats.flag_messages += int64_t(remote_peers) * b.nchunks;  // one ready flag per chunk
-    b.stats.payload_bytes_in += int64_t(remote_peers) * b.numel * 4;
+    return SESGD_OK;
   }
-  return SESGD_OK;
+  for (auto &b : ctx->buckets) b.stats.sync_calls++;
+  return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream));
 }
 
 int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,

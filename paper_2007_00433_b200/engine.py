@@ -115,11 +115,20 @@ class SESGDEngine:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         C.sesgd_sync_step(self.ctx, b, lr, momentum, s.cuda_stream)
 
-    def step(self, t: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
-        """One SESGD iteration over every bucket (Alg.1 lines 3-11 for all local workers)."""
+    def sync_all(self, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        C.sesgd_sync_all(self.ctx, lr, momentum, s.cuda_stream)
+
+    def step(self, t: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None,
+             fused: bool = True):
+        """One SESGD iteration over every bucket (Alg.1 lines 3-11 for all local workers):
+        one sesgd_sync_all call (fused), or one sesgd_sync_step per bucket."""
         self.begin_iter(t)
-        for b in range(len(self.bucket_sizes)):
-            self.sync_step(b, lr, momentum, stream)
+        if fused:
+            self.sync_all(lr, momentum, stream)
+        else:
+            for b in range(len(self.bucket_sizes)):
+                self.sync_step(b, lr, momentum, stream)
 
     def step_host(self, t: int, lr: float, momentum: float, g_host, x_host,
                   stream: Optional[torch.cuda.Stream] = None):

@@ -28,7 +28,7 @@ EXPORTED = (
     "sesgd_attach", "sesgd_register_bucket", "sesgd_workspace_bytes", "sesgd_workspace_prepare",
     "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
-    "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read",
+    "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
 )
 
 
@@ -74,6 +74,7 @@ def lib():
             "sesgd_begin_iter": ([P, i64], ctypes.c_int),
             "sesgd_sync_step": ([P, i32, f32, f32, P], ctypes.c_int),
             "sesgd_sync_step_host": ([P, i32, f32, f32, P, P, P], ctypes.c_int),
+            "sesgd_sync_all": ([P, f32, f32, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -164,6 +165,10 @@ def sesgd_begin_iter(ctx, it: int) -> None:
 
 def sesgd_sync_step(ctx, bucket: int, lr: float, momentum: float, stream: int = 0) -> None:
     _check(lib().sesgd_sync_step(ctx, bucket, lr, momentum, ctypes.c_void_p(int(stream))), ctx)
+
+
+def sesgd_sync_all(ctx, lr: float, momentum: float, stream: int = 0) -> None:
+    _check(lib().sesgd_sync_all(ctx, lr, momentum, ctypes.c_void_p(int(stream))), ctx)
 
 
 def sesgd_sync_step_host(ctx, bucket: int, lr: float, momentum: float, g_host_ptrs, x_host_ptrs,

@@ -26,6 +26,9 @@ def main():
     p.add_argument("--t0", type=int, default=0)
     p.add_argument("--grid", type=int, default=0)
     p.add_argument("--variant", type=int, default=-1)
+    p.add_argument("--fused", type=int, default=1)
+    p.add_argument("--batch", type=int, default=0)
+    p.add_argument("--lag", type=int, default=0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -36,7 +39,8 @@ def main():
     buckets = [int(b) for b in a.buckets.split(",")]
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
-                      grid=a.grid, timeout_ms=10000, p2p_variant=a.variant)
+                      grid=a.grid, timeout_ms=10000, p2p_variant=a.variant,
+                      options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag)) if v})
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):
@@ -45,7 +49,7 @@ def main():
         for s, w in enumerate(eng.local_workers):
             for b, L in enumerate(buckets):
                 synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
-        eng.step(t, 0.1, 0.9)
+        eng.step(t, 0.1, 0.9, fused=bool(a.fused))
     torch.cuda.synchronize()
     eng.poll()
     X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])

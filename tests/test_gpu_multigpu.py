@@ -28,7 +28,8 @@ def _free_port():
     return p
 
 
-def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1):
+def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
+            lag=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -37,7 +38,8 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1):
                "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
                os.path.join(ROOT, "tests", "mgpu_worker.py"), "--workers", str(n), "--gsize", str(m),
                "--iters", str(T), "--buckets", ",".join(map(str, buckets)), "--mode", str(mode),
-               "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--out", out]
+               "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
+               "--batch", str(batch), "--lag", str(lag), "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
             break
@@ -63,20 +65,23 @@ def _compare(got, want):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+@pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_two_gpus_one_worker_each(tmp_path, mode):
-    """n=2 (group_size=2 = n: full averaging, Ring-SGD special case) across 2 GPUs."""
+def test_two_gpus_one_worker_each(tmp_path, mode, fused):
+    """n=2 (group_size=2 = n: full averaging, Ring-SGD special case) across 2 GPUs, one fused
+    launch over all buckets (sesgd_sync_all) or one launch per bucket."""
     buckets = [100003, 7, 40000]
-    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode)
+    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused)
     x, v = _oracle(2, 2, sum(buckets), 6, mode)
     _compare(X, x)
     _compare(V, v)
 
 
-@pytest.mark.parametrize("n,m", [(4, 2), (8, 2), (8, 4), (4, 1)])
+@pytest.mark.parametrize("n,m", [(4, 2), (8, 2), (8, 4), (4, 1), (8, 8)])
 def test_two_gpus_resident_pairs(tmp_path, n, m):
-    """n/2 workers per GPU: groups mix local (same-GPU) and remote (NVLink) members; the
-    schedule changes every iteration, exercising the t-2 stage-reuse guard."""
+    """n/2 workers per GPU: groups mix co-resident members (read from the local stage) and
+    remote members (NVLink push); the schedule changes every iteration, exercising the
+    call-2 receive-slot guard."""
     buckets = [65537, 3, 20000]
     T = 7
     X, V = _launch(tmp_path, 2, n, m, T, buckets)
@@ -93,13 +98,23 @@ def test_two_gpus_small_grid_many_chunks(tmp_path):
     _compare(X, x)
 
 
-@pytest.mark.parametrize("variant", [1, 8, 32, 64])
-def test_two_gpus_kernel_variants(tmp_path, variant):
-    """Every one-shot kernel shape (threads per CTA x lookahead) gives the oracle's bits,
-    with a small grid so each CTA pipelines several chunks."""
-    buckets = [250001, 13]
-    X, V = _launch(tmp_path, 2, 4, 2, 5, buckets, grid=20, variant=variant)
+@pytest.mark.parametrize("variant,batch,lag", [(0, 1, 1), (0, 1, 5), (1, 1, 1), (8, 4, 2), (32, 16, 4),
+                                               (10, 64, 16), (3, 2, 8)])
+def test_two_gpus_kernel_variants(tmp_path, variant, batch, lag):
+    """COMM CTAs x chunks per release x fold lag: every pipeline shape gives the oracle's
+    bits, with a small grid so each CTA pipelines several chunks."""
+    buckets = [250001, 13, 70000]
+    X, V = _launch(tmp_path, 2, 4, 2, 5, buckets, grid=24, variant=variant, batch=batch, lag=lag)
     x, v = _oracle(4, 2, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_two_gpus_random_access_resume(tmp_path):
+    """begin_iter at t0 = 1000 (resume): the flags are keyed by call index, not t."""
+    buckets = [90001]
+    X, V = _launch(tmp_path, 2, 4, 2, 4, buckets, t0=1000)
+    x, v = _oracle(4, 2, sum(buckets), 4, 0, t0=1000)
     _compare(X, x)
     _compare(V, v)
 

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--lag", type=int, default=0)
+    ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--out", default="gpurun_out/k3_phases.json")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -54,7 +55,7 @@ def main():
             synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st.cuda_stream)
             synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, 0, st.cuda_stream)
     for t in range(3):
-        eng.step(t, 0.1, 0.9)
+        eng.step(t, 0.1, 0.9, fused=bool(a.fused))
     torch.cuda.synchronize()
     grid = C.sesgd_launch_grid(eng.ctx)
     C.sesgd_profile_read(eng.ctx, grid)  # reset
@@ -62,7 +63,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for t in range(3, 3 + a.iters):
-        eng.step(t, 0.1, 0.9)
+        eng.step(t, 0.1, 0.9, fused=bool(a.fused))
     e1.record()
     torch.cuda.synchronize()
     prof, comm = C.sesgd_profile_read(eng.ctx, grid)
