@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
     p.add_argument("--comm-batch", type=int, default=0)
     p.add_argument("--fold-lag", type=int, default=0)
+    p.add_argument("--grid", type=int, default=0, help="CTAs per one-shot launch (0 = auto)")
     return p.parse_args()
 
 
@@ -77,8 +78,8 @@ def traffic_for(kernel: str, workload: str):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
-    d = json.load(open(path))
-    return d.get(f"{workload}/{kernel}")
+    d = json.load(open(path)).get(f"{workload}/{kernel}")
+    return None if d is None else d["bytes_per_launch"]
 
 
 class ClockSampler:
@@ -232,7 +233,7 @@ def run_sesgd(args):
     L = sum(buckets)
     mode = C.MODE_PARAM_AVG if args.mode == "param" else C.MODE_GRAD_AVG
     eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world,
-                      p2p_variant=args.p2p_variant, discard=args.discard,
+                      p2p_variant=args.p2p_variant, discard=args.discard, grid=args.grid,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch),
                                                  (C.OPT_FOLD_LAG, args.fold_lag)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT,
