@@ -61,7 +61,10 @@ extern "C" {
 /* ---- data paths for the intra-group exchange ---- */
 #define SESGD_PATH_AUTO 0     /* resident if all workers are local, else one-shot */
 #define SESGD_PATH_RESIDENT 1 /* all n workers on this GPU (1-GPU "k resident replicas") */
-#define SESGD_PATH_ONESHOT 2  /* NVLink P2P: every member pulls its m-1 peers' chunks */
+#define SESGD_PATH_ONESHOT 2  /* NVLink P2P: one handshake round, members push to each other */
+#define SESGD_PATH_RING 3     /* NVLink P2P, the paper's Ring-AllReduce inside each group: 2(m-1)
+                                 handshake steps (Eq. 2/3); one worker per GPU; for the
+                                 handshake / injected-latency comparison (config 4) */
 
 /* ---- options for sesgd_set_option ---- */
 #define SESGD_OPT_MODE 1       /* SESGD_MODE_*                                   (default 0) */

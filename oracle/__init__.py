@@ -70,6 +70,13 @@ def lib():
         L.orc_run_f64.argtypes = [i32, i32, u64, i64, i64, i64, P, u64, ctypes.c_double,
                                   ctypes.c_double, i32, P, P]
         L.orc_run_f64.restype = ctypes.c_int
+        L.orc_step_ring_f32.argtypes = [i32, i32, P, i64, P, P, P, ctypes.c_float, ctypes.c_float, i32]
+        L.orc_step_ring_f32.restype = ctypes.c_int
+        L.orc_slice_of.argtypes = [i64, i32, i64]
+        L.orc_slice_of.restype = i32
+        L.orc_run_ring_f32.argtypes = [i32, i32, u64, i64, i64, i64, i64, u64, ctypes.c_float,
+                                       ctypes.c_float, i32, P, P]
+        L.orc_run_ring_f32.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -148,6 +155,27 @@ def step(n, m, canon, x, v, g, lr, mu, mode=MODE_PARAM):
                                   float(lr), float(mu), mode))
     else:
         raise TypeError(x.dtype)
+
+
+def slice_of(L: int, m: int, e: int) -> int:
+    return int(lib().orc_slice_of(L, m, e))
+
+
+def step_ring(n, m, canon, x, v, g, lr, mu, mode=MODE_PARAM):
+    """One iteration with the group mean in Ring-AllReduce order (float32 arrays, in place)."""
+    canon = np.ascontiguousarray(canon, np.int32)
+    g = np.ascontiguousarray(g, np.float32)
+    assert x.dtype == np.float32 and x.flags.c_contiguous and v.flags.c_contiguous
+    _check(lib().orc_step_ring_f32(n, m, _ptr(canon), x.shape[-1], _ptr(x), _ptr(v), _ptr(g),
+                                   float(lr), float(mu), mode))
+
+
+def run_ring(n, m, seed, T, x, v, *, s_g, lr, mu, mode=MODE_PARAM, t0=0, e0=0):
+    """T ring-order iterations over one bucket (x, v: float32 (n, L) in place) whose
+    elements have global coordinates e0 .. e0 + L - 1."""
+    _check(lib().orc_run_ring_f32(n, m, seed, t0, T, x.shape[-1], e0, s_g, float(lr), float(mu), mode,
+                                  _ptr(x), _ptr(v)))
+    return x, v
 
 
 def run(n, m, seed, T, x, v, *, s_g, lr, mu, mode=MODE_PARAM, t0=0, coords=None):

@@ -232,6 +232,86 @@ int orc_step_f64(int32_t n, int32_t m, const int32_t *canon, int64_t L, double *
   return ORC_OK;
 }
 
+/* ---- the group mean by Ring-AllReduce in ring order (Sec. 2.2) ---- */
+int32_t orc_slice_of(int64_t L, int32_t m, int64_t e) {
+  /* slice s = [floor(s L / m), floor((s+1) L / m)): the largest s with floor(s L / m) <= e */
+  int32_t s = 0;
+  while (s + 1 < m && ((s + 1) * L) / m <= e) ++s;
+  return s;
+}
+
+int orc_step_ring_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                      const float *g, float lr, float mu, int32_t mode) {
+  if (n < 1 || m < 1 || m > n || L < 0 || !canon) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  int32_t k = n / m;
+  const float fm = (float)m;
+  float *pay = (float *)malloc(sizeof(float) * (size_t)n * (size_t)(L > 0 ? L : 1));
+  if (mode == ORC_MODE_PARAM) {
+    /* Alg.1 lines 3-8: the payload is xh_i = x_i - eta (mu v_i + g_i) */
+    for (int32_t i = 0; i < n; ++i)
+      for (int64_t e = 0; e < L; ++e) {
+        size_t at = (size_t)i * (size_t)L + (size_t)e;
+        float mv = mu * v[at];
+        float vn = mv + g[at];
+        float step = lr * vn;
+        v[at] = vn;
+        pay[at] = x[at] - step;
+      }
+  } else if (mode == ORC_MODE_GRAD) {
+    memcpy(pay, g, sizeof(float) * (size_t)n * (size_t)L);
+  } else {
+    free(pay);
+    return ORC_EINVAL;
+  }
+  for (int32_t j = 0; j < k; ++j) {
+    const int32_t *G = canon + (size_t)j * m;
+    for (int64_t e = 0; e < L; ++e) {
+      /* Scatter-Reduce: the slice containing e starts at ring position s and travels the
+       * ring, each member adding its own value to what it received */
+      int32_t s = orc_slice_of(L, m, e);
+      float acc = pay[(size_t)G[s] * (size_t)L + (size_t)e];
+      for (int32_t t = 1; t < m; ++t) acc = acc + pay[(size_t)G[(s + t) % m] * (size_t)L + (size_t)e];
+      float mean = acc / fm; /* "division by m applied once after full accumulation" */
+      /* All-Gather: every member receives the same mean */
+      for (int32_t r = 0; r < m; ++r) {
+        size_t at = (size_t)G[r] * (size_t)L + (size_t)e;
+        if (mode == ORC_MODE_PARAM) {
+          x[at] = mean;
+        } else {
+          float mv = mu * v[at];
+          float vn = mv + mean;
+          float step = lr * vn;
+          v[at] = vn;
+          x[at] = x[at] - step;
+        }
+      }
+    }
+  }
+  free(pay);
+  return ORC_OK;
+}
+
+int orc_run_ring_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t L,
+                     int64_t e0, uint64_t s_g, float lr, float mu, int32_t mode, float *x, float *v) {
+  if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || L < 0) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  float *g = (float *)malloc(sizeof(float) * (size_t)n * (size_t)(L > 0 ? L : 1));
+  int32_t *canon = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int rc = ORC_OK;
+  for (int64_t t = t0; t < t0 + T && rc == ORC_OK; ++t) {
+    for (int32_t i = 0; i < n; ++i) {
+      uint64_t key = synth_grad_key(s_g, i, t);
+      for (int64_t e = 0; e < L; ++e) g[(size_t)i * (size_t)L + (size_t)e] = synth_grad(key, e0 + e);
+    }
+    rc = orc_groups(seed, t, n, m, NULL, canon, NULL);
+    if (rc == ORC_OK) rc = orc_step_ring_f32(n, m, canon, L, x, v, g, lr, mu, mode);
+  }
+  free(g);
+  free(canon);
+  return rc;
+}
+
 /* ---- T iterations with synthetic gradients at chosen coordinates ---- */
 int orc_run_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                 const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode, float *x,

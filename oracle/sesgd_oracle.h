@@ -58,6 +58,19 @@ int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x
 int orc_step_f64(int32_t n, int32_t m, const int32_t *canon, int64_t L, double *x, double *v,
                  const double *g, double lr, double mu, int32_t mode);
 
+/* The same iteration with the group mean computed by the paper's Ring-AllReduce (Sec. 2.2,
+ * P:99-104) in ring order: members in ascending id form the ring; element e lies in slice
+ * s = the slice of SPEC slice_bounds ([floor(sL/m), floor((s+1)L/m))) containing
+ * it, and its sum is accumulated starting at ring position s: ((xh_s + xh_{s+1}) + ...) +
+ * xh_{s+m-1} (positions mod m), then divided once by m.  Equals orc_step_f32 for m <= 2. */
+int orc_step_ring_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                      const float *g, float lr, float mu, int32_t mode);
+/* slice of element e in [0, L) split into m slices */
+int32_t orc_slice_of(int64_t L, int32_t m, int64_t e);
+/* T ring-order iterations over ONE bucket of L elements at global coordinates e0..e0+L-1 */
+int orc_run_ring_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t L,
+                     int64_t e0, uint64_t s_g, float lr, float mu, int32_t mode, float *x, float *v);
+
 /* T iterations t0..t0+T-1 with synthetic gradients (synth_gen.h) at S global
  * coordinates coords[0..S-1] (coordinates are independent, so any subset of the
  * full problem replays exactly).  x, v: [n*S] in/out.  coords==NULL -> 0..S-1. */

@@ -80,6 +80,27 @@ struct P2PArgs {
   int8_t canon[SESGD_MAX_WORKERS];           // canonical groups of the iteration
   int8_t group_of[SESGD_MAX_WORKERS];
 };
+// K5: paper-faithful Ring-AllReduce inside each group (one worker per GPU), see ring.cu.
+struct RingArgs {
+  float *x, *v;                     // this bucket's buffers of the (single) local worker
+  const float *g;
+  char *ws[SESGD_MAX_RANKS];
+  int64_t numel;
+  int64_t rbuf_off;                 // byte offset of this bucket's receive buffers
+  int64_t slice_cap;                // floats per (parity, step) receive buffer
+  int64_t rflag_off, rcons_off;     // byte offsets: flags [2][NB][steps][grid], consumed [NB][grid]
+  int64_t call;
+  uint64_t timeout_ns, hop_delay_ns;
+  unsigned long long *err_host;
+  unsigned int *abort_dev;
+  float lr, mu;
+  int parity, steps, m, pos, grid, my_rank, bucket, nbuckets;
+  int8_t ring_rank[SESGD_MAX_WORKERS];  // rank of ring position 0..m-1 (ascending worker id)
+};
+cudaError_t launch_ring(const RingArgs &a, int mode, cudaStream_t stream);
+int ring_block_threads();
+int ring_occupancy(int mode);
+
 // variant = COMM CTAs per launch (1..148); smem = guard cache bytes
 cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec, size_t smem,
                                cudaStream_t stream);
@@ -106,6 +127,7 @@ struct sesgd_bucket {
   int64_t nchunks = 0, chunk_base = 0;
   int64_t calls = 0;             // sync_step calls on this bucket (flag epochs, parity)
   int64_t seq_hist[2] = {0, 0};  // launch sequence numbers of the last two calls (by call parity)
+  int64_t ring_off = 0, ring_cap = 0;  // K5 receive buffers (bytes offset, floats per buffer)
 };
 
 struct sesgd_ctx {
@@ -141,6 +163,8 @@ struct sesgd_ctx {
           stage_off = 0, recv_off = 0, stage_slot_floats = 0, total_chunks = 0;
   int64_t seq = 0;  // one-shot launches so far (staged / consumed epochs)
   size_t guard_smem = 0;
+  int ring_grid = 0;                      // K5 (0: ring path unavailable for this layout)
+  int64_t rflag_off = 0, rcons_off = 0;
   sesgd::BucketMeta *d_meta = nullptr;  // device bucket tables (multi-GPU path)
   float **d_bx = nullptr, **d_bv = nullptr;
   const float **d_bg = nullptr;

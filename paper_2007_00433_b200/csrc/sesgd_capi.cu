@@ -134,6 +134,28 @@ void freeze_layout(sesgd_ctx *ctx) {
   ctx->stage_off = round_up(ctx->consumed_off + int64_t(r) * gc * 8, 4096);
   ctx->recv_off = ctx->stage_off + int64_t(r) * ctx->stage_slot_floats * 4;
   ctx->ws_bytes = ctx->recv_off + 2 * int64_t(r) * ctx->m * ctx->stage_slot_floats * 4;
+  // K5 ring (one worker per GPU only): per bucket 2 parities x 2(m-1) step buffers of one
+  // slice, flags [2][NB][steps][ring grid], consumed [NB][ring grid]
+  ctx->ring_grid = 0;
+  if (r == 1 && ctx->m >= 2) {
+    const int steps = 2 * (ctx->m - 1);
+    const int rgrid = ctx->sm_count * std::min(sesgd::ring_occupancy(SESGD_MODE_PARAM_AVG),
+                                               sesgd::ring_occupancy(SESGD_MODE_GRAD_AVG));
+    const int64_t nb = int64_t(ctx->buckets.size());
+    int64_t off = round_up(ctx->ws_bytes, 4096);
+    ctx->rflag_off = off;
+    off = round_up(off + 2 * nb * steps * rgrid * 8, 256);
+    ctx->rcons_off = off;
+    off = round_up(off + nb * rgrid * 8, 4096);
+    for (auto &bk : ctx->buckets) {
+      bk.ring_cap = round_up((bk.numel + ctx->m - 1) / ctx->m, 64);
+      bk.ring_off = off;
+      off += 2 * int64_t(steps) * bk.ring_cap * 4;
+    }
+    ctx->ws_bytes = off;
+    ctx->ring_grid = rgrid;
+    h = fnv(h, uint64_t(rgrid));
+  }
   ctx->layout_hash = h;
   ctx->layout_frozen = true;
 }
@@ -341,8 +363,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->mode = int(value);
       return SESGD_OK;
     case SESGD_OPT_PATH:
-      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_ONESHOT)
+      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_RING)
         return fail(ctx, SESGD_EINVAL, "unknown path");
+      if (ctx->peers && value != ctx->path)  // the consumption guards are per path
+        return fail(ctx, SESGD_ESTATE, "the path is fixed once peers attach");
       ctx->path = int(value);
       return SESGD_OK;
     case SESGD_OPT_TIMEOUT_MS:
@@ -597,6 +621,55 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel");
     b.stats.kernel_launches++;
     b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n;
+    return SESGD_OK;
+  }
+
+  if (path == SESGD_PATH_RING) {  // K5: paper-faithful ring inside each group
+    if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
+    if (ctx->n_local != 1 || ctx->ring_grid == 0)
+      return fail(ctx, SESGD_ENOTSUP, "the ring path needs one worker per GPU and group_size >= 2");
+    sesgd::RingArgs ra{};
+    ra.x = b.hx[0];
+    ra.v = b.hv[0];
+    ra.g = b.hg[0];
+    for (int r = 0; r < ctx->n_ranks; ++r) ra.ws[r] = ctx->ws[r];
+    ra.numel = b.numel;
+    ra.rbuf_off = b.ring_off;
+    ra.slice_cap = b.ring_cap;
+    ra.rflag_off = ctx->rflag_off;
+    ra.rcons_off = ctx->rcons_off;
+    ra.call = b.calls;
+    ra.timeout_ns = uint64_t(ctx->timeout_ms) * 1000000ULL;
+    ra.hop_delay_ns = uint64_t(ctx->hop_delay_ns);
+    ra.err_host = ctx->d_err;
+    ra.abort_dev = ctx->d_abort;
+    ra.lr = lr;
+    ra.mu = momentum;
+    ra.parity = int(b.calls & 1);
+    ra.steps = 2 * (ctx->m - 1);
+    ra.m = ctx->m;
+    ra.grid = ctx->ring_grid;
+    ra.my_rank = ctx->rank;
+    ra.bucket = bucket;
+    ra.nbuckets = int(ctx->buckets.size());
+    const int me = ctx->local_workers[0];
+    const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
+    for (int q = 0; q < ctx->m; ++q) {
+      ra.ring_rank[q] = ctx->worker_rank[G[q]];
+      if (G[q] == me) ra.pos = q;
+    }
+    cudaError_t e = sesgd::launch_ring(ra, ctx->mode, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch ring kernel");
+    b.seq_hist[b.calls & 1] = ctx->seq;  // keep the one-shot guard history consistent
+    b.calls++;
+    ctx->seq++;
+    b.stats.kernel_launches++;
+    b.stats.hbm_algo_bytes += 20 * b.numel;
+    if (ctx->m > 1) {
+      b.stats.handshake_rounds = 2 * (ctx->m - 1);  // Eq. 2 / Eq. 3: 2(m-1) per call
+      b.stats.flag_messages += 2 * int64_t(ctx->m - 1) * ctx->ring_grid;
+      b.stats.payload_bytes_in += 2 * int64_t(ctx->m - 1) * ((b.numel + ctx->m - 1) / ctx->m) * 4;
+    }
     return SESGD_OK;
   }
 

@@ -27,6 +27,8 @@ def main():
     p.add_argument("--grid", type=int, default=0)
     p.add_argument("--variant", type=int, default=-1)
     p.add_argument("--fused", type=int, default=1)
+    p.add_argument("--path", type=int, default=0)
+    p.add_argument("--hop-ns", type=int, default=0)
     p.add_argument("--batch", type=int, default=0)
     p.add_argument("--lag", type=int, default=0)
     p.add_argument("--out", required=True)
@@ -39,7 +41,8 @@ def main():
     buckets = [int(b) for b in a.buckets.split(",")]
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
-                      grid=a.grid, timeout_ms=10000, p2p_variant=a.variant,
+                      grid=a.grid, timeout_ms=10000, p2p_variant=a.variant, path=a.path,
+                      hop_delay_ns=a.hop_ns,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag)) if v})
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):

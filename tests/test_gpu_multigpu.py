@@ -29,7 +29,7 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0):
+            lag=0, path=0, hop_ns=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -39,7 +39,8 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                os.path.join(ROOT, "tests", "mgpu_worker.py"), "--workers", str(n), "--gsize", str(m),
                "--iters", str(T), "--buckets", ",".join(map(str, buckets)), "--mode", str(mode),
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
-               "--batch", str(batch), "--lag", str(lag), "--out", out]
+               "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
+               "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
             break
@@ -125,3 +126,48 @@ def test_four_gpus(tmp_path):
     x, v = _oracle(8, 4, sum(buckets), 6, 0)
     _compare(X, x)
     _compare(V, v)
+
+
+def _oracle_ring(n, m, buckets, T, mode):
+    """ring-order oracle, bucket by bucket (each bucket is sliced separately)"""
+    X, V, e0 = [], [], 0
+    for L in buckets:
+        x = np.tile(synth.x0_host(L, e0=e0), (n, 1))
+        v = np.zeros_like(x)
+        oracle.run_ring(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, mode=mode, e0=e0)
+        X.append(x)
+        V.append(v)
+        e0 += L
+    return np.concatenate(X, axis=1), np.concatenate(V, axis=1)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_two_gpus_ring_path(tmp_path, mode):
+    """K5 (the paper's Ring-AllReduce inside the group, 2(m-1) handshakes) on 2 GPUs, m = n = 2:
+    ring order equals the ascending fold for two members, so it matches both oracles bit-exactly."""
+    buckets = [100003, 9, 4096]
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, mode, path=3)
+    x, v = _oracle(2, 2, sum(buckets), 5, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_four_gpus_ring_path(tmp_path, m):
+    """K5 on 4 GPUs: m = 4 is the Ring-SGD special case (ring over all workers, 6 handshakes);
+    bit-exact against the ring-order oracle, within the north-star tolerance of the fold."""
+    buckets = [70001, 33]
+    X, V = _launch(tmp_path, 4, 4, m, 4, buckets, path=3)
+    xr, vr = _oracle_ring(4, m, buckets, 4, 0)
+    _compare(X, xr)
+    _compare(V, vr)
+    x, _ = _oracle(4, m, sum(buckets), 4, 0)
+    np.testing.assert_allclose(X, x, rtol=1e-5, atol=1e-7)
+
+
+def test_two_gpus_ring_path_injected_latency(tmp_path):
+    """The injected per-hop delay changes only the timing, never the bits."""
+    buckets = [20000]
+    X, V = _launch(tmp_path, 2, 2, 2, 3, buckets, path=3, hop_ns=100000)
+    x, v = _oracle(2, 2, sum(buckets), 3, 0)
+    _compare(X, x)

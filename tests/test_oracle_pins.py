@@ -459,3 +459,55 @@ def test_latency_special_cases():
     # monotone in tau
     rs = [oracle.latency(16, 4, 1e5, 1e9, tau)["ratio"] for tau in (0, 1e-6, 1e-4, 1e-2)]
     assert rs == sorted(rs)
+
+
+# ------------------------------------------------------ ring-order group mean
+def test_slice_bounds_worked_example():
+    """SPEC collectives.slice_bounds (S:270-278): L=37, m=4 -> [0,9),[9,18),[18,27),[27,37);
+    L=10, m=2 -> [0,5),[5,10); L=3, m=4 -> sizes {0,1,1,1} (empty slice allowed)."""
+    def slices(L, m):
+        out = [[] for _ in range(m)]
+        for e in range(L):
+            out[oracle.slice_of(L, m, e)].append(e)
+        return out
+    s = slices(37, 4)
+    assert [(x[0], x[-1] + 1) for x in s] == [(0, 9), (9, 18), (18, 27), (27, 37)]
+    s = slices(10, 2)
+    assert [(x[0], x[-1] + 1) for x in s] == [(0, 5), (5, 10)]
+    assert sorted(len(x) for x in slices(3, 4)) == [0, 1, 1, 1]
+
+
+def test_ring_mean_worked_example():
+    """S:267 ([PAPER] handshake count, TRIVIAL mean): m=3, inputs [1,1],[2,2],[3,3] -> every
+    member gets [2,2].  As a step with lr=1, mu=0, x=0 the payload is -g."""
+    canon = np.array([0, 1, 2], np.int32)
+    x = np.zeros((3, 2), np.float32)
+    v = np.zeros_like(x)
+    g = -np.array([[1, 1], [2, 2], [3, 3]], np.float32)
+    oracle.step_ring(3, 3, canon, x, v, g, 1.0, 0.0)
+    assert np.array_equal(x, np.full((3, 2), 2.0, np.float32))
+
+
+def test_ring_order_equals_fold_for_two_members_and_is_close_otherwise():
+    """m <= 2: ring order and ascending fold are the same binary32 sum (commutativity);
+    m > 2: the two differ only by rounding (within the derived bound of the fp64 mean)."""
+    rng = np.random.default_rng(4)
+    for n, m in [(4, 2), (8, 2), (4, 4), (8, 4), (6, 3), (8, 8)]:
+        L = 1031
+        x0 = rng.standard_normal((n, L)).astype(np.float32)
+        g = rng.standard_normal((n, L)).astype(np.float32)
+        _, canon, _ = oracle.groups(SEED, 3, n, m)
+        xa, va = x0.copy(), np.zeros_like(x0)
+        xr, vr = x0.copy(), np.zeros_like(x0)
+        oracle.step(n, m, canon, xa, va, g, 0.1, 0.9)
+        oracle.step_ring(n, m, canon, xr, vr, g, 0.1, 0.9)
+        assert np.array_equal(va, vr)
+        if m <= 2:
+            assert np.array_equal(xa, xr)
+        else:
+            x64 = x0.astype(np.float64)
+            v64 = np.zeros_like(x64)
+            oracle.step(n, m, canon, x64, v64, g.astype(np.float64), 0.1, 0.9)
+            bound = (m + 2) * 2.0 ** -24 * np.abs(x64).max() * 2
+            assert np.abs(xr - x64).max() < bound and np.abs(xa - x64).max() < bound
+            assert not np.array_equal(xa, xr)  # the order really differs
