@@ -531,7 +531,7 @@ struct Split {
       }
       __syncthreads();  // every store of the batch precedes the releases (cumulativity)
       if (threadIdx.x < 32) {
-        hop_delay(a);
+        if (j == q) hop_delay(a);  // one handshake round per launch: delay once (config 4)
         const int n = nb * ns * a.m;
         for (int p = threadIdx.x; p < n; p += 32) {
           const int rr = p % a.m, s = (p / a.m) % ns;
@@ -568,9 +568,11 @@ struct Split {
 
   // release the ready flags of chunk g (warp 0, lane-parallel); every thread's stores of
   // chunk g precede this call through the __syncthreads that ends stage_push(g)
-  __device__ __forceinline__ void release_ready(int64_t g) const {
+  __device__ __forceinline__ void release_ready(int64_t g, bool first) const {
     if (threadIdx.x >= 32) return;
-    hop_delay(a);
+    // injected per-hop latency (config 4): the chunk flags of one launch are pipelined messages
+    // of ONE handshake round, so the delay is paid once, before the first of them
+    if (first) hop_delay(a);
     const uint64_t call1 = uint64_t(a.call) + 1;
     for (int p = threadIdx.x; p < a.r * a.m; p += 32) {
       const int s = p / a.m, rr = p % a.m;
@@ -706,7 +708,7 @@ struct Split {
     __syncthreads();
     uint64_t t_stage = 0, t_fold = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
     for (int64_t k = 0; k < nk + a.lag; ++k) {
-      if (k >= 1 && k <= nk) release_ready(first + (k - 1) * gc);
+      if (k >= 1 && k <= nk) release_ready(first + (k - 1) * gc, k == 1);
       if (k < nk) stage_push(first + k * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
@@ -720,7 +722,7 @@ struct Split {
         t0 = t1;
       }
     }
-    if (a.lag == 0) release_ready(first + (nk - 1) * gc);  // (lag >= 1 releases it in the loop)
+    if (a.lag == 0) release_ready(first + (nk - 1) * gc, nk == 1);  // (lag >= 1: in the loop)
     if (threadIdx.x < a.r)
       dev::st_release_sys(consumed(a.my_workers[threadIdx.x], i),
                           step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
