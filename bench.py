@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--comm-batch", type=int, default=0)
     p.add_argument("--fold-lag", type=int, default=0)
     p.add_argument("--grid", type=int, default=0, help="CTAs per one-shot launch (0 = auto)")
+    p.add_argument("--resident-unroll", type=int, default=0)
     return p.parse_args()
 
 
@@ -235,7 +236,8 @@ def run_sesgd(args):
     eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world,
                       p2p_variant=args.p2p_variant, discard=args.discard, grid=args.grid,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch),
-                                                 (C.OPT_FOLD_LAG, args.fold_lag)) if v},
+                                                 (C.OPT_FOLD_LAG, args.fold_lag),
+                                                 (C.OPT_RESIDENT_UNROLL, args.resident_unroll)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT,
                             "oneshot": C.PATH_ONESHOT}[args.path])
     r = eng.r
@@ -261,7 +263,7 @@ def run_sesgd(args):
 
     nb = len(buckets)
     # one-shot path: one fused launch per step (sesgd_sync_all); resident: one launch per bucket
-    fused = (world > 1 or args.path == "oneshot") and args.fused
+    fused = bool(args.fused)  # one sesgd_sync_all launch per step (all buckets)
     launches_per_step = 1 if fused else nb
     t_next = 0
     for _ in range(args.warmup):
@@ -306,7 +308,8 @@ def run_sesgd(args):
         achieved = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "peak_source": peak_src,
-                "algo_bytes_per_launch": [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets],
+                "algo_bytes_per_launch": ([BYTES_PER_WORKER_ELEM * L * r] if fused else
+                                          [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
         kernel = "k3_push"

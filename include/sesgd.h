@@ -85,6 +85,8 @@ extern "C" {
                                     peers attach */
 #define SESGD_OPT_FOLD_LAG 10    /* chunk steps a COMPUTE CTA stages ahead of its fold (1..64,
                                     default 4): covers the push + release latency */
+#define SESGD_OPT_RESIDENT_UNROLL 11 /* 1-GPU kernel, group size 2: independent items per
+                                    thread per trip (1, 2, 4, 8; 0 = default 4) */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

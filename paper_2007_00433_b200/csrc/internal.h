@@ -32,13 +32,20 @@ struct ResidentArgs {
   float lr, mu;
   int m;                  // group size
   int k;                  // groups
+  int nb;                 // 0: one bucket (x, v, g, numel); > 0: all buckets via the tables
+  int n_local;
+  float *const *bx;       // [nb * n_local] tables of the all-bucket launch
+  float *const *bv;
+  const float *const *bg;
+  const int64_t *numels;  // [nb]
   int8_t member_slot[SESGD_MAX_WORKERS];  // canonical order, mapped to local slots
 };
-// mode: SESGD_MODE_*; vec: all pointers 16-byte aligned; grid_x: CTAs per group.
-cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_x,
+// mode: SESGD_MODE_*; vec: all pointers 16-byte aligned; grid_x: CTAs per group;
+// unroll: 0 = default (SESGD_OPT_RESIDENT_UNROLL)
+cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_x, int unroll,
                             cudaStream_t stream);
 int resident_block_threads();
-int resident_occupancy(int mode, bool vec, int m);
+int resident_occupancy(int mode, bool vec, int m, int unroll);
 
 // K3: one-shot push over NVLink, SM-specialised (COMM CTAs + COMPUTE CTAs), see p2p.cu.
 struct BucketMeta {
@@ -142,6 +149,9 @@ struct sesgd_ctx {
   int comm_batch = 16;   // chunks per COMM release (SESGD_OPT_COMM_BATCH)
   int fold_lag = 4;      // SESGD_OPT_FOLD_LAG
   int discard = 1;      // SESGD_OPT_DISCARD
+  int resident_unroll = 0;  // SESGD_OPT_RESIDENT_UNROLL
+  int64_t *d_numels = nullptr;  // resident all-bucket launch: numel table [NB]
+  bool resident_tables_ok = false;
   // attach
   bool attached = false;
   int device = -1;

@@ -150,28 +150,29 @@ __device__ __forceinline__ void item_generic(const ResidentArgs &a, const int8_t
   }
 }
 
+// Default items per thread per trip.  M = 2 measured on B200 (cfg 2, all-bucket launch):
+// U = 1 (62 regs, 4 CTAs/SM) 0.962 of HBM peak > U = 8 0.947 > U = 4 (128 regs) 0.933 > U = 2.
 template <int M>
 struct Unroll {
-  static constexpr int value = M == 0 ? 1 : (M <= 2 ? 4 : (M <= 4 ? 2 : 1));
+  static constexpr int value = M == 0 ? 1 : (M == 1 ? 4 : (M == 2 ? 1 : (M <= 4 ? 2 : 1)));
 };
 
-template <int M, int W, bool GRAD>
-__global__ void __launch_bounds__(kThreads) k6_resident(const __grid_constant__ ResidentArgs a) {
-  const int m = M > 0 ? M : a.m;
-  const int8_t *mem = a.member_slot + blockIdx.y * m;
-  const int64_t nfull = a.numel / W;  // complete W-wide items
+// One bucket for the group `mem` of this CTA row: grid-stride over W-wide items.
+template <int M, int W, bool GRAD, int U>
+__device__ __forceinline__ void resident_bucket(const ResidentArgs &a, const int8_t *mem, int m,
+                                                float *const *tx, float *const *tv,
+                                                const float *const *tg, int64_t numel) {
+  const int64_t nfull = numel / W;  // complete W-wide items
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-
   if constexpr (M > 0) {
-    constexpr int U = Unroll<M>::value;
     float *xp[M], *vp[M];
     const float *gp[M];
 #pragma unroll
     for (int r = 0; r < M; ++r) {
-      xp[r] = a.x[mem[r]];
-      vp[r] = a.v[mem[r]];
-      gp[r] = a.g[mem[r]];
+      xp[r] = tx[mem[r]];
+      vp[r] = tv[mem[r]];
+      gp[r] = tg[mem[r]];
     }
     // U independent items per trip: all 3*M*U loads are issued before the first store.
     for (; i + (U - 1) * stride < nfull; i += U * stride) {
@@ -187,55 +188,88 @@ __global__ void __launch_bounds__(kThreads) k6_resident(const __grid_constant__ 
       it.finish(xp, vp, i * W, a.lr, a.mu);
     }
   } else {
-    for (; i < nfull; i += stride) item_generic<W, GRAD>(a, mem, m, i * W);
+    ResidentArgs b = a;  // runtime-m path reads the member tables through the args
+    b.x = tx;
+    b.v = tv;
+    b.g = tg;
+    for (; i < nfull; i += stride) item_generic<W, GRAD>(b, mem, m, i * W);
   }
   // ragged tail (numel % 4 elements) of the vector path
   if constexpr (W > 1) {
-    const int64_t tail = a.numel - nfull * W;
-    if (blockIdx.x == 0 && threadIdx.x < tail)
-      item_generic<1, GRAD>(a, mem, m, nfull * W + threadIdx.x);
+    const int64_t tail = numel - nfull * W;
+    if (blockIdx.x == 0 && threadIdx.x < tail) {
+      ResidentArgs b = a;
+      b.x = tx;
+      b.v = tv;
+      b.g = tg;
+      item_generic<1, GRAD>(b, mem, m, nfull * W + threadIdx.x);
+    }
   }
 }
 
-template <int M, int W, bool GRAD>
+// a.nb == 0: one bucket (a.x / a.v / a.g, a.numel).  a.nb > 0: every bucket of the iteration
+// in one launch (tables bx/bv/bg[b * n_local + slot], numels[b]); elements are independent, so
+// CTAs flow from one bucket into the next without any barrier (one launch tail per iteration).
+template <int M, int W, bool GRAD, int U>
+__global__ void __launch_bounds__(kThreads) k6_resident(const __grid_constant__ ResidentArgs a) {
+  const int m = M > 0 ? M : a.m;
+  const int8_t *mem = a.member_slot + blockIdx.y * m;
+  if (a.nb == 0) {
+    resident_bucket<M, W, GRAD, U>(a, mem, m, a.x, a.v, a.g, a.numel);
+  } else {
+    for (int b = 0; b < a.nb; ++b)
+      resident_bucket<M, W, GRAD, U>(a, mem, m, a.bx + int64_t(b) * a.n_local,
+                                     a.bv + int64_t(b) * a.n_local, a.bg + int64_t(b) * a.n_local,
+                                     a.numels[b]);
+  }
+}
+
+template <int M, int W, bool GRAD, int U>
 const void *kernel_ptr() {
-  return reinterpret_cast<const void *>(&k6_resident<M, W, GRAD>);
+  return reinterpret_cast<const void *>(&k6_resident<M, W, GRAD, U>);
 }
 
+// unroll 0 = default per M; 1 / 2 / 4 selectable for M = 2 (SESGD_OPT_RESIDENT_UNROLL)
 template <int W, bool GRAD>
-const void *pick_m(int m) {
+const void *pick_m(int m, int unroll) {
   switch (m) {
-    case 1: return kernel_ptr<1, W, GRAD>();
-    case 2: return kernel_ptr<2, W, GRAD>();
-    case 4: return kernel_ptr<4, W, GRAD>();
-    case 8: return kernel_ptr<8, W, GRAD>();
-    default: return kernel_ptr<0, W, GRAD>();
+    case 1: return kernel_ptr<1, W, GRAD, Unroll<1>::value>();
+    case 2:
+      switch (unroll) {
+        case 4: return kernel_ptr<2, W, GRAD, 4>();
+        case 2: return kernel_ptr<2, W, GRAD, 2>();
+        case 8: return kernel_ptr<2, W, GRAD, 8>();
+        default: return kernel_ptr<2, W, GRAD, Unroll<2>::value>();
+      }
+    case 4: return kernel_ptr<4, W, GRAD, Unroll<4>::value>();
+    case 8: return kernel_ptr<8, W, GRAD, Unroll<8>::value>();
+    default: return kernel_ptr<0, W, GRAD, Unroll<0>::value>();
   }
 }
 
-const void *pick(int mode, bool vec, int m) {
+const void *pick(int mode, bool vec, int m, int unroll) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
-  if (vec) return grad ? pick_m<4, true>(m) : pick_m<4, false>(m);
-  return grad ? pick_m<1, true>(m) : pick_m<1, false>(m);
+  if (vec) return grad ? pick_m<4, true>(m, unroll) : pick_m<4, false>(m, unroll);
+  return grad ? pick_m<1, true>(m, unroll) : pick_m<1, false>(m, unroll);
 }
 
 }  // namespace
 
 int resident_block_threads() { return kThreads; }
 
-int resident_occupancy(int mode, bool vec, int m) {
+int resident_occupancy(int mode, bool vec, int m, int unroll) {
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode, vec, m), kThreads, 0) !=
-      cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode, vec, m, unroll), kThreads,
+                                                    0) != cudaSuccess)
     return 1;
   return blocks > 0 ? blocks : 1;
 }
 
-cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_x,
+cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_x, int unroll,
                             cudaStream_t stream) {
   dim3 grid(grid_x, a.k), block(kThreads);
   void *args[] = {const_cast<ResidentArgs *>(&a)};
-  return cudaLaunchKernel(pick(mode, vec, a.m), grid, block, args, 0, stream);
+  return cudaLaunchKernel(pick(mode, vec, a.m, unroll), grid, block, args, 0, stream);
 }
 
 }  // namespace sesgd

@@ -160,6 +160,59 @@ void freeze_layout(sesgd_ctx *ctx) {
   ctx->layout_frozen = true;
 }
 
+// CTAs per group row of a resident launch covering `numel` elements (per bucket, or the
+// largest bucket of an all-bucket launch): SMs x occupancy spread over the k group rows
+int resident_grid_x(const sesgd_ctx *ctx, bool vec, int64_t numel) {
+  const int k = ctx->n / ctx->m;
+  const int threads = sesgd::resident_block_threads();
+  int target = ctx->sm_count * sesgd::resident_occupancy(ctx->mode, vec, ctx->m, ctx->resident_unroll);
+  if (ctx->grid_opt > 0) target = int(ctx->grid_opt);
+  int gx = (target + k - 1) / k;
+  const int64_t items = vec ? numel / 4 : numel;
+  const int64_t need = (items + threads - 1) / threads;
+  if (need < gx) gx = int(need > 0 ? need : 1);
+  return gx;
+}
+
+// device tables of the resident all-bucket launch: x/v/g pointers [NB * n_local], numel [NB]
+int upload_resident_tables(sesgd_ctx *ctx) {
+  const size_t nb = ctx->buckets.size();
+  const int r = ctx->n_local;
+  std::vector<float *> bx(nb * r), bv(nb * r);
+  std::vector<const float *> bg(nb * r);
+  std::vector<int64_t> numels(nb);
+  for (size_t b = 0; b < nb; ++b) {
+    const sesgd_bucket &bk = ctx->buckets[b];
+    numels[b] = bk.numel;
+    for (int s = 0; s < r; ++s) {
+      bx[b * r + s] = bk.hx[s];
+      bv[b * r + s] = bk.hv[s];
+      bg[b * r + s] = bk.hg[s];
+    }
+  }
+  if (ctx->d_bx) {
+    cudaFree(ctx->d_bx);
+    cudaFree(ctx->d_bv);
+    cudaFree(const_cast<float **>(ctx->d_bg));
+    ctx->d_bx = ctx->d_bv = nullptr;
+    ctx->d_bg = nullptr;
+  }
+  if (ctx->d_numels) cudaFree(ctx->d_numels);
+  ctx->d_numels = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bx), std::max<size_t>(nb * r, 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bv), std::max<size_t>(nb * r, 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bg), std::max<size_t>(nb * r, 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_numels), std::max<size_t>(nb, 1) * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bx, bx.data(), nb * r * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bv, bv.data(), nb * r * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(const_cast<float **>(ctx->d_bg), bg.data(), nb * r * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_numels, numels.data(), nb * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "resident bucket tables");
+  ctx->resident_tables_ok = true;
+  return SESGD_OK;
+}
+
 // device bucket tables of the one-shot kernel: meta[NB], x/v/g pointers [NB * r]
 int upload_tables(sesgd_ctx *ctx) {
   const size_t nb = ctx->buckets.size();
@@ -336,6 +389,7 @@ void sesgd_destroy(sesgd_ctx *ctx) {
   if (ctx->d_bx) cudaFree(ctx->d_bx);
   if (ctx->d_bv) cudaFree(ctx->d_bv);
   if (ctx->d_bg) cudaFree(const_cast<float **>(ctx->d_bg));
+  if (ctx->d_numels) cudaFree(ctx->d_numels);
   delete ctx;
 }
 
@@ -391,6 +445,11 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
     case SESGD_OPT_FOLD_LAG:
       if (value < 1 || value > 64) return fail(ctx, SESGD_EINVAL, "fold lag must be in [1, 64]");
       ctx->fold_lag = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_RESIDENT_UNROLL:
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+        return fail(ctx, SESGD_EINVAL, "resident unroll must be 0, 1, 2, 4 or 8");
+      ctx->resident_unroll = int(value);
       return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");
@@ -494,6 +553,7 @@ int sesgd_register_bucket(sesgd_ctx *ctx, int32_t bucket, int64_t numel, float *
   b.numel = numel;
   b.vec = vec;
   b.registered = true;
+  ctx->resident_tables_ok = false;  // the all-bucket resident launch re-uploads its tables
   if (ctx->layout_frozen) return upload_tables(ctx);  // re-registration after the layout froze
   return SESGD_OK;
 }
@@ -610,14 +670,8 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     a.m = ctx->m;
     a.k = ctx->n / ctx->m;
     for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
-    const int threads = sesgd::resident_block_threads();
-    int target = ctx->sm_count * sesgd::resident_occupancy(ctx->mode, b.vec, ctx->m);
-    if (ctx->grid_opt > 0) target = int(ctx->grid_opt);
-    int gx = (target + a.k - 1) / a.k;
-    const int64_t items = b.vec ? b.numel / 4 : b.numel;
-    const int64_t need = (items + threads - 1) / threads;
-    if (need < gx) gx = int(need > 0 ? need : 1);
-    cudaError_t e = sesgd::launch_resident(a, ctx->mode, b.vec, gx, st);
+    const int gx = resident_grid_x(ctx, b.vec, b.numel);
+    cudaError_t e = sesgd::launch_resident(a, ctx->mode, b.vec, gx, ctx->resident_unroll, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel");
     b.stats.kernel_launches++;
     b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n;
@@ -691,6 +745,39 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
   const bool all_local = (ctx->n_local == ctx->n);
   int path = ctx->path;
   if (path == SESGD_PATH_AUTO) path = all_local ? SESGD_PATH_RESIDENT : SESGD_PATH_ONESHOT;
+  if (path == SESGD_PATH_RESIDENT && all_local) {  // K6 over every bucket in one launch
+    if (!ctx->resident_tables_ok) {
+      rc = upload_resident_tables(ctx);
+      if (rc != SESGD_OK) return rc;
+    }
+    ResidentArgs a{};
+    bool vec = true;
+    int64_t biggest = 0;
+    for (auto &b : ctx->buckets) {
+      vec = vec && b.vec;
+      biggest = std::max(biggest, b.numel);
+    }
+    a.lr = lr;
+    a.mu = momentum;
+    a.m = ctx->m;
+    a.k = ctx->n / ctx->m;
+    a.nb = int(ctx->buckets.size());
+    a.n_local = ctx->n_local;
+    a.bx = ctx->d_bx;
+    a.bv = ctx->d_bv;
+    a.bg = ctx->d_bg;
+    a.numels = ctx->d_numels;
+    for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
+    cudaError_t e = sesgd::launch_resident(a, ctx->mode, vec, resident_grid_x(ctx, vec, biggest),
+                                           ctx->resident_unroll, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel (all buckets)");
+    for (auto &b : ctx->buckets) {
+      b.stats.sync_calls++;
+      b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n;
+    }
+    ctx->buckets[0].stats.kernel_launches++;
+    return SESGD_OK;
+  }
   bool fuse = (path == SESGD_PATH_ONESHOT) && ctx->peers;
   for (auto &b : ctx->buckets)  // one launch needs one shared call history
     fuse = fuse && b.calls == ctx->buckets[0].calls && b.seq_hist[0] == ctx->buckets[0].seq_hist[0] &&

@@ -26,10 +26,10 @@ def _cuda():
     return SESGDEngine
 
 
-def _run_gpu(n, m, buckets, T, mode, seed=42, slot_misalign=False):
+def _run_gpu(n, m, buckets, T, mode, seed=42, fused=True, unroll=0):
     SESGDEngine = _cuda()
     from paper_2007_00433_b200 import sesgd as C
-    eng = SESGDEngine(n, m, buckets, seed=seed, mode=mode)
+    eng = SESGDEngine(n, m, buckets, seed=seed, mode=mode, options={C.OPT_RESIDENT_UNROLL: unroll})
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     stream = torch.cuda.current_stream()
     for s in range(eng.r):
@@ -39,7 +39,7 @@ def _run_gpu(n, m, buckets, T, mode, seed=42, slot_misalign=False):
         for s, w in enumerate(eng.local_workers):
             for b, L in enumerate(buckets):
                 synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, stream.cuda_stream)
-        eng.step(t, LR, MU)
+        eng.step(t, LR, MU, fused=fused)
     torch.cuda.synchronize()
     eng.poll()
     X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
@@ -63,16 +63,29 @@ def _compare(got, want):
     assert mism == 0, f"{mism} elements differ in bits (within tolerance)"
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
-def test_config1_full_parity(mode):
-    """BASELINE configs[0]: n=4, group_size=2, 3 odd-sized buckets totalling 2^20, T=8."""
+def test_config1_full_parity(mode, fused):
+    """BASELINE configs[0]: n=4, group_size=2, 3 odd-sized buckets totalling 2^20, T=8; one
+    all-bucket launch per iteration (sesgd_sync_all) or one launch per bucket."""
     from paper_2007_00433_b200.workloads import CONFIG1_BUCKETS
     n, m, T = 4, 2, 8
-    X, V, stats = _run_gpu(n, m, CONFIG1_BUCKETS, T, mode)
+    X, V, stats = _run_gpu(n, m, CONFIG1_BUCKETS, T, mode, fused=fused)
     x, v = _run_oracle(n, m, sum(CONFIG1_BUCKETS), T, mode)
     _compare(X, x)
     _compare(V, v)
-    assert all(s["sync_calls"] == T and s["kernel_launches"] == T for s in stats)
+    assert all(s["sync_calls"] == T for s in stats)
+    assert sum(s["kernel_launches"] for s in stats) == (T if fused else T * len(CONFIG1_BUCKETS))
+
+
+@pytest.mark.parametrize("unroll", [2, 4, 8])
+def test_resident_unroll_variants(unroll):
+    """Every K6 unroll variant (SESGD_OPT_RESIDENT_UNROLL) gives the oracle's bits."""
+    buckets = [300007, 5, 40000]
+    X, V, _ = _run_gpu(8, 2, buckets, 4, oracle.MODE_PARAM, unroll=unroll)
+    x, v = _run_oracle(8, 2, sum(buckets), 4, oracle.MODE_PARAM)
+    _compare(X, x)
+    _compare(V, v)
 
 
 @pytest.mark.parametrize("n,m", [(4, 1), (4, 4), (8, 2), (8, 4), (8, 8), (6, 3), (16, 4), (12, 6)])
