@@ -82,6 +82,8 @@ struct P2PArgs {
   int discard;                      // drop dead stage / receive lines from L2 (no write-back)
   int8_t my_workers[SESGD_MAX_WORKERS];      // global ids of local slots
   int8_t my_pos[SESGD_MAX_WORKERS];          // position of each local slot in its group
+  int8_t slot_kind[SESGD_MAX_WORKERS];       // 0: group has remote members; 1: all-local group,
+                                             // first member; 2: all-local group, other member
   int8_t worker_rank[SESGD_MAX_WORKERS];
   int8_t worker_slot[SESGD_MAX_WORKERS];
   int8_t canon[SESGD_MAX_WORKERS];           // canonical groups of the iteration

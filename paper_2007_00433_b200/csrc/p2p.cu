@@ -582,9 +582,65 @@ struct Split {
     }
   }
 
+  // A group whose members all live on this GPU: the whole update in registers, like the
+  // 1-GPU kernel (no stage, no flags, no fold); run once, by the group's first member.
+  __device__ void local_group_update(const ChunkRef &c, const int8_t *G) const {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+      const int nv = (int)min(int64_t(W), c.e1 - e);
+      if (nv <= 0) continue;
+      float acc[W];
+      for (int rr = 0; rr < a.m; ++rr) {  // ascending member id
+        const int sl = a.worker_slot[G[rr]];
+        float gr[W];
+        load_m<W>(a.bg[c.b * a.r + sl] + e, gr, nv);
+        if constexpr (!GRAD) {
+          float v[W], x[W];
+          load_m<W>(a.bv[c.b * a.r + sl] + e, v, nv);
+          load_m<W>(a.bx[c.b * a.r + sl] + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            const float xh = dev::sgd(x[q], a.lr, v[q]);
+            acc[q] = (rr == 0) ? xh : __fadd_rn(acc[q], xh);
+          }
+          store_m<W>(a.bv[c.b * a.r + sl] + e, v, nv);
+        } else {
+#pragma unroll
+          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? gr[q] : __fadd_rn(acc[q], gr[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
+      for (int rr = 0; rr < a.m; ++rr) {
+        const int sl = a.worker_slot[G[rr]];
+        if constexpr (!GRAD) {
+          store_m<W>(a.bx[c.b * a.r + sl] + e, acc, nv);
+        } else {
+          float v[W], x[W];
+          load_m<W>(a.bv[c.b * a.r + sl] + e, v, nv);
+          load_m<W>(a.bx[c.b * a.r + sl] + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], acc[q]);
+            x[q] = dev::sgd(x[q], a.lr, v[q]);
+          }
+          store_m<W>(a.bv[c.b * a.r + sl] + e, v, nv);
+          store_m<W>(a.bx[c.b * a.r + sl] + e, x, nv);
+        }
+      }
+    }
+  }
+
   __device__ void stage_push(int64_t g) const {
     const ChunkRef c = locate(g);
     for (int s = 0; s < a.r; ++s) {
+      if (a.slot_kind[s] == 2) continue;  // done by its group's first member
+      if (a.slot_kind[s] == 1) {
+        local_group_update(c, group(a.my_workers[s]));
+        continue;
+      }
       float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
       const float *gs = a.bg[c.b * a.r + s];
       const int me = a.my_workers[s];
@@ -635,6 +691,7 @@ struct Split {
     }
     __syncthreads();
     for (int s = 0; s < a.r; ++s) {
+      if (a.slot_kind[s] != 0) continue;  // all-local group: already updated at stage time
       const int me = a.my_workers[s];
       const int8_t *G = group(me);
       float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
@@ -674,6 +731,7 @@ struct Split {
     if constexpr (W == 4) {
       if (a.discard && (threadIdx.x & 7) == 0) {
         for (int s = 0; s < a.r; ++s) {
+          if (a.slot_kind[s] != 0) continue;  // nothing staged for all-local groups
           const int me = a.my_workers[s];
           const int8_t *G = group(me);
 #pragma unroll

@@ -303,8 +303,14 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
     const int me = ctx->local_workers[s];
     a.my_workers[s] = int8_t(me);
     const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
-    for (int p = 0; p < ctx->m; ++p)
+    bool all_local = true;
+    for (int p = 0; p < ctx->m; ++p) {
       if (G[p] == me) a.my_pos[s] = int8_t(p);
+      all_local = all_local && ctx->worker_rank[G[p]] == ctx->rank;
+    }
+    // the DIRECT kernel updates an all-local group in registers, once, by its first member
+    const bool direct = (ctx->p2p_variant == 0);
+    a.slot_kind[s] = int8_t(!direct || !all_local ? 0 : (G[0] == me ? 1 : 2));
   }
   for (int i = 0; i < ctx->n; ++i) {
     a.worker_rank[i] = ctx->worker_rank[i];
