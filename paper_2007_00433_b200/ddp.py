@@ -1,0 +1,140 @@
+"""SESGDDataParallel: the gradient fusion buffer + backward/sync overlap (SURVEY NEXT-1,
+BASELINE config 5), the paper's integration "imitating the PyTorch DistributedDataParallel
+module and using register_hook ... to implement the overlap between computation and
+communication" (Fig. 1b).
+
+One SESGD worker per process / GPU.  The module's parameters and gradients become views into
+the SESGDEngine's flat per-bucket fp32 buffers (no pack copy): buckets in reverse registration
+order, the first capped at 1 MiB and the rest at 25 MiB, as torch DDP does.  A
+post-accumulate-grad hook per parameter counts the parameters of each bucket; once a bucket's
+gradients are complete (and every earlier bucket's, so every rank issues the same bucket
+order), `sesgd_sync_step(bucket)` is enqueued on a side stream behind an event of the backward
+stream, overlapping the rest of backward.  The SESGD kernel IS the optimizer step: it applies
+momentum SGD and the group average to the parameters in place (Eq. 6), so no torch optimizer
+runs.  `finish_step()` makes the compute stream wait for the side stream.  With
+static_graph=True (torch DDP's option of the same name) the first step records the gradient
+order and later steps keep one hook per bucket, on its last-accumulated parameter.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import sesgd as C
+from .engine import SESGDEngine
+from .workloads import assign_buckets
+
+
+def _like(flat: torch.Tensor, p: torch.Tensor) -> torch.Tensor:
+    """A view of the flat slice with p's shape and, when p is dense in channels_last, its
+    strides (so cuDNN sees the weight layout it was given)."""
+    if p.dim() == 4 and not p.is_contiguous() and p.is_contiguous(memory_format=torch.channels_last):
+        return flat.as_strided(p.size(), p.stride())
+    return flat.view(p.size())
+
+
+class SESGDDataParallel:
+    def __init__(self, module: torch.nn.Module, n: int, group_size: int, *, lr: float, momentum: float,
+                 rank: int = 0, world: int = 1, seed: int = 42, mode: int = C.MODE_PARAM_AVG,
+                 first_bucket_bytes: int = 1 << 20, bucket_bytes: int = 25 << 20, process_group=None,
+                 overlap: bool = True, static_graph: bool = False,
+                 engine_options: Optional[dict] = None):
+        if n != world:
+            raise ValueError("SESGDDataParallel runs one worker per process (n == world size)")
+        self.module = module
+        self.lr, self.momentum = lr, momentum
+        self.overlap = overlap
+        self.params = [p for p in module.parameters() if p.requires_grad]
+        sizes = [p.numel() for p in self.params]
+        self.bucket_params = assign_buckets(sizes, first_bucket_bytes, bucket_bytes)
+        bucket_sizes = [sum(sizes[i] for i in b) for b in self.bucket_params]
+        dev = self.params[0].device
+        self.engine = SESGDEngine(n, group_size, bucket_sizes, seed=seed, mode=mode, rank=rank,
+                                  world=world, device=dev.index, process_group=process_group,
+                                  options=engine_options)
+        self.bucket_of = {}
+        with torch.no_grad():
+            for b, idxs in enumerate(self.bucket_params):
+                off = 0
+                xb, gb = self.engine.x(0, b), self.engine.g(0, b)
+                for i in idxs:
+                    p = self.params[i]
+                    k = p.numel()
+                    view, gview = _like(xb[off:off + k], p), _like(gb[off:off + k], p)
+                    view.copy_(p.data)
+                    p.data = view   # parameter lives in the fusion buffer
+                    p.grad = gview  # gradient accumulates into it (in place)
+                    self.bucket_of[id(p)] = b
+                    off += k
+        self.pending = [0] * len(self.bucket_params)
+        self.next_bucket = 0
+        self.launched_in_backward = 0
+        self.side = torch.cuda.Stream(dev)
+        self.done_event = torch.cuda.Event()
+        self.t = 0
+        # static_graph (as torch DDP's): the autograd graph and its gradient order are the same
+        # every step, so after the first step only the last-accumulated parameter of each bucket
+        # keeps a hook (one Python call per bucket instead of one per parameter)
+        self.static_graph = static_graph
+        self._order: list = []
+        self._hooks = {}
+        if overlap:
+            self._hooks = {id(p): p.register_post_accumulate_grad_hook(self._on_grad) for p in self.params}
+        self._hooked = [len(b) for b in self.bucket_params]
+
+    # ------------------------------------------------------------------ per step
+    def begin_step(self, t: Optional[int] = None) -> None:
+        """Start iteration t: zero the gradient buffers, set the schedule of t."""
+        self.t = self.t if t is None else t
+        for g in self.engine.g_flat:
+            g.zero_()
+        self.engine.begin_iter(self.t)
+        self.pending = list(self._hooked)
+        self.next_bucket = 0
+        self.launched_in_backward = 0  # buckets whose sync was enqueued from a gradient hook
+        self._order = []
+
+    def _launch_ready(self) -> None:
+        # strictly in bucket order on every rank (peers' kernels wait on the same bucket)
+        while self.next_bucket < len(self.pending) and self.pending[self.next_bucket] == 0:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self.side.wait_event(ev)
+            self.engine.sync_step(self.next_bucket, self.lr, self.momentum, self.side)
+            self.next_bucket += 1
+
+    def _on_grad(self, p: torch.Tensor) -> None:
+        self.pending[self.bucket_of[id(p)]] -= 1
+        self._order.append(p)
+        self._launch_ready()
+        self.launched_in_backward = self.next_bucket
+
+    def finish_step(self) -> None:
+        """After backward: sync every remaining bucket, then order the compute stream after the
+        side stream (the next forward reads the updated parameters)."""
+        if not self.overlap:
+            self.pending = [0] * len(self.pending)
+        self._launch_ready()
+        if self.next_bucket != len(self.pending):
+            raise RuntimeError("some gradients never arrived; every parameter must receive a gradient")
+        self.done_event.record(self.side)
+        torch.cuda.current_stream().wait_event(self.done_event)
+        self.t += 1
+        if self.static_graph and self.overlap and len(self._hooks) == len(self.params):
+            self._trim_hooks()
+
+    def _trim_hooks(self) -> None:
+        last = {}
+        for p in self._order:  # firing order of the step just finished
+            last[self.bucket_of[id(p)]] = id(p)
+        keep = set(last.values())
+        for pid in [k for k in self._hooks if k not in keep]:
+            self._hooks.pop(pid).remove()
+        self._hooked = [1] * len(self.bucket_params)
+
+    def close(self) -> None:
+        for h in self._hooks.values():
+            h.remove()
+        self._hooks = {}
+        self.engine.close()

@@ -34,19 +34,30 @@ VGG16_TENSORS = (
 )
 
 
-def ddp_buckets(tensor_sizes: Sequence[int], first_cap_bytes: int = 1 << 20,
-                cap_bytes: int = 25 << 20, elem_bytes: int = 4) -> List[int]:
+def assign_buckets(tensor_sizes: Sequence[int], first_cap_bytes: int = 1 << 20,
+                   cap_bytes: int = 25 << 20, elem_bytes: int = 4) -> List[List[int]]:
+    """Tensor indices per bucket: reverse registration order, a bucket closes once it reaches
+    its cap (first 1 MiB, the rest 25 MiB)."""
     caps = (first_cap_bytes // elem_bytes, cap_bytes // elem_bytes)
-    out: List[int] = []
-    cur = 0
-    for s in reversed(tensor_sizes):
-        cur += int(s)
-        if cur >= caps[min(len(out), 1)]:
+    out: List[List[int]] = []
+    cur: List[int] = []
+    total = 0
+    for i in reversed(range(len(tensor_sizes))):
+        cur.append(i)
+        total += int(tensor_sizes[i])
+        if total >= caps[min(len(out), 1)]:
             out.append(cur)
-            cur = 0
+            cur, total = [], 0
     if cur:
         out.append(cur)
     return out
+
+
+def ddp_buckets(tensor_sizes: Sequence[int], first_cap_bytes: int = 1 << 20,
+                cap_bytes: int = 25 << 20, elem_bytes: int = 4) -> List[int]:
+    """Elements per bucket of assign_buckets."""
+    return [sum(int(tensor_sizes[i]) for i in b)
+            for b in assign_buckets(tensor_sizes, first_cap_bytes, cap_bytes, elem_bytes)]
 
 
 # BASELINE.json configs[0]: 3 buckets summing to 2^20 with odd sizes (vector tails)
