@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--p2p-variant", type=int, default=-1)
     p.add_argument("--discard", type=int, default=1)
-    p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot"])
+    p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot", "ring", "twoshot"])
     p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
     p.add_argument("--comm-batch", type=int, default=0)
     p.add_argument("--fold-lag", type=int, default=0)
@@ -238,8 +238,8 @@ def run_sesgd(args):
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch),
                                                  (C.OPT_FOLD_LAG, args.fold_lag),
                                                  (C.OPT_RESIDENT_UNROLL, args.resident_unroll)) if v},
-                      path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT,
-                            "oneshot": C.PATH_ONESHOT}[args.path])
+                      path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
+                            "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT}[args.path])
     r = eng.r
     stream = torch.cuda.current_stream(dev)
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
@@ -264,7 +264,8 @@ def run_sesgd(args):
     nb = len(buckets)
     # one-shot path: one fused launch per step (sesgd_sync_all); resident: one launch per bucket
     fused = bool(args.fused)  # one sesgd_sync_all launch per step (all buckets)
-    launches_per_step = 1 if fused else nb
+    launches_per_step = 1 if fused else nb  # event pairs per step
+    kernels_per_step = nb if args.path == "ring" else launches_per_step  # K5 launches per bucket
     t_next = 0
     for _ in range(args.warmup):
         eng.step(t_next, LR, MU, stream, fused=fused)
@@ -302,7 +303,7 @@ def run_sesgd(args):
     # dominant kernel roofline (all timed launches are the one fused kernel)
     hbm_peak, peak_src = measured_peaks()
     algo_bytes_per_step_gpu = BYTES_PER_WORKER_ELEM * L * r
-    resident = (world == 1 and args.path != "oneshot")
+    resident = (world == 1 and args.path in ("auto", "resident"))
     if resident:
         kernel = "k6_resident"
         achieved = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
@@ -312,7 +313,7 @@ def run_sesgd(args):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        kernel = "k3_push"
+        kernel = {"twoshot": "k4_twoshot", "ring": "k5_ring"}.get(args.path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
         # of them 2(s-1)/s * 4 B per element (co-resident members pre-combine); max over
@@ -388,7 +389,10 @@ def run_sesgd(args):
                              f"({nb} buckets, {L:,} fp32 per worker), {args.mode.upper()} mode, "
                              f"lr {LR}, momentum {MU}; {r} worker(s) resident per GPU"),
                 "n": n, "group_size": m, "workers_per_gpu": r,
-                "path": "resident (K6)" if resident else "one-shot push over NVLink P2P (K3)",
+                "path": "resident (K6)" if resident else {
+                    "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P (K4)",
+                    "ring": "ring inside each group over NVLink P2P (K5)"}.get(
+                        args.path, "one-shot push over NVLink P2P (K3)"),
                 "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush",
                 "parallelism": f"sesgd groups over {world} GPU(s)",
             },
@@ -397,7 +401,7 @@ def run_sesgd(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * launches_per_step,
+            "gpu_launches": K * kernels_per_step,
             "clocks": clocks,
             "handshakes": {
                 "sesgd_per_tensor": lat["sesgd_handshakes"], "ring_per_tensor": lat["ring_handshakes"],

@@ -59,12 +59,17 @@ extern "C" {
 #define SESGD_MODE_GRAD_AVG 1  /* Eq. 5 variant: average gradients, then local update */
 
 /* ---- data paths for the intra-group exchange ---- */
-#define SESGD_PATH_AUTO 0     /* resident if all workers are local, else one-shot */
+#define SESGD_PATH_AUTO 0     /* resident if all workers are local; two-shot with one worker per
+                                 GPU (and P2P variant 0); else one-shot */
 #define SESGD_PATH_RESIDENT 1 /* all n workers on this GPU (1-GPU "k resident replicas") */
 #define SESGD_PATH_ONESHOT 2  /* NVLink P2P: one handshake round, members push to each other */
 #define SESGD_PATH_RING 3     /* NVLink P2P, the paper's Ring-AllReduce inside each group: 2(m-1)
                                  handshake steps (Eq. 2/3); one worker per GPU; for the
                                  handshake / injected-latency comparison (config 4) */
+#define SESGD_PATH_TWOSHOT 4  /* NVLink P2P, two handshake rounds: reduce-scatter pushes to the
+                                 slice owners, all-gather pushes of the slice means; moves
+                                 2(m-1)/m of a bucket per GPU instead of one-shot's (m-1);
+                                 one worker per GPU (else SESGD_ENOTSUP) */
 
 /* ---- options for sesgd_set_option ---- */
 #define SESGD_OPT_MODE 1       /* SESGD_MODE_*                                   (default 0) */
@@ -84,9 +89,10 @@ extern "C" {
                                     amortises the system-scope release (default 16); fixed once
                                     peers attach */
 #define SESGD_OPT_FOLD_LAG 10    /* chunk steps a COMPUTE CTA stages ahead of its fold (1..64,
-                                    default 4): covers the push + release latency */
+                                    default 4): covers the push + release latency; the two-shot
+                                    path uses ceil(lag / 2) per round (stage -> reduce -> finish) */
 #define SESGD_OPT_RESIDENT_UNROLL 11 /* 1-GPU kernel, group size 2: independent items per
-                                    thread per trip (1, 2, 4, 8; 0 = default 4) */
+                                    thread per trip (1, 2, 4, 8; 0 = default 1) */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

@@ -119,6 +119,9 @@ int p2p_chunk_elems(int variant);
 int p2p_guard_pairs_max();
 size_t p2p_smem_bytes(int variant, int guard_pairs, int grid);  // COMM ring + mbarriers + guard cache
 int p2p_occupancy(int variant, int r, int mode, bool vec, size_t smem);
+// K4: two-shot (reduce-scatter + all-gather pushes), one worker per GPU, DIRECT grid (no COMM CTAs)
+cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
+int p2p_twoshot_occupancy(int mode, bool vec);
 
 }  // namespace sesgd
 

@@ -793,6 +793,239 @@ struct Split {
     }
   }
 
+  // ---------------------------------------------------------------- K4 TWO-SHOT (r == 1)
+  // Reduce-scatter + all-gather inside the group, both as NVLink pushes: the member at
+  // position j OWNS slice j of every chunk.  Per chunk g (epochs e1 = 2 call + 1, e2 = e1 + 1):
+  //  rs_stage(g): local step in registers; own slice -> own stage, slice j -> member a_j's
+  //               receive slot [my position] (NVLink); flag ready(a_j, g, my pos) = e1
+  //  reduce(g):   wait e1 from every peer; fold my slice over positions in ascending order
+  //               (= ascending worker id, the oracle's order) ; (/) m ; apply it to my x
+  //               (PARAM: x = mean; GRAD: momentum update with the mean gradient) and push the
+  //               mean to every peer's receive slot [my position] at my slice; ready = e2
+  //  finish(g):   wait e2 from every peer; apply the peers' slices (PARAM: x = mean slice;
+  //               GRAD: momentum update)
+  // A sender's RS data (the receiver's slice) and AG data (the sender's slice) share the
+  // receiver's slot [sender position] without overlap.  Bytes pushed per GPU per element:
+  // 2 (m-1)/m x 4 (one-shot: (m-1) x 4).  Flags are released at the top of the next chunk
+  // step (a system-scope release waits for the CTA's remote stores to drain; by then they
+  // have), reduce runs `lag` chunk steps after rs_stage and finish `lag` after reduce; every
+  // wait targets a flag released at the top of an earlier step or of this one: no deadlock.
+  __device__ __forceinline__ int ts_slice() const { return (int(kChunk) / a.m) & ~31; }
+  __device__ __forceinline__ int64_t ts_lo(int j, int64_t len) const {
+    return min(int64_t(j) * ts_slice(), len);
+  }
+  __device__ __forceinline__ int64_t ts_hi(int j, int64_t len) const {
+    return j == a.m - 1 ? len : min(int64_t(j + 1) * ts_slice(), len);
+  }
+
+  __device__ void ts_rs_stage(int64_t g) const {
+    const ChunkRef c = locate(g);
+    const int me = a.my_workers[0];
+    const int8_t *G = group(me);
+    const int p = a.my_pos[0];
+    const int S = ts_slice();
+    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
+    const float *gs = a.bg[c.b * a.r];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * W;  // offset inside the chunk
+      const int64_t e = c.e0 + o;
+      const int nv = (int)min(int64_t(W), c.e1 - e);
+      if (nv <= 0) continue;
+      float gr[W], val[W];
+      load_m<W>(gs + e, gr, nv);
+      if constexpr (!GRAD) {
+        float v[W], x[W];
+        load_m<W>(vs + e, v, nv);
+        load_m<W>(xs + e, x, nv);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          v[q] = dev::momentum(a.mu, v[q], gr[q]);
+          val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
+        }
+        store_m<W>(vs + e, v, nv);
+      } else {
+#pragma unroll
+        for (int q = 0; q < W; ++q) val[q] = gr[q];
+      }
+      const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
+      float *dst = (j == p) ? stage(0) : recv(G[j], p);
+      st_slot<W>(dst + c.soff + e, val, nv);
+    }
+    __syncthreads();  // every store of chunk g precedes its (deferred) flag release
+  }
+
+  // flags of the previous chunk step: RS of chunk grs, AG of chunk gag (-1: none)
+  __device__ __forceinline__ void ts_release(int64_t grs, int64_t gag, bool first_rs,
+                                             bool first_ag) const {
+    if (threadIdx.x >= 32) return;
+    if (first_rs || first_ag) hop_delay(a);  // one per handshake round and launch (config 4)
+    const int me = a.my_workers[0];
+    const int8_t *G = group(me);
+    const int p = a.my_pos[0];
+    const uint64_t e1 = 2 * uint64_t(a.call) + 1;
+    for (int q = threadIdx.x; q < 2 * a.m; q += 32) {
+      const int j = q % a.m;
+      const int64_t g = (q < a.m) ? grs : gag;
+      if (j == p || g < 0) continue;
+      dev::st_release_sys(ready(G[j], g, p), q < a.m ? e1 : e1 + 1);
+    }
+  }
+
+  __device__ __forceinline__ void ts_wait(int64_t g, uint64_t epoch) const {
+    if (threadIdx.x < 32) {
+      const int me = a.my_workers[0];
+      const int p = a.my_pos[0];
+      for (int j = threadIdx.x; j < a.m; j += 32)
+        if (j != p) wait_geq(a, ready(me, g, j), epoch, kWaitReady, me, j);
+    }
+    __syncthreads();
+  }
+
+  __device__ void ts_reduce(int64_t g) const {
+    const ChunkRef c = locate(g);
+    const int me = a.my_workers[0];
+    const int8_t *G = group(me);
+    const int p = a.my_pos[0];
+    ts_wait(g, 2 * uint64_t(a.call) + 1);
+    const int64_t len = c.e1 - c.e0, lo = ts_lo(p, len), hi = ts_hi(p, len);
+    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
+    for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
+      const int64_t e = c.e0 + o;
+      const int nv = (int)min(int64_t(W), hi - o);
+      float acc[W];
+      for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
+        const float *src = (rr == p) ? stage(0) : recv(me, rr);
+        float y[W];
+        ld_slot<W>(src + c.soff + e, y, nv);
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
+      for (int j = 0; j < a.m; ++j)  // all-gather: my slice's mean to every peer
+        if (j != p) st_slot<W>(recv(G[j], p) + c.soff + e, acc, nv);
+      if constexpr (!GRAD) {
+        store_m<W>(xs + e, acc, nv);
+      } else {
+        float v[W], x[W];
+        load_m<W>(vs + e, v, nv);
+        load_m<W>(xs + e, x, nv);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          v[q] = dev::momentum(a.mu, v[q], acc[q]);
+          x[q] = dev::sgd(x[q], a.lr, v[q]);
+        }
+        store_m<W>(vs + e, v, nv);
+        store_m<W>(xs + e, x, nv);
+      }
+    }
+    __syncthreads();  // my slice is folded: drop the dead lines (RS data, own stage)
+    if constexpr (W == 4) {
+      if (a.discard) {
+        for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
+          for (int rr = 0; rr < a.m; ++rr)
+            discard_l2(((rr == p) ? stage(0) : recv(me, rr)) + c.soff + c.e0 + o);
+      }
+    }
+    __syncthreads();  // the AG stores precede the (deferred) flag release
+  }
+
+  __device__ void ts_finish(int64_t g) const {
+    const ChunkRef c = locate(g);
+    const int me = a.my_workers[0];
+    const int p = a.my_pos[0];
+    ts_wait(g, 2 * uint64_t(a.call) + 2);
+    const int64_t len = c.e1 - c.e0;
+    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
+    for (int j = 0; j < a.m; ++j) {
+      if (j == p) continue;
+      const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
+      const float *src = recv(me, j) + c.soff;
+      for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
+        const int64_t e = c.e0 + o;
+        const int nv = (int)min(int64_t(W), hi - o);
+        float y[W];
+        ld_slot<W>(src + e, y, nv);
+        if constexpr (!GRAD) {
+          store_m<W>(xs + e, y, nv);
+        } else {
+          float v[W], x[W];
+          load_m<W>(vs + e, v, nv);
+          load_m<W>(xs + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], y[q]);
+            x[q] = dev::sgd(x[q], a.lr, v[q]);
+          }
+          store_m<W>(vs + e, v, nv);
+          store_m<W>(xs + e, x, nv);
+        }
+      }
+    }
+    __syncthreads();
+    if constexpr (W == 4) {
+      if (a.discard) {
+        for (int j = 0; j < a.m; ++j) {
+          if (j == p) continue;
+          const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
+          for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
+            discard_l2(recv(me, j) + c.soff + c.e0 + o);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void compute_twoshot(int i) const {
+    const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
+    const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
+    if (nk == 0) return;
+    const int me = a.my_workers[0];
+    const int8_t *G = group(me);
+    if (a.call >= 2 && threadIdx.x < 32) {  // guard: peers consumed their call-2 receive slots
+      const uint64_t need = step_epoch(a.prev2_epoch0, first + (nk - 1) * gc);
+      for (int j = threadIdx.x; j < a.m; j += 32)
+        if (G[j] != me) wait_geq(a, consumed(G[j], i), need, kWaitConsumed, G[j], j);
+    }
+    __syncthreads();
+    const int L = a.lag;
+    uint64_t t_stage = 0, t_red = 0, t_fin = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
+    for (int64_t k = 0; k < nk + 2 * L; ++k) {
+      const int64_t krs = k - 1, kag = k - 1 - L;  // pushes of the previous step
+      ts_release((krs >= 0 && krs < nk) ? first + krs * gc : -1,
+                 (kag >= 0 && kag < nk) ? first + kag * gc : -1, krs == 0, kag == 0);
+      if (k < nk) ts_rs_stage(first + k * gc);
+      if (a.prof) {
+        const uint64_t t1 = dev::globaltimer();
+        t_stage += t1 - t0;
+        t0 = t1;
+      }
+      if (k >= L && k - L < nk) ts_reduce(first + (k - L) * gc);
+      if (a.prof) {
+        const uint64_t t1 = dev::globaltimer();
+        t_red += t1 - t0;
+        t0 = t1;
+      }
+      if (k >= 2 * L && k - 2 * L < nk) ts_finish(first + (k - 2 * L) * gc);
+      if (a.prof) {
+        const uint64_t t1 = dev::globaltimer();
+        t_fin += t1 - t0;
+        t0 = t1;
+      }
+    }
+    if (threadIdx.x == 0)  // every read of my receive slots is done (guard of call + 2)
+      dev::st_release_sys(consumed(me, i), step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
+    if (a.prof && threadIdx.x == 0) {
+      uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
+      pr[0] += t_stage;
+      pr[1] += t_red;
+      pr[2] += t0 - tstart;
+      pr[3] += t_fin;
+      pr[7] += 1;
+    }
+  }
+
   // m == 1: no exchange, the local step is the whole update (x / 1 = x)
   __device__ void local_only() const {
     for (int64_t g = a.g0 + blockIdx.x; g < a.g1; g += a.grid) {
@@ -844,6 +1077,24 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
     p.compute_direct(blockIdx.x);
 }
 
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
+  const Split<W, GRAD> p(a);
+  if (a.m == 1)
+    p.local_only();
+  else
+    p.compute_twoshot(blockIdx.x);
+}
+
+const void *pick_twoshot(int mode, bool vec) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (vec)
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false>);
+}
+
 // variant 0: DIRECT push from the compute CTAs; variant >= 1: that many COMM CTAs
 const void *pick(int variant, int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
@@ -890,6 +1141,19 @@ cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
   return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
+}
+
+int p2p_twoshot_occupancy(int mode, bool vec) {
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_twoshot(mode, vec), kThreads, 0) !=
+      cudaSuccess)
+    return 1;
+  return blocks > 0 ? blocks : 1;
+}
+
+cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, cudaStream_t stream) {
+  void *args[] = {const_cast<P2PArgs *>(&a)};
+  return cudaLaunchKernel(pick_twoshot(mode, vec), dim3(a.grid), dim3(kThreads), args, 0, stream);
 }
 
 }  // namespace sesgd

@@ -78,6 +78,7 @@ void free_bucket(sesgd_bucket &b) {
 //   [recv_off, ..)      f32 recv    [2 parity][r slot][m position][region]
 // region = stage_slot_floats = sum over buckets of round_up(numel, 64).
 void freeze_layout(sesgd_ctx *ctx) {
+  if (ctx->path == SESGD_PATH_TWOSHOT) ctx->p2p_variant = 0;  // K4 runs on the DIRECT grid
   const int var = ctx->p2p_variant;
   const int chunk = sesgd::p2p_chunk_elems(var);
   const int r = ctx->n_local;
@@ -87,6 +88,9 @@ void freeze_layout(sesgd_ctx *ctx) {
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, true, smem));
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, false, smem));
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, false, smem));
+    if (var == 0 && r == 1)  // K4 (two-shot) shares the grid and the flag layout
+      for (int mode = 0; mode < 2; ++mode)
+        for (int vec = 0; vec < 2; ++vec) occ = std::min(occ, sesgd::p2p_twoshot_occupancy(mode, vec));
     return occ;
   };
   // every CTA must be co-resident (COMM and COMPUTE wait on each other): grid = SMs x
@@ -158,6 +162,16 @@ void freeze_layout(sesgd_ctx *ctx) {
   }
   ctx->layout_hash = h;
   ctx->layout_frozen = true;
+}
+
+// SESGD_PATH_AUTO: every worker on this GPU -> K6; one worker per GPU -> K4 two-shot (it moves
+// 2(m-1)/m of a bucket per GPU instead of (m-1), measured faster at m = 2 and 2x at m = 4);
+// several workers per GPU (or a COMM-CTA layout) -> K3 one-shot
+int resolve_path(const sesgd_ctx *ctx) {
+  if (ctx->path != SESGD_PATH_AUTO) return ctx->path;
+  if (ctx->n_local == ctx->n) return SESGD_PATH_RESIDENT;
+  if (ctx->n_local == 1 && ctx->m >= 2 && ctx->p2p_variant == 0) return SESGD_PATH_TWOSHOT;
+  return SESGD_PATH_ONESHOT;
 }
 
 // CTAs per group row of a resident launch covering `numel` elements (per bucket, or the
@@ -248,7 +262,8 @@ int upload_tables(sesgd_ctx *ctx) {
 
 // One one-shot launch over bucket `bucket` (>= 0) or over every bucket (-1, all buckets
 // share the same call history).  Host bookkeeping of calls / launch sequence follows.
-int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st) {
+int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st,
+                   bool twoshot = false) {
   const sesgd_bucket &ref = ctx->buckets[bucket >= 0 ? bucket : 0];
   P2PArgs a{};
   a.meta = ctx->d_meta;
@@ -291,9 +306,9 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.m = ctx->m;
   a.r = ctx->n_local;
   a.grid = ctx->grid;
-  a.comm_ctas = ctx->p2p_variant;
+  a.comm_ctas = twoshot ? 0 : ctx->p2p_variant;
   a.comm_batch = ctx->comm_batch;
-  a.lag = ctx->fold_lag;
+  a.lag = twoshot ? (ctx->fold_lag + 1) / 2 : ctx->fold_lag;  // two-shot: per round
   a.parity = int(call & 1);
   a.my_rank = ctx->rank;
   a.bucket = bucket;
@@ -321,8 +336,10 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   bool vec = true;
   for (size_t b = 0; b < ctx->buckets.size(); ++b)
     if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
-  cudaError_t e = sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec, ctx->guard_smem, st);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch one-shot kernel");
+  cudaError_t e = twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, st)
+                          : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
+                                                      ctx->guard_smem, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
   // bookkeeping
   int remote_peers = 0;
   for (int s = 0; s < ctx->n_local; ++s) {
@@ -338,7 +355,11 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
     bk.calls++;
     bk.stats.kernel_launches += (bucket >= 0 || b == 0) ? 1 : 0;
     bk.stats.hbm_algo_bytes += 20 * bk.numel * ctx->n_local;
-    if (ctx->m > 1) {
+    if (ctx->m > 1 && twoshot) {  // RS + AG flag per (chunk, peer); 2 (m-1)/m of the bucket in
+      bk.stats.handshake_rounds = 2;
+      bk.stats.flag_messages += 2 * int64_t(remote_peers) * bk.nchunks;
+      bk.stats.payload_bytes_in += 2 * int64_t(remote_peers) * bk.numel * 4 / ctx->m;
+    } else if (ctx->m > 1) {
       bk.stats.handshake_rounds = 1;
       bk.stats.flag_messages += int64_t(remote_peers) * bk.nchunks;  // one ready flag per chunk
       bk.stats.payload_bytes_in += int64_t(remote_peers) * bk.numel * 4;
@@ -423,10 +444,12 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->mode = int(value);
       return SESGD_OK;
     case SESGD_OPT_PATH:
-      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_RING)
+      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_TWOSHOT)
         return fail(ctx, SESGD_EINVAL, "unknown path");
       if (ctx->peers && value != ctx->path)  // the consumption guards are per path
         return fail(ctx, SESGD_ESTATE, "the path is fixed once peers attach");
+      if (value == SESGD_PATH_TWOSHOT && ctx->layout_frozen && ctx->p2p_variant != 0)
+        return fail(ctx, SESGD_ESTATE, "the two-shot path needs the DIRECT layout (P2P variant 0)");
       ctx->path = int(value);
       return SESGD_OK;
     case SESGD_OPT_TIMEOUT_MS:
@@ -661,8 +684,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
   if (b.numel == 0) return SESGD_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool all_local = (ctx->n_local == ctx->n);
-  int path = ctx->path;
-  if (path == SESGD_PATH_AUTO) path = all_local ? SESGD_PATH_RESIDENT : SESGD_PATH_ONESHOT;
+  const int path = resolve_path(ctx);
 
   if (path == SESGD_PATH_RESIDENT) {
     if (!all_local) return fail(ctx, SESGD_ESTATE, "resident path needs all n workers on this GPU");
@@ -733,9 +755,11 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     return SESGD_OK;
   }
 
-  // one-shot push over NVLink P2P
+  // one-shot (K3) or two-shot (K4) push over NVLink P2P
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
-  return launch_oneshot(ctx, bucket, lr, momentum, st);
+  if (path == SESGD_PATH_TWOSHOT && (ctx->n_local != 1 || ctx->p2p_variant != 0))
+    return fail(ctx, SESGD_ENOTSUP, "the two-shot path needs one worker per GPU");
+  return launch_oneshot(ctx, bucket, lr, momentum, st, path == SESGD_PATH_TWOSHOT);
 }
 
 int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
@@ -749,8 +773,7 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
   if (!std::isfinite(lr) || !std::isfinite(momentum))
     return fail(ctx, SESGD_EINVAL, "lr and momentum must be finite");
   const bool all_local = (ctx->n_local == ctx->n);
-  int path = ctx->path;
-  if (path == SESGD_PATH_AUTO) path = all_local ? SESGD_PATH_RESIDENT : SESGD_PATH_ONESHOT;
+  const int path = resolve_path(ctx);
   if (path == SESGD_PATH_RESIDENT && all_local) {  // K6 over every bucket in one launch
     if (!ctx->resident_tables_ok) {
       rc = upload_resident_tables(ctx);
@@ -784,7 +807,9 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     ctx->buckets[0].stats.kernel_launches++;
     return SESGD_OK;
   }
-  bool fuse = (path == SESGD_PATH_ONESHOT) && ctx->peers;
+  const bool twoshot = (path == SESGD_PATH_TWOSHOT);
+  bool fuse = (path == SESGD_PATH_ONESHOT || (twoshot && ctx->n_local == 1 && ctx->p2p_variant == 0)) &&
+              ctx->peers;
   for (auto &b : ctx->buckets)  // one launch needs one shared call history
     fuse = fuse && b.calls == ctx->buckets[0].calls && b.seq_hist[0] == ctx->buckets[0].seq_hist[0] &&
            b.seq_hist[1] == ctx->buckets[0].seq_hist[1];
@@ -796,7 +821,7 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     return SESGD_OK;
   }
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
-  return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream));
+  return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot);
 }
 
 int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libsesgd.so")
 OK, EINVAL, ENOTDIV, ESTATE, ECUDA, ETIMEOUT, ENOMEM, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7
 MAX_WORKERS, MAX_RANKS = 64, 8
 MODE_PARAM_AVG, MODE_GRAD_AVG = 0, 1
-PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT, PATH_RING = 0, 1, 2, 3
+PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT, PATH_RING, PATH_TWOSHOT = 0, 1, 2, 3, 4
 OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS, OPT_P2P_VARIANT, OPT_DISCARD = (
     1, 2, 3, 4, 5, 6, 7)
 OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL = 8, 9, 10, 11

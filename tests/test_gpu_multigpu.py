@@ -69,10 +69,10 @@ def _compare(got, want):
 @pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_two_gpus_one_worker_each(tmp_path, mode, fused):
-    """n=2 (group_size=2 = n: full averaging, Ring-SGD special case) across 2 GPUs, one fused
-    launch over all buckets (sesgd_sync_all) or one launch per bucket."""
+    """n=2 (group_size=2 = n: full averaging, Ring-SGD special case) across 2 GPUs through the
+    one-shot kernel (K3), one fused launch over all buckets (sesgd_sync_all) or one per bucket."""
     buckets = [100003, 7, 40000]
-    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused)
+    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused, path=2)
     x, v = _oracle(2, 2, sum(buckets), 6, mode)
     _compare(X, x)
     _compare(V, v)
@@ -171,3 +171,47 @@ def test_two_gpus_ring_path_injected_latency(tmp_path):
     X, V = _launch(tmp_path, 2, 2, 2, 3, buckets, path=3, hop_ns=100000)
     x, v = _oracle(2, 2, sum(buckets), 3, 0)
     _compare(X, x)
+
+
+# ---------------------------------------------------------------- K4 two-shot (path 4)
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_two_gpus_twoshot(tmp_path, mode, fused):
+    """K4 (reduce-scatter + all-gather pushes, two handshake rounds) on 2 GPUs, n = m = 2:
+    the slice owner folds in ascending worker id and divides once, so the bits are the oracle's."""
+    buckets = [100003, 7, 40000, 4096]
+    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused, path=4)
+    x, v = _oracle(2, 2, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("lag,grid", [(1, 8), (2, 24), (3, 0), (8, 16), (64, 4)])
+def test_two_gpus_twoshot_pipeline_shapes(tmp_path, lag, grid):
+    """Small grids (many chunks per CTA) x fold lags (1 .. 32 per round): every pipeline depth,
+    including ones longer than a CTA's chunk list, gives the oracle's bits."""
+    buckets = [250001, 13, 70000]
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, grid=grid, lag=lag, path=4)
+    x, v = _oracle(2, 2, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_two_gpus_twoshot_resume(tmp_path):
+    buckets = [90001]
+    X, V = _launch(tmp_path, 2, 2, 2, 4, buckets, t0=1000, path=4)
+    x, v = _oracle(2, 2, sum(buckets), 4, 0, t0=1000)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_four_gpus_twoshot(tmp_path, m, mode):
+    """K4 on 4 GPUs: m = 2 (groups change every iteration) and m = 4 (4 slice owners,
+    ragged last slice and bucket tails)."""
+    buckets = [200003, 5000, 1]
+    X, V = _launch(tmp_path, 4, 4, m, 6, buckets, mode, path=4)
+    x, v = _oracle(4, m, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
