@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--p2p-variant", type=int, default=-1)
     p.add_argument("--discard", type=int, default=1)
+    p.add_argument("--push-tma", type=int, default=0, help="two-shot: TMA bulk pushes (SESGD_OPT_PUSH_TMA)")
     p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot", "ring", "twoshot"])
     p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
     p.add_argument("--comm-batch", type=int, default=0)
@@ -237,7 +238,8 @@ def run_sesgd(args):
                       p2p_variant=args.p2p_variant, discard=args.discard, grid=args.grid,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch),
                                                  (C.OPT_FOLD_LAG, args.fold_lag),
-                                                 (C.OPT_RESIDENT_UNROLL, args.resident_unroll)) if v},
+                                                 (C.OPT_RESIDENT_UNROLL, args.resident_unroll),
+                                                 (C.OPT_PUSH_TMA, args.push_tma)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
                             "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT}[args.path])
     r = eng.r

@@ -93,6 +93,9 @@ extern "C" {
                                     path uses ceil(lag / 2) per round (stage -> reduce -> finish) */
 #define SESGD_OPT_RESIDENT_UNROLL 11 /* 1-GPU kernel, group size 2: independent items per
                                     thread per trip (1, 2, 4, 8; 0 = default 1) */
+#define SESGD_OPT_PUSH_TMA 12    /* two-shot kernel: 1 = NVLink pushes assembled in shared memory
+                                    and sent with cp.async.bulk (TMA) by one thread per CTA;
+                                    0 (default) = 128-bit stores from every thread */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

@@ -135,6 +135,10 @@ __device__ __forceinline__ void bulk_wait_upto(int newest) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// generic-proxy shared-memory writes (st.shared) become visible to a following bulk copy
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 }  // namespace dev
 }  // namespace sesgd

@@ -120,8 +120,9 @@ int p2p_guard_pairs_max();
 size_t p2p_smem_bytes(int variant, int guard_pairs, int grid);  // COMM ring + mbarriers + guard cache
 int p2p_occupancy(int variant, int r, int mode, bool vec, size_t smem);
 // K4: two-shot (reduce-scatter + all-gather pushes), one worker per GPU, DIRECT grid (no COMM CTAs)
-cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
-int p2p_twoshot_occupancy(int mode, bool vec);
+// tma: pushes staged in shared memory and sent with cp.async.bulk (SESGD_OPT_PUSH_TMA)
+cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream);
+int p2p_twoshot_occupancy(int mode, bool vec, bool tma);
 
 }  // namespace sesgd
 
@@ -155,6 +156,7 @@ struct sesgd_ctx {
   int fold_lag = 4;      // SESGD_OPT_FOLD_LAG
   int discard = 1;      // SESGD_OPT_DISCARD
   int resident_unroll = 0;  // SESGD_OPT_RESIDENT_UNROLL
+  int push_tma = 0;         // SESGD_OPT_PUSH_TMA (two-shot kernel)
   int64_t *d_numels = nullptr;  // resident all-bucket launch: numel table [NB]
   bool resident_tables_ok = false;
   // attach

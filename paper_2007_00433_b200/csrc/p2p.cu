@@ -818,14 +818,51 @@ struct Split {
     return j == a.m - 1 ? len : min(int64_t(j + 1) * ts_slice(), len);
   }
 
-  __device__ void ts_rs_stage(int64_t g) const {
+  // TMA variant (SESGD_OPT_PUSH_TMA): the remote part of a push is assembled in a shared-memory
+  // ring entry (one 16 KiB chunk image) and sent with one cp.async.bulk shared -> peer global per
+  // peer, issued by thread 0, so remote stores never occupy the LSU request slots the HBM
+  // stream needs.  Group q of the CTA's bulk groups uses entry q mod kPushRing; flags of a
+  // step's pushes are released two steps later, after cp.async.bulk.wait_group.
+  static constexpr int kPushRing = 3;
+
+  // bulk-copyable prefix of slice j (whole float4s; the ragged tail goes by plain stores)
+  __device__ __forceinline__ int64_t ts_bulk_hi(int j, int64_t len) const {
+    const int64_t lo = ts_lo(j, len);
+    return lo + ((ts_hi(j, len) - lo) & ~int64_t(3));
+  }
+
+  // issue (thread 0) the bulk copies of ring entry `ent` for slice range owner `j` (or every
+  // slice but mine when j < 0) to the peers' receive slots, and commit one group
+  __device__ __forceinline__ void ts_bulk_push(const ChunkRef &c, const float *ent, int j) const {
+    const int me = a.my_workers[0];
+    const int8_t *G = group(me);
+    const int p = a.my_pos[0];
+    const int64_t len = c.e1 - c.e0;
+    dev::fence_proxy_async_shared();
+    for (int q = 0; q < a.m; ++q) {
+      if (q == p) continue;
+      const int s = (j < 0) ? q : j;  // RS: peer q's slice; AG: my slice to every peer
+      const int64_t lo = ts_lo(s, len), bh = ts_bulk_hi(s, len);
+      if (bh > lo)
+        dev::bulk_s2g(recv(G[q], p) + c.soff + c.e0 + lo, ent + lo, uint32_t((bh - lo) * 4));
+    }
+    dev::bulk_commit();
+  }
+
+  template <bool TMA>
+  __device__ void ts_rs_stage(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     const int me = a.my_workers[0];
     const int8_t *G = group(me);
     const int p = a.my_pos[0];
     const int S = ts_slice();
+    const int64_t len = c.e1 - c.e0;
     float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
     const float *gs = a.bg[c.b * a.r];
+    if constexpr (TMA) {  // the entry's previous bulk group has finished reading it
+      if (threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();
+      __syncthreads();
+    }
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * W;  // offset inside the chunk
@@ -849,21 +886,45 @@ struct Split {
         for (int q = 0; q < W; ++q) val[q] = gr[q];
       }
       const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
-      float *dst = (j == p) ? stage(0) : recv(G[j], p);
-      st_slot<W>(dst + c.soff + e, val, nv);
+      if (j == p) {
+        st_slot<W>(stage(0) + c.soff + e, val, nv);
+      } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
+        st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
+      } else {
+        st_slot<W>(recv(G[j], p) + c.soff + e, val, nv);  // NVLink store
+      }
     }
-    __syncthreads();  // every store of chunk g precedes its (deferred) flag release
+    __syncthreads();  // every store of chunk g precedes its bulk push / (deferred) flag release
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) ts_bulk_push(c, ent, -1);
+    }
   }
 
-  // flags of the previous chunk step: RS of chunk grs, AG of chunk gag (-1: none)
-  __device__ __forceinline__ void ts_release(int64_t grs, int64_t gag, bool first_rs,
-                                             bool first_ag) const {
+  // flags of an earlier step's pushes: RS of chunk grs, AG of chunk gag (-1: none).  TMA: the
+  // pushes of the `newer` most recent bulk groups may still be in flight, all others must have
+  // landed first.
+  template <bool TMA>
+  __device__ __forceinline__ void ts_release(int64_t grs, int64_t gag, bool first_rs, bool first_ag,
+                                             int newer) const {
     if (threadIdx.x >= 32) return;
     if (first_rs || first_ag) hop_delay(a);  // one per handshake round and launch (config 4)
     const int me = a.my_workers[0];
     const int8_t *G = group(me);
     const int p = a.my_pos[0];
     const uint64_t e1 = 2 * uint64_t(a.call) + 1;
+    if constexpr (TMA) {
+      if (threadIdx.x == 0 && (grs >= 0 || gag >= 0)) {
+        dev::bulk_wait_upto(newer);  // those bulk writes are complete ...
+        dev::fence_proxy_async_global();
+        for (int q = 0; q < 2 * a.m; ++q) {  // ... before the flags (one releasing thread)
+          const int j = q % a.m;
+          const int64_t g = (q < a.m) ? grs : gag;
+          if (j == p || g < 0) continue;
+          dev::st_release_sys(ready(G[j], g, p), q < a.m ? e1 : e1 + 1);
+        }
+      }
+      return;
+    }
     for (int q = threadIdx.x; q < 2 * a.m; q += 32) {
       const int j = q % a.m;
       const int64_t g = (q < a.m) ? grs : gag;
@@ -882,13 +943,15 @@ struct Split {
     __syncthreads();
   }
 
-  __device__ void ts_reduce(int64_t g) const {
+  template <bool TMA>
+  __device__ void ts_reduce(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     const int me = a.my_workers[0];
     const int8_t *G = group(me);
     const int p = a.my_pos[0];
+    if (TMA && threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();  // entry free (+ sync below)
     ts_wait(g, 2 * uint64_t(a.call) + 1);
-    const int64_t len = c.e1 - c.e0, lo = ts_lo(p, len), hi = ts_hi(p, len);
+    const int64_t len = c.e1 - c.e0, lo = ts_lo(p, len), hi = ts_hi(p, len), bh = ts_bulk_hi(p, len);
     float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
     for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
       const int64_t e = c.e0 + o;
@@ -903,8 +966,12 @@ struct Split {
       }
 #pragma unroll
       for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
-      for (int j = 0; j < a.m; ++j)  // all-gather: my slice's mean to every peer
-        if (j != p) st_slot<W>(recv(G[j], p) + c.soff + e, acc, nv);
+      if (TMA && o + nv <= bh) {
+        st_slot<W>(ent + o, acc, nv);  // all-gather image, bulk-pushed below
+      } else {
+        for (int j = 0; j < a.m; ++j)  // all-gather: my slice's mean to every peer
+          if (j != p) st_slot<W>(recv(G[j], p) + c.soff + e, acc, nv);
+      }
       if constexpr (!GRAD) {
         store_m<W>(xs + e, acc, nv);
       } else {
@@ -921,6 +988,9 @@ struct Split {
       }
     }
     __syncthreads();  // my slice is folded: drop the dead lines (RS data, own stage)
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) ts_bulk_push(c, ent, p);
+    }
     if constexpr (W == 4) {
       if (a.discard) {
         for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
@@ -977,7 +1047,12 @@ struct Split {
     __syncthreads();
   }
 
-  __device__ void compute_twoshot(int i) const {
+  // LSU pushes: flags of step k-1's pushes at the top of step k (reduce `lag` >= 1 steps after
+  // rs_stage).  TMA pushes: flags of step k-2's pushes at the top of step k, once their bulk
+  // groups completed (lag >= 2).  Either way every wait targets a flag released at the top of
+  // this step or an earlier one.
+  template <bool TMA>
+  __device__ void compute_twoshot(int i, float *ring) const {
     const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
     const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
     if (nk == 0) return;
@@ -989,19 +1064,31 @@ struct Split {
         if (G[j] != me) wait_geq(a, consumed(G[j], i), need, kWaitConsumed, G[j], j);
     }
     __syncthreads();
-    const int L = a.lag;
+    const int L = TMA ? max(a.lag, 2) : a.lag;
+    const int D = TMA ? 2 : 1;  // release delay in steps
+    auto groups_of = [&](int64_t k) {  // bulk groups committed in step k
+      return int(k >= 0 && k < nk) + int(k >= L && k - L < nk);
+    };
+    uint32_t q = 0;  // bulk groups committed so far (uniform across the CTA)
     uint64_t t_stage = 0, t_red = 0, t_fin = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
     for (int64_t k = 0; k < nk + 2 * L; ++k) {
-      const int64_t krs = k - 1, kag = k - 1 - L;  // pushes of the previous step
-      ts_release((krs >= 0 && krs < nk) ? first + krs * gc : -1,
-                 (kag >= 0 && kag < nk) ? first + kag * gc : -1, krs == 0, kag == 0);
-      if (k < nk) ts_rs_stage(first + k * gc);
+      const int64_t krs = k - D, kag = k - D - L;  // pushes whose flags are due now
+      ts_release<TMA>((krs >= 0 && krs < nk) ? first + krs * gc : -1,
+                      (kag >= 0 && kag < nk) ? first + kag * gc : -1, krs == 0, kag == 0,
+                      groups_of(k - 1));
+      if (k < nk) {
+        ts_rs_stage<TMA>(first + k * gc, ring + (q % kPushRing) * kChunk);
+        q += TMA ? 1 : 0;
+      }
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_stage += t1 - t0;
         t0 = t1;
       }
-      if (k >= L && k - L < nk) ts_reduce(first + (k - L) * gc);
+      if (k >= L && k - L < nk) {
+        ts_reduce<TMA>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
+        q += TMA ? 1 : 0;
+      }
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_red += t1 - t0;
@@ -1014,6 +1101,7 @@ struct Split {
         t0 = t1;
       }
     }
+    if (TMA && threadIdx.x == 0) dev::bulk_wait_all();  // no bulk copy outlives the CTA
     if (threadIdx.x == 0)  // every read of my receive slots is done (guard of call + 2)
       dev::st_release_sys(consumed(me, i), step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
     if (a.prof && threadIdx.x == 0) {
@@ -1077,22 +1165,29 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
     p.compute_direct(blockIdx.x);
 }
 
-template <int W, bool GRAD>
+template <int W, bool GRAD, bool TMA>
 __global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
+  extern __shared__ __align__(128) unsigned char dsmem[];  // TMA: kPushRing chunk images
   const Split<W, GRAD> p(a);
   if (a.m == 1)
     p.local_only();
   else
-    p.compute_twoshot(blockIdx.x);
+    p.template compute_twoshot<TMA>(blockIdx.x, reinterpret_cast<float *>(dsmem));
 }
 
-const void *pick_twoshot(int mode, bool vec) {
+constexpr size_t kTwoshotTmaSmem = size_t(Split<4, false>::kPushRing) * size_t(kChunk) * 4;  // 48 KiB
+
+template <bool TMA>
+const void *pick_twoshot_t(int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
   if (vec)
-    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true>)
-                : reinterpret_cast<const void *>(&k4_twoshot<4, false>);
-  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true>)
-              : reinterpret_cast<const void *>(&k4_twoshot<1, false>);
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, TMA>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false, TMA>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, TMA>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false, TMA>);
+}
+const void *pick_twoshot(int mode, bool vec, bool tma) {
+  return tma ? pick_twoshot_t<true>(mode, vec) : pick_twoshot_t<false>(mode, vec);
 }
 
 // variant 0: DIRECT push from the compute CTAs; variant >= 1: that many COMM CTAs
@@ -1143,17 +1238,22 @@ cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec
   return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
 }
 
-int p2p_twoshot_occupancy(int mode, bool vec) {
+int p2p_twoshot_occupancy(int mode, bool vec, bool tma) {
+  const void *k = pick_twoshot(mode, vec, tma);
+  const size_t smem = tma ? kTwoshotTmaSmem : 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_twoshot(mode, vec), kThreads, 0) !=
-      cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, smem) != cudaSuccess)
     return 1;
   return blocks > 0 ? blocks : 1;
 }
 
-cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, cudaStream_t stream) {
+cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream) {
+  const void *k = pick_twoshot(mode, vec, tma);
+  const size_t smem = tma ? kTwoshotTmaSmem : 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
-  return cudaLaunchKernel(pick_twoshot(mode, vec), dim3(a.grid), dim3(kThreads), args, 0, stream);
+  return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
 }
 
 }  // namespace sesgd

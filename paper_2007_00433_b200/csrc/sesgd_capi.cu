@@ -90,7 +90,9 @@ void freeze_layout(sesgd_ctx *ctx) {
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, false, smem));
     if (var == 0 && r == 1)  // K4 (two-shot) shares the grid and the flag layout
       for (int mode = 0; mode < 2; ++mode)
-        for (int vec = 0; vec < 2; ++vec) occ = std::min(occ, sesgd::p2p_twoshot_occupancy(mode, vec));
+        for (int vec = 0; vec < 2; ++vec)
+          for (int tma = 0; tma < 2; ++tma)
+            occ = std::min(occ, sesgd::p2p_twoshot_occupancy(mode, vec, tma));
     return occ;
   };
   // every CTA must be co-resident (COMM and COMPUTE wait on each other): grid = SMs x
@@ -336,7 +338,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   bool vec = true;
   for (size_t b = 0; b < ctx->buckets.size(); ++b)
     if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
-  cudaError_t e = twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, st)
+  cudaError_t e = twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
                           : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
                                                       ctx->guard_smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
@@ -479,6 +481,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
         return fail(ctx, SESGD_EINVAL, "resident unroll must be 0, 1, 2, 4 or 8");
       ctx->resident_unroll = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_PUSH_TMA:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "push TMA must be 0 or 1");
+      ctx->push_tma = int(value);
       return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");

@@ -20,7 +20,7 @@ MODE_PARAM_AVG, MODE_GRAD_AVG = 0, 1
 PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT, PATH_RING, PATH_TWOSHOT = 0, 1, 2, 3, 4
 OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS, OPT_P2P_VARIANT, OPT_DISCARD = (
     1, 2, 3, 4, 5, 6, 7)
-OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL = 8, 9, 10, 11
+OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL, OPT_PUSH_TMA = 8, 9, 10, 11, 12
 
 # every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
 EXPORTED = (

@@ -31,6 +31,7 @@ def main():
     p.add_argument("--hop-ns", type=int, default=0)
     p.add_argument("--batch", type=int, default=0)
     p.add_argument("--lag", type=int, default=0)
+    p.add_argument("--tma", type=int, default=0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -43,7 +44,8 @@ def main():
     eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
                       grid=a.grid, timeout_ms=10000, p2p_variant=a.variant, path=a.path,
                       hop_delay_ns=a.hop_ns,
-                      options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag)) if v})
+                      options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
+                                                   (C.OPT_PUSH_TMA, a.tma)) if v})
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):

@@ -29,7 +29,7 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0, path=0, hop_ns=0):
+            lag=0, path=0, hop_ns=0, tma=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -40,6 +40,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--iters", str(T), "--buckets", ",".join(map(str, buckets)), "--mode", str(mode),
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
+               "--tma", str(tma),
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -213,5 +214,26 @@ def test_four_gpus_twoshot(tmp_path, m, mode):
     buckets = [200003, 5000, 1]
     X, V = _launch(tmp_path, 4, 4, m, 6, buckets, mode, path=4)
     x, v = _oracle(4, m, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("lag,grid", [(0, 0), (1, 8), (6, 24), (64, 4)])
+def test_two_gpus_twoshot_tma(tmp_path, mode, lag, grid):
+    """K4 with TMA bulk pushes (SESGD_OPT_PUSH_TMA): shared-memory chunk images sent with
+    cp.async.bulk, flags released after the bulk groups complete; ragged tails by plain stores."""
+    buckets = [250001, 13, 70000, 3]
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, mode, grid=grid, lag=lag, path=4, tma=1)
+    x, v = _oracle(2, 2, sum(buckets), 5, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_four_gpus_twoshot_tma(tmp_path, m):
+    buckets = [200003, 5000, 1]
+    X, V = _launch(tmp_path, 4, 4, m, 6, buckets, 0, path=4, tma=1)
+    x, v = _oracle(4, m, sum(buckets), 6, 0)
     _compare(X, x)
     _compare(V, v)

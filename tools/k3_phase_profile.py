@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Per-CTA phase timers of the one-shot K3 kernel (SESGD_OPT_PROFILE), multi-GPU.
+"""Per-CTA phase timers of the one-shot K3 / two-shot K4 kernels (SESGD_OPT_PROFILE), multi-GPU.
 
     python -m torch.distributed.run --nproc-per-node 2 tools/k3_phase_profile.py --workers 2
 
@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--lag", type=int, default=0)
     ap.add_argument("--fused", type=int, default=1)
+    ap.add_argument("--path", type=int, default=0, help="SESGD_PATH_* (4 = two-shot)")
+    ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--out", default="gpurun_out/k3_phases.json")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -46,7 +48,7 @@ def main():
     if a.lag:
         opts[C.OPT_FOLD_LAG] = a.lag
     eng = SESGDEngine(a.workers, a.gsize, buckets, rank=rank, world=world, p2p_variant=a.variant,
-                      options=opts)
+                      path=a.path, grid=a.grid, options=opts)
     C.sesgd_set_option(eng.ctx, C.OPT_PROFILE, 1)
     st = torch.cuda.current_stream()
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
@@ -76,7 +78,8 @@ def main():
                "comm_release": cm[:, 2].mean() / a.iters / 1e3,
                "comm_total": cm[:, 3].mean() / a.iters / 1e3,
                "compute_stage": cp[:, 0].mean() / a.iters / 1e3,
-               "compute_fold": cp[:, 1].mean() / a.iters / 1e3,
+               "compute_fold": cp[:, 1].mean() / a.iters / 1e3,  # two-shot: reduce
+               "compute_finish": cp[:, 3].mean() / a.iters / 1e3,  # two-shot only
                "compute_total": cp[:, 2].mean() / a.iters / 1e3,
                "compute_total_max": cp[:, 2].max() / a.iters / 1e3},
            "launches_seen": int(prof[:, 7].max()), "launches": launches}
