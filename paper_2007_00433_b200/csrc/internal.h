@@ -76,6 +76,8 @@ struct P2PArgs {
   int n, m, r, grid;
   int comm_ctas, comm_batch;        // COMM CTAs (blockIdx < comm_ctas) and chunks per release
   int lag;                          // COMPUTE folds chunk step k - lag after staging step k
+  int release_delay;                // two-shot: steps between a push and its flag release
+  int release_every;                // two-shot: chunk steps between flag-release batches
   int parity;                       // call & 1: receive slots / ready flags double buffer
   int my_rank;
   int bucket, nbuckets;             // bucket of a single-bucket launch, -1 for all buckets
@@ -157,6 +159,8 @@ struct sesgd_ctx {
   int discard = 1;      // SESGD_OPT_DISCARD
   int resident_unroll = 0;  // SESGD_OPT_RESIDENT_UNROLL
   int push_tma = 0;         // SESGD_OPT_PUSH_TMA (two-shot kernel)
+  int release_delay = 1;    // SESGD_OPT_RELEASE_DELAY (two-shot kernel)
+  int release_every = 3;    // SESGD_OPT_RELEASE_EVERY (two-shot kernel)
   int64_t *d_numels = nullptr;  // resident all-bucket launch: numel table [NB]
   bool resident_tables_ok = false;
   // attach

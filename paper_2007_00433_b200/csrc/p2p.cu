@@ -122,6 +122,9 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 __device__ __forceinline__ void st_release_gpu(uint64_t *p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // what a timed-out wait was waiting for (reported through sesgd_last_error)
 enum WaitKind : int { kWaitConsumed = 1, kWaitReady = 2, kWaitStaged = 3, kWaitSent = 4 };
@@ -900,36 +903,36 @@ struct Split {
     }
   }
 
-  // flags of an earlier step's pushes: RS of chunk grs, AG of chunk gag (-1: none).  TMA: the
-  // pushes of the `newer` most recent bulk groups may still be in flight, all others must have
-  // landed first.
+  // Flags of earlier pushes, one batch: RS of my chunk ordinals [rs0, rs1), AG of [ag0, ag1)
+  // (ordinal c = chunk first + c * gc).  ONE system-scope fence per batch (a fence waits for the
+  // SM's outstanding remote stores: measured ~8 us per chunk step under load), then relaxed
+  // flag stores spread over warp 0's lanes.  TMA: the `newer` most recent bulk groups may still
+  // be in flight, every older one must have landed first.
   template <bool TMA>
-  __device__ __forceinline__ void ts_release(int64_t grs, int64_t gag, bool first_rs, bool first_ag,
-                                             int newer) const {
-    if (threadIdx.x >= 32) return;
-    if (first_rs || first_ag) hop_delay(a);  // one per handshake round and launch (config 4)
+  __device__ __forceinline__ void ts_release(int64_t first, int64_t rs0, int64_t rs1, int64_t ag0,
+                                             int64_t ag1, int newer) const {
+    if (threadIdx.x >= 32 || (rs1 <= rs0 && ag1 <= ag0)) return;
+    if ((rs0 == 0 && rs1 > 0) || (ag0 == 0 && ag1 > 0)) hop_delay(a);  // once per round (config 4)
     const int me = a.my_workers[0];
     const int8_t *G = group(me);
     const int p = a.my_pos[0];
+    const int peers = a.m - 1;
     const uint64_t e1 = 2 * uint64_t(a.call) + 1;
     if constexpr (TMA) {
-      if (threadIdx.x == 0 && (grs >= 0 || gag >= 0)) {
+      if (threadIdx.x == 0) {
         dev::bulk_wait_upto(newer);  // those bulk writes are complete ...
         dev::fence_proxy_async_global();
-        for (int q = 0; q < 2 * a.m; ++q) {  // ... before the flags (one releasing thread)
-          const int j = q % a.m;
-          const int64_t g = (q < a.m) ? grs : gag;
-          if (j == p || g < 0) continue;
-          dev::st_release_sys(ready(G[j], g, p), q < a.m ? e1 : e1 + 1);
-        }
       }
-      return;
+      __syncwarp();
     }
-    for (int q = threadIdx.x; q < 2 * a.m; q += 32) {
-      const int j = q % a.m;
-      const int64_t g = (q < a.m) ? grs : gag;
-      if (j == p || g < 0) continue;
-      dev::st_release_sys(ready(G[j], g, p), q < a.m ? e1 : e1 + 1);
+    dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
+    const int64_t nrs = (rs1 - rs0) * peers, nall = nrs + (ag1 - ag0) * peers;
+    for (int64_t q = threadIdx.x; q < nall; q += 32) {
+      const int kind = q < nrs ? 0 : 1;
+      const int64_t qq = kind == 0 ? q : q - nrs;
+      const int64_t c = (kind == 0 ? rs0 : ag0) + qq / peers;
+      const int jj = int(qq % peers), j = jj < p ? jj : jj + 1;
+      st_relaxed_sys(ready(G[j], first + c * gc, p), e1 + kind);
     }
   }
 
@@ -1047,10 +1050,11 @@ struct Split {
     __syncthreads();
   }
 
-  // LSU pushes: flags of step k-1's pushes at the top of step k (reduce `lag` >= 1 steps after
-  // rs_stage).  TMA pushes: flags of step k-2's pushes at the top of step k, once their bulk
-  // groups completed (lag >= 2).  Either way every wait targets a flag released at the top of
-  // this step or an earlier one.
+  // Releases happen at the top of every R-th chunk step (R = release_every) and cover every push
+  // made at least D steps earlier (D = 1 for LSU stores; 2 for TMA, whose bulk groups of the
+  // last step may still be in flight).  A chunk pushed at step s is released by step
+  // s + D + R - 1, so with reduce L >= D + R - 1 steps after rs_stage (and finish L after
+  // reduce) every wait targets a flag released at the top of this step or an earlier one.
   template <bool TMA>
   __device__ void compute_twoshot(int i, float *ring) const {
     const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
@@ -1064,18 +1068,32 @@ struct Split {
         if (G[j] != me) wait_geq(a, consumed(G[j], i), need, kWaitConsumed, G[j], j);
     }
     __syncthreads();
-    const int L = TMA ? max(a.lag, 2) : a.lag;
-    const int D = TMA ? 2 : 1;  // release delay in steps
+    const int D = TMA ? max(a.release_delay, 2) : max(a.release_delay, 1);
+    const int R = max(a.release_every, 1);
+    const int L = max(a.lag, D + R - 1);
     auto groups_of = [&](int64_t k) {  // bulk groups committed in step k
       return int(k >= 0 && k < nk) + int(k >= L && k - L < nk);
     };
+    auto clampk = [&](int64_t v) { return v < 0 ? int64_t(0) : (v > nk ? nk : v); };
+    int64_t rs_out = 0, ag_out = 0;  // chunk ordinals whose RS / AG flags are released
     uint32_t q = 0;  // bulk groups committed so far (uniform across the CTA)
-    uint64_t t_stage = 0, t_red = 0, t_fin = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
+    uint64_t t_stage = 0, t_red = 0, t_fin = 0, t_rel = 0;
+    uint64_t t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
     for (int64_t k = 0; k < nk + 2 * L; ++k) {
-      const int64_t krs = k - D, kag = k - D - L;  // pushes whose flags are due now
-      ts_release<TMA>((krs >= 0 && krs < nk) ? first + krs * gc : -1,
-                      (kag >= 0 && kag < nk) ? first + kag * gc : -1, krs == 0, kag == 0,
-                      groups_of(k - 1));
+      if (k % R == 0) {  // pushes of steps <= k - D: RS of ordinals < k-D+1, AG of < k-D-L+1
+        const int64_t rs1 = clampk(k - D + 1), ag1 = clampk(k - D - L + 1);
+        int newer = 0;
+        if constexpr (TMA)
+          for (int64_t s2 = k - D + 1; s2 < k; ++s2) newer += groups_of(s2);
+        ts_release<TMA>(first, rs_out, rs1, ag_out, ag1, newer);
+        rs_out = rs1;
+        ag_out = ag1;
+      }
+      if (a.prof) {
+        const uint64_t t1 = dev::globaltimer();
+        t_rel += t1 - t0;
+        t0 = t1;
+      }
       if (k < nk) {
         ts_rs_stage<TMA>(first + k * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
@@ -1110,6 +1128,7 @@ struct Split {
       pr[1] += t_red;
       pr[2] += t0 - tstart;
       pr[3] += t_fin;
+      pr[4] += t_rel;
       pr[7] += 1;
     }
   }

@@ -311,6 +311,8 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.comm_ctas = twoshot ? 0 : ctx->p2p_variant;
   a.comm_batch = ctx->comm_batch;
   a.lag = twoshot ? (ctx->fold_lag + 1) / 2 : ctx->fold_lag;  // two-shot: per round
+  a.release_delay = ctx->release_delay;
+  a.release_every = ctx->release_every;
   a.parity = int(call & 1);
   a.my_rank = ctx->rank;
   a.bucket = bucket;
@@ -485,6 +487,14 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
     case SESGD_OPT_PUSH_TMA:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "push TMA must be 0 or 1");
       ctx->push_tma = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_RELEASE_DELAY:
+      if (value < 1 || value > 8) return fail(ctx, SESGD_EINVAL, "release delay must be in [1, 8]");
+      ctx->release_delay = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_RELEASE_EVERY:
+      if (value < 1 || value > 16) return fail(ctx, SESGD_EINVAL, "release interval must be in [1, 16]");
+      ctx->release_every = int(value);
       return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");

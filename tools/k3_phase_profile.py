@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--path", type=int, default=0, help="SESGD_PATH_* (4 = two-shot)")
     ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--rel-delay", type=int, default=0)
+    ap.add_argument("--rel-every", type=int, default=0)
     ap.add_argument("--out", default="gpurun_out/k3_phases.json")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -47,6 +49,10 @@ def main():
         opts[C.OPT_COMM_BATCH] = a.batch
     if a.lag:
         opts[C.OPT_FOLD_LAG] = a.lag
+    if a.rel_delay:
+        opts[C.OPT_RELEASE_DELAY] = a.rel_delay
+    if a.rel_every:
+        opts[C.OPT_RELEASE_EVERY] = a.rel_every
     eng = SESGDEngine(a.workers, a.gsize, buckets, rank=rank, world=world, p2p_variant=a.variant,
                       path=a.path, grid=a.grid, options=opts)
     C.sesgd_set_option(eng.ctx, C.OPT_PROFILE, 1)
@@ -80,6 +86,7 @@ def main():
                "compute_stage": cp[:, 0].mean() / a.iters / 1e3,
                "compute_fold": cp[:, 1].mean() / a.iters / 1e3,  # two-shot: reduce
                "compute_finish": cp[:, 3].mean() / a.iters / 1e3,  # two-shot only
+               "compute_release": cp[:, 4].mean() / a.iters / 1e3,  # two-shot only
                "compute_total": cp[:, 2].mean() / a.iters / 1e3,
                "compute_total_max": cp[:, 2].max() / a.iters / 1e3},
            "launches_seen": int(prof[:, 7].max()), "launches": launches}
