@@ -98,10 +98,10 @@ extern "C" {
                                     0 (default) = 128-bit stores from every thread */
 #define SESGD_OPT_RELEASE_DELAY 13 /* two-shot kernel: chunk steps between a push and the
                                     system-scope release of its flag (1..8, default 1; TMA >= 2) */
-#define SESGD_OPT_RELEASE_EVERY 14 /* two-shot kernel: chunk steps between flag-release batches
-                                    (1..16, default 3); each batch is ONE system-scope fence
-                                    (~8 us under load) followed by relaxed flag stores; the
-                                    per-round lag is raised to at least delay + every - 1 */
+#define SESGD_OPT_RELEASE_EVERY 14 /* two-shot and DIRECT one-shot kernels: chunk steps between
+                                    flag-release batches (1..16, default 3); each batch is ONE
+                                    system-scope fence (~8 us under load) followed by relaxed
+                                    flag stores; the lag is raised to cover it */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

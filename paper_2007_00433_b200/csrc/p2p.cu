@@ -566,22 +566,27 @@ struct Split {
   // ---------------------------------------------------------------- DIRECT (no COMM CTAs)
   // Every CTA is a compute CTA that pushes its own x_hat to the remote members straight from
   // registers (remote stores are fire-and-forget), so nothing is ever re-read from the stage
-  // for sending.  The ready flags of chunk k are released at the start of chunk k+1's stage,
-  // when those stores have long drained, so the system-scope release costs little.
+  // for sending.  Ready flags go out in batches every R = release_every chunk steps, at the
+  // top of a step, covering every chunk staged before it: ONE system-scope fence per batch (a
+  // fence waits for the SM's outstanding remote stores, ~8 us under load), then relaxed stores.
 
-  // release the ready flags of chunk g (warp 0, lane-parallel); every thread's stores of
-  // chunk g precede this call through the __syncthreads that ends stage_push(g)
-  __device__ __forceinline__ void release_ready(int64_t g, bool first) const {
-    if (threadIdx.x >= 32) return;
+  // release the ready flags of my chunk ordinals [c0, c1) (chunk first + c * gc; warp 0,
+  // lane-parallel); every thread's stores of those chunks precede this call through the
+  // __syncthreads that ends stage_push
+  __device__ __forceinline__ void release_ready(int64_t first, int64_t c0, int64_t c1) const {
+    if (threadIdx.x >= 32 || c1 <= c0) return;
     // injected per-hop latency (config 4): the chunk flags of one launch are pipelined messages
     // of ONE handshake round, so the delay is paid once, before the first of them
-    if (first) hop_delay(a);
+    if (c0 == 0) hop_delay(a);
     const uint64_t call1 = uint64_t(a.call) + 1;
-    for (int p = threadIdx.x; p < a.r * a.m; p += 32) {
-      const int s = p / a.m, rr = p % a.m;
+    const int pairs = a.r * a.m;
+    dev::fence_acq_rel_sys();
+    for (int64_t q = threadIdx.x; q < (c1 - c0) * pairs; q += 32) {
+      const int64_t c = c0 + q / pairs;
+      const int p = int(q % pairs), s = p / a.m, rr = p % a.m;
       const int me = a.my_workers[s];
       const int w = group(me)[rr];
-      if (w != me && remote(w)) dev::st_release_sys(ready(w, g, a.my_pos[s]), call1);
+      if (w != me && remote(w)) st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), call1);
     }
   }
 
@@ -767,23 +772,31 @@ struct Split {
       }
     }
     __syncthreads();
+    // chunk c is staged at step c and released by step c + R (the first multiple of R above c),
+    // so the fold of chunk k - L at step k finds its flags out when L >= R
+    const int R = max(a.release_every, 1);
+    const int L = max(a.lag, R);
+    int64_t out = 0;  // chunk ordinals whose ready flags are released
     uint64_t t_stage = 0, t_fold = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
-    for (int64_t k = 0; k < nk + a.lag; ++k) {
-      if (k >= 1 && k <= nk) release_ready(first + (k - 1) * gc, k == 1);
+    for (int64_t k = 0; k < nk + L; ++k) {
+      if (k % R == 0 || k == nk) {
+        const int64_t c1 = k < nk ? k : nk;
+        release_ready(first, out, c1);
+        out = c1;
+      }
       if (k < nk) stage_push(first + k * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_stage += t1 - t0;
         t0 = t1;
       }
-      if (k >= a.lag) fold_direct(first + (k - a.lag) * gc);
+      if (k >= L) fold_direct(first + (k - L) * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_fold += t1 - t0;
         t0 = t1;
       }
     }
-    if (a.lag == 0) release_ready(first + (nk - 1) * gc, nk == 1);  // (lag >= 1: in the loop)
     if (threadIdx.x < a.r)
       dev::st_release_sys(consumed(a.my_workers[threadIdx.x], i),
                           step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
