@@ -59,17 +59,18 @@ extern "C" {
 #define SESGD_MODE_GRAD_AVG 1  /* Eq. 5 variant: average gradients, then local update */
 
 /* ---- data paths for the intra-group exchange ---- */
-#define SESGD_PATH_AUTO 0     /* resident if all workers are local; two-shot with one worker per
-                                 GPU (and P2P variant 0); else one-shot */
+#define SESGD_PATH_AUTO 0     /* resident if all workers are local; else two-shot (P2P variant 0),
+                                 one-shot with COMM CTAs (variant >= 1) */
 #define SESGD_PATH_RESIDENT 1 /* all n workers on this GPU (1-GPU "k resident replicas") */
 #define SESGD_PATH_ONESHOT 2  /* NVLink P2P: one handshake round, members push to each other */
 #define SESGD_PATH_RING 3     /* NVLink P2P, the paper's Ring-AllReduce inside each group: 2(m-1)
                                  handshake steps (Eq. 2/3); one worker per GPU; for the
                                  handshake / injected-latency comparison (config 4) */
-#define SESGD_PATH_TWOSHOT 4  /* NVLink P2P, two handshake rounds: reduce-scatter pushes to the
-                                 slice owners, all-gather pushes of the slice means; moves
-                                 2(m-1)/m of a bucket per GPU instead of one-shot's (m-1);
-                                 one worker per GPU (else SESGD_ENOTSUP) */
+#define SESGD_PATH_TWOSHOT 4  /* NVLink P2P, two handshake rounds: every member owns a slice of
+                                 each chunk; reduce-scatter pushes to remote slice owners, all-gather
+                                 pushes of the slice means (co-resident members are read / updated
+                                 in place); a remote member pair exchanges 2/m of a bucket instead of
+                                 one-shot's full copy; needs P2P variant 0 (else SESGD_ENOTSUP) */
 
 /* ---- options for sesgd_set_option ---- */
 #define SESGD_OPT_MODE 1       /* SESGD_MODE_*                                   (default 0) */

@@ -124,7 +124,7 @@ int p2p_occupancy(int variant, int r, int mode, bool vec, size_t smem);
 // K4: two-shot (reduce-scatter + all-gather pushes), one worker per GPU, DIRECT grid (no COMM CTAs)
 // tma: pushes staged in shared memory and sent with cp.async.bulk (SESGD_OPT_PUSH_TMA)
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream);
-int p2p_twoshot_occupancy(int mode, bool vec, bool tma);
+int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi);
 
 }  // namespace sesgd
 

@@ -809,7 +809,7 @@ struct Split {
     }
   }
 
-  // ---------------------------------------------------------------- K4 TWO-SHOT (r == 1)
+  // ---------------------------------------------------------------- K4 TWO-SHOT
   // Reduce-scatter + all-gather inside the group, both as NVLink pushes: the member at
   // position j OWNS slice j of every chunk.  Per chunk g (epochs e1 = 2 call + 1, e2 = e1 + 1):
   //  rs_stage(g): local step in registers; own slice -> own stage, slice j -> member a_j's
@@ -865,49 +865,68 @@ struct Split {
     dev::bulk_commit();
   }
 
-  template <bool TMA>
+  // is worker w on another GPU?  (one worker per GPU: every other member is)
+  template <bool MULTI>
+  __device__ __forceinline__ bool rem(int w) const {
+    return MULTI ? remote(w) : w != a.my_workers[0];
+  }
+
+  // ---- K4 with r >= 1 workers per GPU.  Slot s (worker me_s at position p_s of its group G_s)
+  // owns slice p_s of every chunk.  A member's x_hat for a slice owned by a co-resident worker
+  // (or itself) stays in its own stage, read in place by the owner; for a remote owner it is
+  // pushed to the owner's receive slot [p_s].  The owner applies the mean to co-resident members
+  // directly (their x, v are on this GPU) and pushes it to remote members.  Groups whose members
+  // all live here are updated in registers (slot_kind 1 / 2, as in K3).
+  template <bool TMA, bool MULTI>
   __device__ void ts_rs_stage(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
-    const int me = a.my_workers[0];
-    const int8_t *G = group(me);
-    const int p = a.my_pos[0];
     const int S = ts_slice();
     const int64_t len = c.e1 - c.e0;
-    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
-    const float *gs = a.bg[c.b * a.r];
-    if constexpr (TMA) {  // the entry's previous bulk group has finished reading it
+    if constexpr (TMA) {  // the entry's previous bulk group has finished reading it (r == 1)
       if (threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();
       __syncthreads();
     }
-#pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * W;  // offset inside the chunk
-      const int64_t e = c.e0 + o;
-      const int nv = (int)min(int64_t(W), c.e1 - e);
-      if (nv <= 0) continue;
-      float gr[W], val[W];
-      load_m<W>(gs + e, gr, nv);
-      if constexpr (!GRAD) {
-        float v[W], x[W];
-        load_m<W>(vs + e, v, nv);
-        load_m<W>(xs + e, x, nv);
-#pragma unroll
-        for (int q = 0; q < W; ++q) {
-          v[q] = dev::momentum(a.mu, v[q], gr[q]);
-          val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
-        }
-        store_m<W>(vs + e, v, nv);
-      } else {
-#pragma unroll
-        for (int q = 0; q < W; ++q) val[q] = gr[q];
+    for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
+      if (MULTI && a.slot_kind[s] == 2) continue;  // done by its group's first member
+      const int8_t *G = group(a.my_workers[s]);
+      if (MULTI && a.slot_kind[s] == 1) {
+        local_group_update(c, G);
+        continue;
       }
-      const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
-      if (j == p) {
-        st_slot<W>(stage(0) + c.soff + e, val, nv);
-      } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
-        st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
-      } else {
-        st_slot<W>(recv(G[j], p) + c.soff + e, val, nv);  // NVLink store
+      const int p = a.my_pos[s];
+      float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
+      const float *gs = a.bg[c.b * a.r + s];
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * W;  // offset inside the chunk
+        const int64_t e = c.e0 + o;
+        const int nv = (int)min(int64_t(W), c.e1 - e);
+        if (nv <= 0) continue;
+        float gr[W], val[W];
+        load_m<W>(gs + e, gr, nv);
+        if constexpr (!GRAD) {
+          float v[W], x[W];
+          load_m<W>(vs + e, v, nv);
+          load_m<W>(xs + e, x, nv);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
+          }
+          store_m<W>(vs + e, v, nv);
+        } else {
+#pragma unroll
+          for (int q = 0; q < W; ++q) val[q] = gr[q];
+        }
+        const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
+        const int w = G[j];
+        if (!rem<MULTI>(w)) {
+          st_slot<W>(stage(s) + c.soff + e, val, nv);  // read in place by the local owner
+        } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
+          st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
+        } else {
+          st_slot<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store
+        }
       }
     }
     __syncthreads();  // every store of chunk g precedes its bulk push / (deferred) flag release
@@ -917,19 +936,16 @@ struct Split {
   }
 
   // Flags of earlier pushes, one batch: RS of my chunk ordinals [rs0, rs1), AG of [ag0, ag1)
-  // (ordinal c = chunk first + c * gc).  ONE system-scope fence per batch (a fence waits for the
-  // SM's outstanding remote stores: measured ~8 us per chunk step under load), then relaxed
-  // flag stores spread over warp 0's lanes.  TMA: the `newer` most recent bulk groups may still
-  // be in flight, every older one must have landed first.
-  template <bool TMA>
+  // (ordinal c = chunk first + c * gc), for every (slot, remote member) pair.  ONE system-scope
+  // fence per batch (a fence waits for the SM's outstanding remote stores: measured ~8 us per
+  // chunk step under load), then relaxed flag stores spread over warp 0's lanes.  TMA (r == 1):
+  // the `newer` most recent bulk groups may still be in flight, every older one must have landed.
+  template <bool TMA, bool MULTI>
   __device__ __forceinline__ void ts_release(int64_t first, int64_t rs0, int64_t rs1, int64_t ag0,
                                              int64_t ag1, int newer) const {
     if (threadIdx.x >= 32 || (rs1 <= rs0 && ag1 <= ag0)) return;
     if ((rs0 == 0 && rs1 > 0) || (ag0 == 0 && ag1 > 0)) hop_delay(a);  // once per round (config 4)
-    const int me = a.my_workers[0];
-    const int8_t *G = group(me);
-    const int p = a.my_pos[0];
-    const int peers = a.m - 1;
+    const int pairs = (MULTI ? a.r : 1) * a.m;
     const uint64_t e1 = 2 * uint64_t(a.call) + 1;
     if constexpr (TMA) {
       if (threadIdx.x == 0) {
@@ -939,124 +955,158 @@ struct Split {
       __syncwarp();
     }
     dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
-    const int64_t nrs = (rs1 - rs0) * peers, nall = nrs + (ag1 - ag0) * peers;
+    const int64_t nrs = (rs1 - rs0) * pairs, nall = nrs + (ag1 - ag0) * pairs;
     for (int64_t q = threadIdx.x; q < nall; q += 32) {
       const int kind = q < nrs ? 0 : 1;
       const int64_t qq = kind == 0 ? q : q - nrs;
-      const int64_t c = (kind == 0 ? rs0 : ag0) + qq / peers;
-      const int jj = int(qq % peers), j = jj < p ? jj : jj + 1;
-      st_relaxed_sys(ready(G[j], first + c * gc, p), e1 + kind);
+      const int64_t c = (kind == 0 ? rs0 : ag0) + qq / pairs;
+      const int pr = int(qq % pairs), s = pr / a.m, j = pr % a.m;
+      if ((MULTI && a.slot_kind[s] != 0) || j == a.my_pos[s]) continue;
+      const int w = group(a.my_workers[s])[j];
+      if (rem<MULTI>(w)) st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), e1 + kind);
     }
   }
 
+  // every remote member's flag of chunk g (for every slot) reached `epoch`
+  template <bool MULTI>
   __device__ __forceinline__ void ts_wait(int64_t g, uint64_t epoch) const {
     if (threadIdx.x < 32) {
-      const int me = a.my_workers[0];
-      const int p = a.my_pos[0];
-      for (int j = threadIdx.x; j < a.m; j += 32)
-        if (j != p) wait_geq(a, ready(me, g, j), epoch, kWaitReady, me, j);
+      for (int pr = threadIdx.x; pr < (MULTI ? a.r : 1) * a.m; pr += 32) {
+        const int s = pr / a.m, j = pr % a.m;
+        if ((MULTI && a.slot_kind[s] != 0) || j == a.my_pos[s]) continue;
+        const int me = a.my_workers[s];
+        if (rem<MULTI>(group(me)[j])) wait_geq(a, ready(me, g, j), epoch, kWaitReady, me, j);
+      }
     }
     __syncthreads();
   }
 
-  template <bool TMA>
+  template <bool TMA, bool MULTI>
   __device__ void ts_reduce(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
-    const int me = a.my_workers[0];
-    const int8_t *G = group(me);
-    const int p = a.my_pos[0];
     if (TMA && threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();  // entry free (+ sync below)
-    ts_wait(g, 2 * uint64_t(a.call) + 1);
-    const int64_t len = c.e1 - c.e0, lo = ts_lo(p, len), hi = ts_hi(p, len), bh = ts_bulk_hi(p, len);
-    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
-    for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
-      const int64_t e = c.e0 + o;
-      const int nv = (int)min(int64_t(W), hi - o);
-      float acc[W];
-      for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
-        const float *src = (rr == p) ? stage(0) : recv(me, rr);
-        float y[W];
-        ld_slot<W>(src + c.soff + e, y, nv);
+    ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 1);
+    const int64_t len = c.e1 - c.e0;
+    for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
+      if (MULTI && a.slot_kind[s] != 0) continue;
+      const int me = a.my_workers[s];
+      const int8_t *G = group(me);
+      const int p = a.my_pos[s];
+      const int64_t lo = ts_lo(p, len), hi = ts_hi(p, len), bh = ts_bulk_hi(p, len);
+      for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
+        const int64_t e = c.e0 + o;
+        const int nv = (int)min(int64_t(W), hi - o);
+        float acc[W];
+        for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
+          const int w = G[rr];
+          const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
+          float y[W];
+          ld_slot<W>(src + c.soff + e, y, nv);
 #pragma unroll
-        for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
-      if (TMA && o + nv <= bh) {
-        st_slot<W>(ent + o, acc, nv);  // all-gather image, bulk-pushed below
-      } else {
-        for (int j = 0; j < a.m; ++j)  // all-gather: my slice's mean to every peer
-          if (j != p) st_slot<W>(recv(G[j], p) + c.soff + e, acc, nv);
-      }
-      if constexpr (!GRAD) {
-        store_m<W>(xs + e, acc, nv);
-      } else {
-        float v[W], x[W];
-        load_m<W>(vs + e, v, nv);
-        load_m<W>(xs + e, x, nv);
-#pragma unroll
-        for (int q = 0; q < W; ++q) {
-          v[q] = dev::momentum(a.mu, v[q], acc[q]);
-          x[q] = dev::sgd(x[q], a.lr, v[q]);
+          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
         }
-        store_m<W>(vs + e, v, nv);
-        store_m<W>(xs + e, x, nv);
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
+        const bool bulk = TMA && o + nv <= bh;
+        if (bulk) st_slot<W>(ent + o, acc, nv);  // all-gather image, bulk-pushed below (r == 1)
+        for (int rr = 0; rr < a.m; ++rr) {  // apply to every member: here directly, else push
+          const int w = G[rr];
+          if (rem<MULTI>(w)) {
+            if (!bulk) st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
+            continue;
+          }
+          const int sl = a.worker_slot[w];
+          float *xw = a.bx[c.b * a.r + sl] + e, *vw = a.bv[c.b * a.r + sl] + e;
+          if constexpr (!GRAD) {
+            store_m<W>(xw, acc, nv);
+          } else {
+            float v[W], x[W];
+            load_m<W>(vw, v, nv);
+            load_m<W>(xw, x, nv);
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+              v[q] = dev::momentum(a.mu, v[q], acc[q]);
+              x[q] = dev::sgd(x[q], a.lr, v[q]);
+            }
+            store_m<W>(vw, v, nv);
+            store_m<W>(xw, x, nv);
+          }
+        }
       }
     }
-    __syncthreads();  // my slice is folded: drop the dead lines (RS data, own stage)
+    __syncthreads();  // my slices are folded: drop the dead lines (stages, RS data)
     if constexpr (TMA) {
-      if (threadIdx.x == 0) ts_bulk_push(c, ent, p);
+      if (threadIdx.x == 0) ts_bulk_push(c, ent, a.my_pos[0]);
     }
     if constexpr (W == 4) {
       if (a.discard) {
-        for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
-          for (int rr = 0; rr < a.m; ++rr)
-            discard_l2(((rr == p) ? stage(0) : recv(me, rr)) + c.soff + c.e0 + o);
+        for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
+          if (MULTI && a.slot_kind[s] != 0) continue;
+          const int me = a.my_workers[s];
+          const int8_t *G = group(me);
+          const int p = a.my_pos[s];
+          const int64_t lo = ts_lo(p, len), hi = ts_hi(p, len);
+          for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
+            for (int rr = 0; rr < a.m; ++rr) {
+              const int w = G[rr];
+              discard_l2((rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w])) + c.soff + c.e0 + o);
+            }
+        }
       }
     }
     __syncthreads();  // the AG stores precede the (deferred) flag release
   }
 
+  // the slices owned by remote members: their means arrived in my receive slots
+  template <bool MULTI>
   __device__ void ts_finish(int64_t g) const {
     const ChunkRef c = locate(g);
-    const int me = a.my_workers[0];
-    const int p = a.my_pos[0];
-    ts_wait(g, 2 * uint64_t(a.call) + 2);
+    ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 2);
     const int64_t len = c.e1 - c.e0;
-    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
-    for (int j = 0; j < a.m; ++j) {
-      if (j == p) continue;
-      const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
-      const float *src = recv(me, j) + c.soff;
-      for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
-        const int64_t e = c.e0 + o;
-        const int nv = (int)min(int64_t(W), hi - o);
-        float y[W];
-        ld_slot<W>(src + e, y, nv);
-        if constexpr (!GRAD) {
-          store_m<W>(xs + e, y, nv);
-        } else {
-          float v[W], x[W];
-          load_m<W>(vs + e, v, nv);
-          load_m<W>(xs + e, x, nv);
+    for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
+      if (MULTI && a.slot_kind[s] != 0) continue;
+      const int me = a.my_workers[s];
+      const int8_t *G = group(me);
+      float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
+      for (int j = 0; j < a.m; ++j) {
+        if (j == a.my_pos[s] || !rem<MULTI>(G[j])) continue;
+        const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
+        const float *src = recv(me, j) + c.soff;
+        for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
+          const int64_t e = c.e0 + o;
+          const int nv = (int)min(int64_t(W), hi - o);
+          float y[W];
+          ld_slot<W>(src + e, y, nv);
+          if constexpr (!GRAD) {
+            store_m<W>(xs + e, y, nv);
+          } else {
+            float v[W], x[W];
+            load_m<W>(vs + e, v, nv);
+            load_m<W>(xs + e, x, nv);
 #pragma unroll
-          for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], y[q]);
-            x[q] = dev::sgd(x[q], a.lr, v[q]);
+            for (int q = 0; q < W; ++q) {
+              v[q] = dev::momentum(a.mu, v[q], y[q]);
+              x[q] = dev::sgd(x[q], a.lr, v[q]);
+            }
+            store_m<W>(vs + e, v, nv);
+            store_m<W>(xs + e, x, nv);
           }
-          store_m<W>(vs + e, v, nv);
-          store_m<W>(xs + e, x, nv);
         }
       }
     }
     __syncthreads();
     if constexpr (W == 4) {
       if (a.discard) {
-        for (int j = 0; j < a.m; ++j) {
-          if (j == p) continue;
-          const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
-          for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
-            discard_l2(recv(me, j) + c.soff + c.e0 + o);
+        for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
+          if (MULTI && a.slot_kind[s] != 0) continue;
+          const int me = a.my_workers[s];
+          const int8_t *G = group(me);
+          for (int j = 0; j < a.m; ++j) {
+            if (j == a.my_pos[s] || !rem<MULTI>(G[j])) continue;
+            const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
+            for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
+              discard_l2(recv(me, j) + c.soff + c.e0 + o);
+          }
         }
       }
     }
@@ -1068,17 +1118,19 @@ struct Split {
   // last step may still be in flight).  A chunk pushed at step s is released by step
   // s + D + R - 1, so with reduce L >= D + R - 1 steps after rs_stage (and finish L after
   // reduce) every wait targets a flag released at the top of this step or an earlier one.
-  template <bool TMA>
+  template <bool TMA, bool MULTI>
   __device__ void compute_twoshot(int i, float *ring) const {
     const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
     const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
     if (nk == 0) return;
-    const int me = a.my_workers[0];
-    const int8_t *G = group(me);
-    if (a.call >= 2 && threadIdx.x < 32) {  // guard: peers consumed their call-2 receive slots
+    if (a.call >= 2 && threadIdx.x < 32) {  // guard: remote members consumed their call-2 slots
       const uint64_t need = step_epoch(a.prev2_epoch0, first + (nk - 1) * gc);
-      for (int j = threadIdx.x; j < a.m; j += 32)
-        if (G[j] != me) wait_geq(a, consumed(G[j], i), need, kWaitConsumed, G[j], j);
+      for (int pr = threadIdx.x; pr < (MULTI ? a.r : 1) * a.m; pr += 32) {
+        const int sl = pr / a.m, j = pr % a.m;
+        if (MULTI && a.slot_kind[sl] != 0) continue;
+        const int w = group(a.my_workers[sl])[j];
+        if (rem<MULTI>(w)) wait_geq(a, consumed(w, i), need, kWaitConsumed, w, j);
+      }
     }
     __syncthreads();
     const int D = TMA ? max(a.release_delay, 2) : max(a.release_delay, 1);
@@ -1098,7 +1150,7 @@ struct Split {
         int newer = 0;
         if constexpr (TMA)
           for (int64_t s2 = k - D + 1; s2 < k; ++s2) newer += groups_of(s2);
-        ts_release<TMA>(first, rs_out, rs1, ag_out, ag1, newer);
+        ts_release<TMA, MULTI>(first, rs_out, rs1, ag_out, ag1, newer);
         rs_out = rs1;
         ag_out = ag1;
       }
@@ -1108,7 +1160,7 @@ struct Split {
         t0 = t1;
       }
       if (k < nk) {
-        ts_rs_stage<TMA>(first + k * gc, ring + (q % kPushRing) * kChunk);
+        ts_rs_stage<TMA, MULTI>(first + k * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1117,7 +1169,7 @@ struct Split {
         t0 = t1;
       }
       if (k >= L && k - L < nk) {
-        ts_reduce<TMA>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
+        ts_reduce<TMA, MULTI>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1125,7 +1177,7 @@ struct Split {
         t_red += t1 - t0;
         t0 = t1;
       }
-      if (k >= 2 * L && k - 2 * L < nk) ts_finish(first + (k - 2 * L) * gc);
+      if (k >= 2 * L && k - 2 * L < nk) ts_finish<MULTI>(first + (k - 2 * L) * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_fin += t1 - t0;
@@ -1133,8 +1185,9 @@ struct Split {
       }
     }
     if (TMA && threadIdx.x == 0) dev::bulk_wait_all();  // no bulk copy outlives the CTA
-    if (threadIdx.x == 0)  // every read of my receive slots is done (guard of call + 2)
-      dev::st_release_sys(consumed(me, i), step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
+    if (threadIdx.x < (MULTI ? a.r : 1))  // every read of my receive slots is done (call + 2 guard)
+      dev::st_release_sys(consumed(a.my_workers[threadIdx.x], i),
+                          step_epoch(a.seq_epoch0, first + (nk - 1) * gc));
     if (a.prof && threadIdx.x == 0) {
       uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
       pr[0] += t_stage;
@@ -1197,29 +1250,31 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
     p.compute_direct(blockIdx.x);
 }
 
-template <int W, bool GRAD, bool TMA>
+template <int W, bool GRAD, bool TMA, bool MULTI>
 __global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];  // TMA: kPushRing chunk images
   const Split<W, GRAD> p(a);
   if (a.m == 1)
     p.local_only();
   else
-    p.template compute_twoshot<TMA>(blockIdx.x, reinterpret_cast<float *>(dsmem));
+    p.template compute_twoshot<TMA, MULTI>(blockIdx.x, reinterpret_cast<float *>(dsmem));
 }
 
 constexpr size_t kTwoshotTmaSmem = size_t(Split<4, false>::kPushRing) * size_t(kChunk) * 4;  // 48 KiB
 
-template <bool TMA>
+template <bool TMA, bool MULTI>
 const void *pick_twoshot_t(int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
   if (vec)
-    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, TMA>)
-                : reinterpret_cast<const void *>(&k4_twoshot<4, false, TMA>);
-  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, TMA>)
-              : reinterpret_cast<const void *>(&k4_twoshot<1, false, TMA>);
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, TMA, MULTI>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false, TMA, MULTI>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, TMA, MULTI>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false, TMA, MULTI>);
 }
-const void *pick_twoshot(int mode, bool vec, bool tma) {
-  return tma ? pick_twoshot_t<true>(mode, vec) : pick_twoshot_t<false>(mode, vec);
+// TMA pushes: one worker per GPU only; several workers per GPU: the MULTI kernel
+const void *pick_twoshot(int mode, bool vec, bool tma, bool multi) {
+  if (tma) return pick_twoshot_t<true, false>(mode, vec);
+  return multi ? pick_twoshot_t<false, true>(mode, vec) : pick_twoshot_t<false, false>(mode, vec);
 }
 
 // variant 0: DIRECT push from the compute CTAs; variant >= 1: that many COMM CTAs
@@ -1270,8 +1325,8 @@ cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec
   return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
 }
 
-int p2p_twoshot_occupancy(int mode, bool vec, bool tma) {
-  const void *k = pick_twoshot(mode, vec, tma);
+int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
+  const void *k = pick_twoshot(mode, vec, tma, multi);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int blocks = 0;
@@ -1281,7 +1336,7 @@ int p2p_twoshot_occupancy(int mode, bool vec, bool tma) {
 }
 
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream) {
-  const void *k = pick_twoshot(mode, vec, tma);
+  const void *k = pick_twoshot(mode, vec, tma, a.r > 1);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};

@@ -88,11 +88,11 @@ void freeze_layout(sesgd_ctx *ctx) {
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, true, smem));
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_PARAM_AVG, false, smem));
     occ = std::min(occ, sesgd::p2p_occupancy(var, r, SESGD_MODE_GRAD_AVG, false, smem));
-    if (var == 0 && r == 1)  // K4 (two-shot) shares the grid and the flag layout
+    if (var == 0)  // K4 (two-shot) shares the grid and the flag layout
       for (int mode = 0; mode < 2; ++mode)
         for (int vec = 0; vec < 2; ++vec)
           for (int tma = 0; tma < 2; ++tma)
-            occ = std::min(occ, sesgd::p2p_twoshot_occupancy(mode, vec, tma));
+            occ = std::min(occ, sesgd::p2p_twoshot_occupancy(mode, vec, tma, r > 1));
     return occ;
   };
   // every CTA must be co-resident (COMM and COMPUTE wait on each other): grid = SMs x
@@ -166,13 +166,13 @@ void freeze_layout(sesgd_ctx *ctx) {
   ctx->layout_frozen = true;
 }
 
-// SESGD_PATH_AUTO: every worker on this GPU -> K6; one worker per GPU -> K4 two-shot (it moves
-// 2(m-1)/m of a bucket per GPU instead of (m-1), measured faster at m = 2 and 2x at m = 4);
-// several workers per GPU (or a COMM-CTA layout) -> K3 one-shot
+// SESGD_PATH_AUTO: every worker on this GPU -> K6; else K4 two-shot (a remote member receives
+// 2(m-1)/m of a bucket per member pair instead of one-shot's full copy: measured faster at
+// m = 2 and 2x at m = 4); a COMM-CTA layout (P2P variant >= 1) -> K3 one-shot
 int resolve_path(const sesgd_ctx *ctx) {
   if (ctx->path != SESGD_PATH_AUTO) return ctx->path;
   if (ctx->n_local == ctx->n) return SESGD_PATH_RESIDENT;
-  if (ctx->n_local == 1 && ctx->m >= 2 && ctx->p2p_variant == 0) return SESGD_PATH_TWOSHOT;
+  if (ctx->m >= 2 && ctx->p2p_variant == 0) return SESGD_PATH_TWOSHOT;
   return SESGD_PATH_ONESHOT;
 }
 
@@ -773,8 +773,8 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
 
   // one-shot (K3) or two-shot (K4) push over NVLink P2P
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
-  if (path == SESGD_PATH_TWOSHOT && (ctx->n_local != 1 || ctx->p2p_variant != 0))
-    return fail(ctx, SESGD_ENOTSUP, "the two-shot path needs one worker per GPU");
+  if (path == SESGD_PATH_TWOSHOT && (ctx->p2p_variant != 0 || (ctx->push_tma && ctx->n_local != 1)))
+    return fail(ctx, SESGD_ENOTSUP, "two-shot needs the DIRECT layout; its TMA pushes one worker per GPU");
   return launch_oneshot(ctx, bucket, lr, momentum, st, path == SESGD_PATH_TWOSHOT);
 }
 
@@ -824,7 +824,8 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     return SESGD_OK;
   }
   const bool twoshot = (path == SESGD_PATH_TWOSHOT);
-  bool fuse = (path == SESGD_PATH_ONESHOT || (twoshot && ctx->n_local == 1 && ctx->p2p_variant == 0)) &&
+  bool fuse = (path == SESGD_PATH_ONESHOT ||
+               (twoshot && ctx->p2p_variant == 0 && (!ctx->push_tma || ctx->n_local == 1))) &&
               ctx->peers;
   for (auto &b : ctx->buckets)  // one launch needs one shared call history
     fuse = fuse && b.calls == ctx->buckets[0].calls && b.seq_hist[0] == ctx->buckets[0].seq_hist[0] &&

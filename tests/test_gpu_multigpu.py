@@ -1,4 +1,4 @@
-"""Multi-GPU parity of the one-shot NVLink P2P path (K3) against the CPU oracle.
+"""Multi-GPU parity of the NVLink P2P paths (K3 one-shot, K4 two-shot, K5 ring) against the CPU oracle.
 
 Launches tests/mgpu_worker.py under torch.distributed.run on 2 (and, if present, 4)
 GPUs, one process per GPU, and compares every worker's x, v after T iterations with
@@ -79,15 +79,28 @@ def test_two_gpus_one_worker_each(tmp_path, mode, fused):
     _compare(V, v)
 
 
+@pytest.mark.parametrize("path", [2, 4])
 @pytest.mark.parametrize("n,m", [(4, 2), (8, 2), (8, 4), (4, 1), (8, 8)])
-def test_two_gpus_resident_pairs(tmp_path, n, m):
-    """n/2 workers per GPU: groups mix co-resident members (read from the local stage) and
-    remote members (NVLink push); the schedule changes every iteration, exercising the
-    call-2 receive-slot guard."""
+def test_two_gpus_resident_pairs(tmp_path, n, m, path):
+    """n/2 workers per GPU through K3 (one-shot) and K4 (two-shot): groups mix co-resident
+    members (read in place from the local stage, updated in place) and remote members (NVLink
+    push); all-local groups are updated in registers; the schedule changes every iteration,
+    exercising the call-2 receive-slot guard."""
     buckets = [65537, 3, 20000]
     T = 7
-    X, V = _launch(tmp_path, 2, n, m, T, buckets)
+    X, V = _launch(tmp_path, 2, n, m, T, buckets, path=path)
     x, v = _oracle(n, m, sum(buckets), T, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("n,m", [(8, 4), (4, 2)])
+def test_two_gpus_resident_pairs_twoshot_grad(tmp_path, n, m):
+    """K4 with co-resident members in GRAD mode: the slice owner applies the mean gradient to
+    its co-resident members' v and x."""
+    buckets = [65537, 3, 20000]
+    X, V = _launch(tmp_path, 2, n, m, 6, buckets, mode=1, path=4)
+    x, v = _oracle(n, m, sum(buckets), 6, 1)
     _compare(X, x)
     _compare(V, v)
 
@@ -121,10 +134,21 @@ def test_two_gpus_random_access_resume(tmp_path):
     _compare(V, v)
 
 
-def test_four_gpus(tmp_path):
+@pytest.mark.parametrize("path", [2, 4])
+def test_four_gpus(tmp_path, path):
     buckets = [200003, 5000]
-    X, V = _launch(tmp_path, 4, 8, 4, 6, buckets)
+    X, V = _launch(tmp_path, 4, 8, 4, 6, buckets, path=path)
     x, v = _oracle(8, 4, sum(buckets), 6, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_four_gpus_sixteen_workers_twoshot(tmp_path):
+    """BASELINE cfg 3's shape on 4 GPUs: n = 16, m = 4, four workers per GPU (groups span 1-4
+    GPUs), K4 two-shot."""
+    buckets = [100003, 77]
+    X, V = _launch(tmp_path, 4, 16, 4, 5, buckets, path=4)
+    x, v = _oracle(16, 4, sum(buckets), 5, 0)
     _compare(X, x)
     _compare(V, v)
 
