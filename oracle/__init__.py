@@ -77,6 +77,13 @@ def lib():
         L.orc_run_ring_f32.argtypes = [i32, i32, u64, i64, i64, i64, i64, u64, ctypes.c_float,
                                        ctypes.c_float, i32, P, P]
         L.orc_run_ring_f32.restype = ctypes.c_int
+        L.orc_run_local_f32.argtypes = [i32, i32, u64, i64, i64, i64, P, u64, ctypes.c_float,
+                                        ctypes.c_float, i32, i64, P, P]
+        L.orc_run_local_f32.restype = ctypes.c_int
+        L.orc_global_average_f32.argtypes = [i32, i64, P]
+        L.orc_global_average_f32.restype = ctypes.c_int
+        L.orc_global_average_f64.argtypes = [i32, i64, P]
+        L.orc_global_average_f64.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -197,3 +204,29 @@ def run(n, m, seed, T, x, v, *, s_g, lr, mu, mode=MODE_PARAM, t0=0, coords=None)
     else:
         raise TypeError(x.dtype)
     return x, v
+
+
+def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0, coords=None):
+    """Local-SESGD: T iterations where the group exchange fires only when
+    (t + 1) % period == 0; float32 x, v (n, S) in place.  period = 1 is `run`; m = n is
+    Local-SGD."""
+    S = x.shape[-1]
+    cp = None
+    if coords is not None:
+        coords = np.ascontiguousarray(coords, np.int64)
+        assert coords.shape == (S,)
+        cp = _ptr(coords)
+    assert x.dtype == np.float32 and x.flags.c_contiguous and v.flags.c_contiguous
+    _check(lib().orc_run_local_f32(n, m, seed, t0, T, S, cp, s_g, float(lr), float(mu), mode,
+                                   int(period), _ptr(x), _ptr(v)))
+    return x, v
+
+
+def global_average(x):
+    """Algorithm 1's last line: every row of x (n, L) becomes the ascending-fold mean of
+    all rows, in place (float32 or float64)."""
+    assert x.flags.c_contiguous and x.ndim == 2
+    fn = {np.dtype(np.float32): lib().orc_global_average_f32,
+          np.dtype(np.float64): lib().orc_global_average_f64}[x.dtype]
+    _check(fn(x.shape[0], x.shape[1], _ptr(x)))
+    return x

@@ -356,3 +356,54 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
   free(canon);
   return rc;
 }
+
+/* ---- Local-SESGD: exchange only when (t + 1) mod H == 0 ---- */
+int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
+                      const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
+                      int64_t H, float *x, float *v) {
+  if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || S < 0 || H < 1) return ORC_EINVAL;
+  if (n % m != 0) return ORC_ENOTDIV;
+  float *g = (float *)malloc(sizeof(float) * (size_t)n * (size_t)(S > 0 ? S : 1));
+  int32_t *canon = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int rc = ORC_OK;
+  for (int64_t t = t0; t < t0 + T && rc == ORC_OK; ++t) {
+    for (int32_t i = 0; i < n; ++i) {
+      uint64_t key = synth_grad_key(s_g, i, t);
+      for (int64_t e = 0; e < S; ++e)
+        g[(size_t)i * (size_t)S + (size_t)e] = synth_grad(key, coords ? coords[e] : e);
+    }
+    if ((t + 1) % H == 0) { /* synchronisation iteration: SESGD step with the groups of t */
+      rc = orc_groups(seed, t, n, m, NULL, canon, NULL);
+      if (rc == ORC_OK) rc = orc_step_f32(n, m, canon, S, x, v, g, lr, mu, mode);
+    } else { /* local iteration: every worker its own singleton group */
+      for (int32_t i = 0; i < n; ++i) canon[i] = i;
+      rc = orc_step_f32(n, 1, canon, S, x, v, g, lr, mu, mode);
+    }
+  }
+  free(g);
+  free(canon);
+  return rc;
+}
+
+/* ---- final global average (Alg.1 last line) ---- */
+int orc_global_average_f32(int32_t n, int64_t L, float *x) {
+  if (n < 1 || L < 0 || (L > 0 && !x)) return ORC_EINVAL;
+  for (int64_t e = 0; e < L; ++e) {
+    float s = x[e];
+    for (int32_t i = 1; i < n; ++i) s = s + x[(size_t)i * (size_t)L + (size_t)e];
+    s = s / (float)n;
+    for (int32_t i = 0; i < n; ++i) x[(size_t)i * (size_t)L + (size_t)e] = s;
+  }
+  return ORC_OK;
+}
+
+int orc_global_average_f64(int32_t n, int64_t L, double *x) {
+  if (n < 1 || L < 0 || (L > 0 && !x)) return ORC_EINVAL;
+  for (int64_t e = 0; e < L; ++e) {
+    double s = x[e];
+    for (int32_t i = 1; i < n; ++i) s = s + x[(size_t)i * (size_t)L + (size_t)e];
+    s = s / (double)n;
+    for (int32_t i = 0; i < n; ++i) x[(size_t)i * (size_t)L + (size_t)e] = s;
+  }
+  return ORC_OK;
+}

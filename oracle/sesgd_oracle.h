@@ -81,6 +81,21 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
                 const int64_t *coords, uint64_t s_g, double lr, double mu, int32_t mode, double *x,
                 double *v);
 
+/* Local-SESGD (paper Sec. 4.1 "Baseline" P:315-317): as orc_run_f32, but the
+ * group exchange of iteration t fires only when (t + 1) mod H == 0 (groups of that t); on the
+ * other iterations the locally updated parameters are kept (the iteration with m = 1:
+ * PARAM x = xh, GRAD v = mu v + g, x = x - lr v).  H = 1 is SESGD; m = n is Local-SGD
+ * (the paper's baseline with period 2). */
+int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
+                      const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
+                      int64_t H, float *x, float *v);
+
+/* Algorithm 1's last line: xbar = Ring-AllReduce(x_i; Global), the mean of the n
+ * workers' parameters, left fold in ascending worker id then one division by n
+ * (R7, R10); written back to every worker's row of x [n*L]. */
+int orc_global_average_f32(int32_t n, int64_t L, float *x);
+int orc_global_average_f64(int32_t n, int64_t L, double *x);
+
 #ifdef __cplusplus
 }
 #endif

@@ -511,3 +511,92 @@ def test_ring_order_equals_fold_for_two_members_and_is_close_otherwise():
             bound = (m + 2) * 2.0 ** -24 * np.abs(x64).max() * 2
             assert np.abs(xr - x64).max() < bound and np.abs(xa - x64).max() < bound
             assert not np.array_equal(xa, xr)  # the order really differs
+
+
+# ---------------------------------------------------------------- NEXT-2: Local-SESGD, final average
+def _run_local(n, m, T, L, period, mode=oracle.MODE_PARAM, t0=0):
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, SEED, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=period,
+                     mode=mode, t0=t0)
+    return x, v
+
+
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+def test_local_period_one_is_sesgd(mode):
+    """H = 1 is identical to SESGD (every iteration exchanges)."""
+    n, m, T, L = 8, 2, 6, 257
+    x, v = _run_local(n, m, T, L, 1, mode)
+    xs = np.tile(synth.x0_host(L), (n, 1))
+    vs = np.zeros_like(xs)
+    oracle.run(n, m, SEED, T, xs, vs, s_g=synth.SEED_G, lr=0.1, mu=0.9, mode=mode)
+    assert np.array_equal(x, xs) and np.array_equal(v, vs)
+
+
+def test_local_period_longer_than_run_is_independent_sgd():
+    """H -> infinity: no communication, every worker is textbook momentum SGD on its own
+    gradients (torch.optim.SGD float32, within FMA-contraction tolerance)."""
+    n, T, L = 4, 7, 300
+    x, _ = _run_local(n, 2, T, L, 1000)
+    for i in range(n):
+        ref = _torch_sgd_trajectory(synth.x0_host(L), [synth.grad_host(i, t, L) for t in range(T)],
+                                    0.1, 0.9, dtype=torch.float32)
+        np.testing.assert_allclose(x[i], ref, rtol=1e-6, atol=1e-8)
+
+
+def test_local_sesgd_exchange_events():
+    """n = 4, k = 2, H = 2, 4 iterations -> exactly 2 shuffle+allreduce events: group
+    members of G_t are byte-identical right after iterations t = 1 and t = 3 only."""
+    n, m, L = 4, 2, 64
+    events = []
+    for T in range(1, 5):
+        x, _ = _run_local(n, m, T, L, 2)
+        t = T - 1
+        groups = oracle.canonical_groups(SEED, t, n, m)
+        if all(np.array_equal(x[g[0]], x[g[1]]) for g in groups):
+            events.append(t)
+    assert events == [1, 3]
+
+
+@pytest.mark.parametrize("period", [2, 3])
+def test_local_sgd_is_global_average_every_period(period):
+    """m = n (Local-SGD, the paper's baseline with period 2): all workers
+    byte-identical exactly after synchronisation iterations; the worker mean follows momentum SGD
+    on the mean gradient at every t (P8 holds for any averaging schedule; float32 tolerance)."""
+    n, L = 4, 128
+    gbars = []
+    for T in range(1, 7):
+        x, _ = _run_local(n, n, T, L, period)
+        same = all(np.array_equal(x[0], x[i]) for i in range(n))
+        assert same == (T % period == 0)
+        gbars.append(np.mean([synth.grad_host(i, T - 1, L).astype(np.float64) for i in range(n)], 0))
+        ref = _torch_sgd_trajectory(synth.x0_host(L).astype(np.float64), gbars, 0.1, 0.9)
+        np.testing.assert_allclose(x.astype(np.float64).mean(0), ref, rtol=0, atol=2e-7)
+
+
+def test_global_average_special_cases():
+    """identical workers -> unchanged; [0] and [2] -> [1]."""
+    x = np.tile(np.array([0.25, -3.5, 7.0], np.float32), (5, 1))
+    y = oracle.global_average(x.copy())
+    assert np.array_equal(y, x)
+    z = oracle.global_average(np.array([[0.0], [2.0]], np.float32))
+    assert np.array_equal(z, np.array([[1.0], [1.0]], np.float32))
+
+
+def test_global_average_matches_sequential_mean():
+    """16 random workers -> the sequential mean; f64 within 1e-12 of math.fsum / n; f32
+    bit-exact against a brute-force left fold in numpy float32 scalars, and within the fp32 bound
+    of the exact mean."""
+    rng = np.random.default_rng(5)
+    x64 = rng.standard_normal((16, 37))
+    got64 = oracle.global_average(x64.copy())
+    exact = np.array([math.fsum(x64[:, e]) / 16 for e in range(37)])
+    np.testing.assert_allclose(got64[7], exact, rtol=1e-12, atol=1e-15)
+    x32 = x64.astype(np.float32)
+    got32 = oracle.global_average(x32.copy())
+    for e in range(37):
+        s = np.float32(x32[0, e])
+        for i in range(1, 16):
+            s = np.float32(s + x32[i, e])
+        assert got32[3, e] == np.float32(s / np.float32(16))
+    np.testing.assert_allclose(got32[0], exact, rtol=0, atol=16 * 6e-8 * np.abs(x64).max())
