@@ -103,6 +103,11 @@ extern "C" {
                                     flag-release batches (1..16, default 3); each batch is ONE
                                     system-scope fence (~8 us under load) followed by relaxed
                                     flag stores; the lag is raised to cover it */
+#define SESGD_OPT_LOCAL_PERIOD 15  /* Local-SESGD (paper Sec. 4.1, period 2 at
+                                    P:328): the group exchange of iteration t (sesgd_begin_iter)
+                                    fires only when (t + 1) mod H == 0; other iterations run the
+                                    local step alone (x <- x_hat).  H >= 1, default 1 = SESGD;
+                                    group_size = n gives Local-SGD */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {
@@ -213,6 +218,16 @@ SESGD_API int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *str
  * like sesgd_sync_step; host buffers must stay valid until the stream is synchronised. */
 SESGD_API int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,
                          const float *const *g_host, float *const *x_host_out, void *stream);
+
+/* Algorithm 1's last line, xbar <- Ring-AllReduce(x_i; Global), for bucket `bucket`:
+ * every LOCAL worker's parameters become (rows[0] (+) rows[1] (+) ... (+) rows[n-1]) (/) n,
+ * a left fold in ascending worker id (R7, R10).  rows: host array of n device pointers to the n
+ * workers' parameters of this bucket (numel fp32 each, caller-owned; e.g. an all-gather of every
+ * rank's x), or NULL when all n workers are local (their registered x is used, in place).
+ * Momentum buffers are not touched.  Asynchronous on `stream` (K8).  Errors: SESGD_EINVAL (nrows
+ * != n, null row, NULL rows with remote workers), SESGD_ESTATE, SESGD_ECUDA. */
+SESGD_API int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *const *rows,
+                                   int32_t nrows, void *stream);
 
 /* Non-blocking check of the latched device error word: SESGD_OK or SESGD_ETIMEOUT. */
 SESGD_API int sesgd_poll(sesgd_ctx *ctx);

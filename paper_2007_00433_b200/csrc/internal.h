@@ -45,6 +45,14 @@ struct ResidentArgs {
 cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_x, int unroll,
                             cudaStream_t stream);
 int resident_block_threads();
+// K8: global average (Alg.1 last line): outs[s][e] = fold_i rows[i][e] / nrows
+struct AverageArgs {
+  const float *rows[SESGD_MAX_WORKERS];  // the n workers' parameters, ascending worker id
+  float *outs[SESGD_MAX_WORKERS];        // every local worker's parameters
+  int nrows, nouts;
+  int64_t numel;
+};
+cudaError_t launch_average(const AverageArgs &a, bool vec, int sm_count, cudaStream_t stream);
 int resident_occupancy(int mode, bool vec, int m, int unroll);
 
 // K3: one-shot push over NVLink, SM-specialised (COMM CTAs + COMPUTE CTAs), see p2p.cu.
@@ -161,6 +169,7 @@ struct sesgd_ctx {
   int push_tma = 0;         // SESGD_OPT_PUSH_TMA (two-shot kernel)
   int release_delay = 1;    // SESGD_OPT_RELEASE_DELAY (two-shot kernel)
   int release_every = 3;    // SESGD_OPT_RELEASE_EVERY (two-shot kernel)
+  int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
   int64_t *d_numels = nullptr;  // resident all-bucket launch: numel table [NB]
   bool resident_tables_ok = false;
   // attach

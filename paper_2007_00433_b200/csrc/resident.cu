@@ -253,7 +253,50 @@ const void *pick(int mode, bool vec, int m, int unroll) {
   return grad ? pick_m<1, true>(m, unroll) : pick_m<1, false>(m, unroll);
 }
 
+// K8: Algorithm 1's last line, xbar = Ring-AllReduce(x_i; Global): per element, the
+// left fold of the n workers' parameters in ascending worker id, one division by n (R7, R10),
+// stored to every local worker.  Each thread reads all rows of its elements before writing them,
+// so the rows may alias the outputs (one GPU, in place).
+template <int W>
+__global__ void __launch_bounds__(kThreads) k8_average(const __grid_constant__ AverageArgs a) {
+  const int64_t items = (W == 4) ? a.numel / 4 : a.numel;
+  const float nr = float(a.nrows);
+  for (int64_t it = int64_t(blockIdx.x) * kThreads + threadIdx.x; it < items;
+       it += int64_t(gridDim.x) * kThreads) {
+    const int64_t e = it * W;
+    float acc[W], y[W];
+    load<W>(a.rows[0] + e, acc);
+    for (int i = 1; i < a.nrows; ++i) {
+      load<W>(a.rows[i] + e, y);
+#pragma unroll
+      for (int q = 0; q < W; ++q) acc[q] = __fadd_rn(acc[q], y[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], nr);
+    for (int s = 0; s < a.nouts; ++s) store<W>(a.outs[s] + e, acc);
+  }
+  if constexpr (W == 4) {  // ragged tail of 1..3 elements
+    const int64_t e = items * 4 + int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (blockIdx.x == 0 && e < a.numel) {
+      float acc = a.rows[0][e];
+      for (int i = 1; i < a.nrows; ++i) acc = __fadd_rn(acc, a.rows[i][e]);
+      acc = __fdiv_rn(acc, nr);
+      for (int s = 0; s < a.nouts; ++s) a.outs[s][e] = acc;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_average(const AverageArgs &a, bool vec, int sm_count, cudaStream_t stream) {
+  const int64_t items = vec ? a.numel / 4 : a.numel;
+  int64_t blocks = (items + kThreads - 1) / kThreads;
+  blocks = blocks < 1 ? 1 : (blocks > int64_t(sm_count) * 8 ? int64_t(sm_count) * 8 : blocks);
+  void *args[] = {const_cast<AverageArgs *>(&a)};
+  const void *k = vec ? reinterpret_cast<const void *>(&k8_average<4>)
+                      : reinterpret_cast<const void *>(&k8_average<1>);
+  return cudaLaunchKernel(k, dim3(unsigned(blocks)), dim3(kThreads), args, 0, stream);
+}
 
 int resident_block_threads() { return kThreads; }
 

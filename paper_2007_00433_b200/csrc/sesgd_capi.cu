@@ -166,6 +166,64 @@ void freeze_layout(sesgd_ctx *ctx) {
   ctx->layout_frozen = true;
 }
 
+// Local-SESGD: an iteration whose (t + 1) is not a multiple of the local period only
+// takes the local step on every local worker -- K6 with singleton groups (m = 1, k = n_local),
+// no flags, no exchange; the exchange paths' call counters do not move (every rank skips the
+// same iterations).  bucket < 0: every bucket in one launch.
+int upload_resident_tables(sesgd_ctx *ctx);
+
+bool local_only_iteration(const sesgd_ctx *ctx) {
+  return ctx->local_period > 1 && (ctx->t + 1) % ctx->local_period != 0;
+}
+
+int local_step(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st) {
+  ResidentArgs a{};
+  a.lr = lr;
+  a.mu = momentum;
+  a.m = 1;
+  a.k = ctx->n_local;
+  a.n_local = ctx->n_local;
+  for (int s = 0; s < ctx->n_local; ++s) a.member_slot[s] = int8_t(s);
+  bool vec = true;
+  int64_t biggest = 0;
+  if (bucket >= 0) {
+    const sesgd_bucket &b = ctx->buckets[bucket];
+    a.x = b.d_x;
+    a.v = b.d_v;
+    a.g = b.d_g;
+    a.numel = b.numel;
+    vec = b.vec;
+    biggest = b.numel;
+  } else {
+    if (!ctx->resident_tables_ok) {
+      const int rc = upload_resident_tables(ctx);
+      if (rc != SESGD_OK) return rc;
+    }
+    for (auto &b : ctx->buckets) {
+      vec = vec && b.vec;
+      biggest = std::max(biggest, b.numel);
+    }
+    a.nb = int(ctx->buckets.size());
+    a.bx = ctx->d_bx;
+    a.bv = ctx->d_bv;
+    a.bg = ctx->d_bg;
+    a.numels = ctx->d_numels;
+  }
+  const int threads = sesgd::resident_block_threads();
+  const int target = ctx->sm_count * sesgd::resident_occupancy(ctx->mode, vec, 1, 0);
+  int gx = (target + a.k - 1) / a.k;
+  const int64_t need = ((vec ? biggest / 4 : biggest) + threads - 1) / threads;
+  if (need < gx) gx = int(need > 0 ? need : 1);
+  cudaError_t e = sesgd::launch_resident(a, ctx->mode, vec, gx, 0, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch local step");
+  for (size_t b = 0; b < ctx->buckets.size(); ++b) {
+    if (bucket >= 0 && int(b) != bucket) continue;
+    ctx->buckets[b].stats.hbm_algo_bytes += 20 * ctx->buckets[b].numel * ctx->n_local;
+    if (bucket >= 0 || b == 0) ctx->buckets[b].stats.kernel_launches++;
+  }
+  return SESGD_OK;
+}
+
 // SESGD_PATH_AUTO: every worker on this GPU -> K6; else K4 two-shot (a remote member receives
 // 2(m-1)/m of a bucket per member pair instead of one-shot's full copy: measured faster at
 // m = 2 and 2x at m = 4); a COMM-CTA layout (P2P variant >= 1) -> K3 one-shot
@@ -496,6 +554,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       if (value < 1 || value > 16) return fail(ctx, SESGD_EINVAL, "release interval must be in [1, 16]");
       ctx->release_every = int(value);
       return SESGD_OK;
+    case SESGD_OPT_LOCAL_PERIOD:
+      if (value < 1) return fail(ctx, SESGD_EINVAL, "local period must be >= 1");
+      ctx->local_period = value;
+      return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");
       ctx->profile = int(value);
@@ -699,6 +761,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
   b.stats.sync_calls++;
   if (b.numel == 0) return SESGD_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (local_only_iteration(ctx)) return local_step(ctx, bucket, lr, momentum, st);
   const bool all_local = (ctx->n_local == ctx->n);
   const int path = resolve_path(ctx);
 
@@ -788,6 +851,10 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     if (!b.registered) return fail(ctx, SESGD_ESTATE, "bucket ids must be dense from 0");
   if (!std::isfinite(lr) || !std::isfinite(momentum))
     return fail(ctx, SESGD_EINVAL, "lr and momentum must be finite");
+  if (local_only_iteration(ctx)) {  // Local-SESGD: local step only, every bucket in one launch
+    for (auto &b : ctx->buckets) b.stats.sync_calls++;
+    return local_step(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream));
+  }
   const bool all_local = (ctx->n_local == ctx->n);
   const int path = resolve_path(ctx);
   if (path == SESGD_PATH_RESIDENT && all_local) {  // K6 over every bucket in one launch
@@ -839,6 +906,40 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
   }
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
   return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot);
+}
+
+int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,
+                         void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  int rc = check_latched(ctx);
+  if (rc != SESGD_OK) return rc;
+  if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
+  if (bucket < 0 || size_t(bucket) >= ctx->buckets.size() || !ctx->buckets[bucket].registered)
+    return fail(ctx, SESGD_EINVAL, "bucket not registered");
+  if (nrows != ctx->n) return fail(ctx, SESGD_EINVAL, "nrows must equal n (every worker's parameters)");
+  sesgd_bucket &b = ctx->buckets[bucket];
+  if (b.numel == 0) return SESGD_OK;
+  sesgd::AverageArgs a{};
+  bool vec = b.vec;
+  for (int i = 0; i < ctx->n; ++i) {
+    if (rows) {
+      if (!rows[i]) return fail(ctx, SESGD_EINVAL, "null row pointer");
+      a.rows[i] = rows[i];
+      vec = vec && aligned16(rows[i]);
+    } else {
+      if (ctx->n_local != ctx->n)
+        return fail(ctx, SESGD_EINVAL, "rows may be NULL only when every worker is local");
+      a.rows[i] = b.hx[ctx->slot_of[i]];
+    }
+  }
+  for (int s = 0; s < ctx->n_local; ++s) a.outs[s] = b.hx[s];
+  a.nrows = ctx->n;
+  a.nouts = ctx->n_local;
+  a.numel = b.numel;
+  cudaError_t e = sesgd::launch_average(a, vec, ctx->sm_count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch global average");
+  b.stats.kernel_launches++;
+  return SESGD_OK;
 }
 
 int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,

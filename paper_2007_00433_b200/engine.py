@@ -79,6 +79,7 @@ class SESGDEngine:
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
         group = process_group or dist.group.WORLD
+        self.group = group
         nbytes = C.sesgd_workspace_bytes(self.ctx)
         if hasattr(symm_mem, "enable_symm_mem_for_group"):
             try:
@@ -138,6 +139,27 @@ class SESGDEngine:
         for b in range(len(self.bucket_sizes)):
             C.sesgd_sync_step_host(self.ctx, b, lr, momentum, [h.data_ptr() for h in g_host[b]],
                                    [h.data_ptr() for h in x_host[b]], s.cuda_stream)
+
+    def global_average(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Algorithm 1's last line: every worker's parameters become the mean over all n
+        workers (K8, ascending fold).  Several GPUs: the ranks' parameters are all-gathered
+        (data movement only) and every rank averages the n rows locally."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nb = len(self.bucket_sizes)
+        if self.world == 1:
+            for b in range(nb):
+                C.sesgd_global_average(self.ctx, b, self.n, None, s.cuda_stream)
+            return
+        import torch.distributed as dist
+        with torch.cuda.stream(s):
+            local = torch.stack(self.x_flat)  # [r, total]
+            gathered = torch.empty((self.world,) + tuple(local.shape), dtype=local.dtype, device=self.device)
+            dist.all_gather_into_tensor(gathered, local, group=self.group)
+            rows = gathered.view(self.n, -1)  # worker w = rank w // r, slot w % r: ascending id
+            for b in range(nb):
+                ptrs = [rows[w].data_ptr() + 4 * self.offsets[b] for w in range(self.n)]
+                C.sesgd_global_average(self.ctx, b, self.n, ptrs, s.cuda_stream)
+        self._gathered = gathered  # alive until the next call (the kernels read it on s)
 
     def groups(self, t: int):
         return C.sesgd_groups(self.ctx, t, self.n)

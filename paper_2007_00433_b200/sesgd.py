@@ -21,7 +21,7 @@ PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT, PATH_RING, PATH_TWOSHOT = 0, 1, 2, 3, 4
 OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS, OPT_P2P_VARIANT, OPT_DISCARD = (
     1, 2, 3, 4, 5, 6, 7)
 OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL, OPT_PUSH_TMA = 8, 9, 10, 11, 12
-OPT_RELEASE_DELAY, OPT_RELEASE_EVERY = 13, 14
+OPT_RELEASE_DELAY, OPT_RELEASE_EVERY, OPT_LOCAL_PERIOD = 13, 14, 15
 
 # every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
 EXPORTED = (
@@ -30,6 +30,7 @@ EXPORTED = (
     "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
+    "sesgd_global_average",
 )
 
 
@@ -76,6 +77,7 @@ def lib():
             "sesgd_sync_step": ([P, i32, f32, f32, P], ctypes.c_int),
             "sesgd_sync_step_host": ([P, i32, f32, f32, P, P, P], ctypes.c_int),
             "sesgd_sync_all": ([P, f32, f32, P], ctypes.c_int),
+            "sesgd_global_average": ([P, i32, P, i32, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -176,6 +178,12 @@ def sesgd_sync_step_host(ctx, bucket: int, lr: float, momentum: float, g_host_pt
                          stream: int = 0) -> None:
     _check(lib().sesgd_sync_step_host(ctx, bucket, lr, momentum, _ptr_array(g_host_ptrs),
                                       _ptr_array(x_host_ptrs), ctypes.c_void_p(int(stream))), ctx)
+
+
+def sesgd_global_average(ctx, bucket: int, n: int, row_ptrs=None, stream: int = 0) -> None:
+    """row_ptrs: the n workers' device pointers (ascending worker id), or None (all local)."""
+    rows = _ptr_array(row_ptrs) if row_ptrs is not None else None
+    _check(lib().sesgd_global_average(ctx, bucket, rows, n, ctypes.c_void_p(int(stream))), ctx)
 
 
 def sesgd_poll(ctx) -> None:

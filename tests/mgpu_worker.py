@@ -32,6 +32,8 @@ def main():
     p.add_argument("--batch", type=int, default=0)
     p.add_argument("--lag", type=int, default=0)
     p.add_argument("--tma", type=int, default=0)
+    p.add_argument("--period", type=int, default=1)
+    p.add_argument("--final-avg", type=int, default=0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -45,7 +47,8 @@ def main():
                       grid=a.grid, timeout_ms=10000, p2p_variant=a.variant, path=a.path,
                       hop_delay_ns=a.hop_ns,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
-                                                   (C.OPT_PUSH_TMA, a.tma)) if v})
+                                                   (C.OPT_PUSH_TMA, a.tma),
+                                                   (C.OPT_LOCAL_PERIOD, a.period)) if v})
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):
@@ -55,6 +58,8 @@ def main():
             for b, L in enumerate(buckets):
                 synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
         eng.step(t, 0.1, 0.9, fused=bool(a.fused))
+    if a.final_avg:
+        eng.global_average()
     torch.cuda.synchronize()
     eng.poll()
     X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])

@@ -29,7 +29,7 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0, path=0, hop_ns=0, tma=0):
+            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -40,7 +40,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--iters", str(T), "--buckets", ",".join(map(str, buckets)), "--mode", str(mode),
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
-               "--tma", str(tma),
+               "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -261,3 +261,19 @@ def test_four_gpus_twoshot_tma(tmp_path, m):
     x, v = _oracle(4, m, sum(buckets), 6, 0)
     _compare(X, x)
     _compare(V, v)
+
+
+# ---------------------------------------------------------------- NEXT-2: Local-SESGD + final average
+@pytest.mark.parametrize("path", [2, 4])
+@pytest.mark.parametrize("n,m,period", [(4, 2, 2), (2, 2, 3), (4, 4, 2)])
+def test_two_gpus_local_sesgd_final_average(tmp_path, n, m, period, path):
+    """Local-SESGD (exchange only when (t + 1) % period == 0; m = n is Local-SGD) over NVLink,
+    then Algorithm 1's final global average (all-gather + K8): the oracle's bits."""
+    buckets = [65537, 3, 20000]
+    T = 5
+    X, V = _launch(tmp_path, 2, n, m, T, buckets, path=path, period=period, final_avg=1)
+    x = np.tile(synth.x0_host(sum(buckets)), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=period)
+    _compare(V, v)
+    _compare(X, oracle.global_average(x))

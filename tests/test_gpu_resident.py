@@ -190,3 +190,41 @@ def _padded(idx, buckets, offsets):
     starts = torch.tensor(np.concatenate([[0], np.cumsum(buckets)[:-1]]), device=idx.device)
     b = torch.searchsorted(starts, idx, right=True) - 1
     return idx - starts[b] + torch.tensor(offsets, device=idx.device)[b]
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+def test_local_sesgd_and_final_global_average(mode, fused):
+    """NEXT-2: Local-SESGD with period H = 3 (SESGD_OPT_LOCAL_PERIOD; exchange only when
+    (t + 1) % 3 == 0), then Algorithm 1's final global average (K8): the oracle's
+    bits after every stage."""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    n, m, T, H = 8, 2, 7, 3
+    buckets = [30001, 5, 4096]
+    L = sum(buckets)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    eng = SESGDEngine(n, m, buckets, mode=mode, options={C.OPT_LOCAL_PERIOD: H})
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(n):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), st)
+    for t in range(T):
+        for s in range(n):
+            for b, Lb in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), s, t, st)
+        eng.step(t, LR, MU, fused=fused)
+    torch.cuda.synchronize()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
+    V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, period=H, mode=mode)
+    _compare(X, x)
+    _compare(V, v)
+    assert sum(eng.stats(b)["kernel_launches"] for b in range(len(buckets))) == (T if fused else T * 3)
+    eng.global_average()
+    torch.cuda.synchronize()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
+    eng.close()
+    _compare(X, oracle.global_average(x.copy()))
