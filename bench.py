@@ -7,7 +7,7 @@
 Workload (BASELINE.json configs[1]): n = 8 workers, group_size = 2, ResNet-50 DDP
 buckets (5 buckets, 25,557,032 fp32 per worker), PARAM mode (Eq. 6), lr 0.1,
 momentum 0.9.  N=1: all 8 workers resident on one B200 (kernel K6).  N>1: 8/N
-workers per GPU, groups exchange over NVLink P2P (kernel K3); the total work is
+workers per GPU, groups exchange over NVLink P2P (kernel K4 two-shot); the total work is
 fixed ("scaling": "strong").  One step = one SESGD iteration over all buckets
 of all workers (every row of SURVEY.md Sec. 8(a): schedule, local step, group
 handshake + exchange + average, write-back).
@@ -310,6 +310,10 @@ def run_sesgd(args):
     hbm_peak, peak_src = measured_peaks()
     algo_bytes_per_step_gpu = BYTES_PER_WORKER_ELEM * L * r
     resident = (world == 1 and args.path in ("auto", "resident"))
+    # the path AUTO resolves to (sesgd_capi.cu resolve_path): K4 two-shot unless COMM CTAs
+    eff_path = args.path
+    if eff_path == "auto" and not resident:
+        eff_path = "oneshot" if args.p2p_variant >= 1 else "twoshot"
     if resident:
         kernel = "k6_resident"
         achieved = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
@@ -319,7 +323,7 @@ def run_sesgd(args):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        kernel = {"twoshot": "k4_twoshot", "ring": "k5_ring"}.get(args.path, "k3_push")
+        kernel = {"twoshot": "k4_twoshot", "ring": "k5_ring"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
         # of them 2(s-1)/s * 4 B per element (co-resident members pre-combine); max over
@@ -398,7 +402,7 @@ def run_sesgd(args):
                 "path": "resident (K6)" if resident else {
                     "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P (K4)",
                     "ring": "ring inside each group over NVLink P2P (K5)"}.get(
-                        args.path, "one-shot push over NVLink P2P (K3)"),
+                        eff_path, "one-shot push over NVLink P2P (K3)"),
                 "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush",
                 "parallelism": f"sesgd groups over {world} GPU(s)",
             },
