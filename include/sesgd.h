@@ -108,6 +108,12 @@ extern "C" {
                                     fires only when (t + 1) mod H == 0; other iterations run the
                                     local step alone (x <- x_hat).  H >= 1, default 1 = SESGD;
                                     group_size = n gives Local-SGD */
+#define SESGD_OPT_SCHEDULE 16      /* 0 (default): seeded uniform random partition (R1);
+                                    1: Stone's shuffle-exchange network -- iteration t exchanges
+                                    index dimensions (t p + q) mod d, q < p, for n = 2^d,
+                                    group_size = 2^p (else SESGD_EINVAL); n = 4, m = 2 gives the
+                                    paper's example {0,1},{2,3} -> {0,2},{1,3}; set it
+                                    identically on every rank, before sesgd_begin_iter */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

@@ -78,7 +78,9 @@ def lib():
                                        ctypes.c_float, i32, P, P]
         L.orc_run_ring_f32.restype = ctypes.c_int
         L.orc_run_local_f32.argtypes = [i32, i32, u64, i64, i64, i64, P, u64, ctypes.c_float,
-                                        ctypes.c_float, i32, i64, P, P]
+                                        ctypes.c_float, i32, i64, i32, P, P]
+        L.orc_groups_stone.argtypes = [i64, i32, i32, P, P]
+        L.orc_groups_stone.restype = ctypes.c_int
         L.orc_run_local_f32.restype = ctypes.c_int
         L.orc_global_average_f32.argtypes = [i32, i64, P]
         L.orc_global_average_f32.restype = ctypes.c_int
@@ -206,7 +208,19 @@ def run(n, m, seed, T, x, v, *, s_g, lr, mu, mode=MODE_PARAM, t0=0, coords=None)
     return x, v
 
 
-def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0, coords=None):
+SCHED_RANDOM, SCHED_STONE = 0, 1
+
+
+def groups_stone(t: int, n: int, m: int):
+    """(canon, group_of) of Stone's dimension-exchange schedule at iteration t (NEXT-3)."""
+    canon = np.empty(n, np.int32)
+    gof = np.empty(n, np.int32)
+    _check(lib().orc_groups_stone(t, n, m, _ptr(canon), _ptr(gof)))
+    return canon, gof
+
+
+def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0, coords=None,
+              schedule=SCHED_RANDOM):
     """Local-SESGD: T iterations where the group exchange fires only when
     (t + 1) % period == 0; float32 x, v (n, S) in place.  period = 1 is `run`; m = n is
     Local-SGD."""
@@ -218,7 +232,7 @@ def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0
         cp = _ptr(coords)
     assert x.dtype == np.float32 and x.flags.c_contiguous and v.flags.c_contiguous
     _check(lib().orc_run_local_f32(n, m, seed, t0, T, S, cp, s_g, float(lr), float(mu), mode,
-                                   int(period), _ptr(x), _ptr(v)))
+                                   int(period), int(schedule), _ptr(x), _ptr(v)))
     return x, v
 
 

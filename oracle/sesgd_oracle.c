@@ -102,6 +102,35 @@ int orc_groups(uint64_t seed, int64_t t, int32_t n, int32_t m, int32_t *raw, int
   return ORC_OK;
 }
 
+/* ---- NEXT-3: Stone's shuffle-exchange as a deterministic schedule (alternative reading of
+ * R1).  n = 2^d workers, m = 2^p: at iteration t the group of worker i is every worker that
+ * agrees with i on all index bits except dimensions (t*p + q) mod d, q = 0..p-1 (shuffling the
+ * index bits t*p times, then exchanging the low p bits).  n = 4, m = 2 gives {0,1},{2,3} then
+ * {0,2},{1,3}: the example of P:176-177. ---- */
+static int is_pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int orc_groups_stone(int64_t t, int32_t n, int32_t m, int32_t *canon, int32_t *group_of) {
+  if (n < 1 || m < 1 || m > n || t < 0 || !is_pow2(n) || !is_pow2(m)) return ORC_EINVAL;
+  int32_t d = 0, p = 0;
+  while ((1 << d) < n) ++d;
+  while ((1 << p) < m) ++p;
+  int32_t mask = 0; /* the p exchanged dimensions of iteration t */
+  for (int32_t q = 0; q < p; ++q) mask |= 1 << (int32_t)(((int64_t)t * p + q) % d);
+  int32_t j = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if ((i & mask) != 0) continue; /* i is the smallest member of its group */
+    int32_t r = 0;
+    for (int32_t w = 0; w < n; ++w) { /* ascending: every w that differs from i only in mask */
+      if ((w & ~mask) != i) continue;
+      if (canon) canon[(size_t)j * m + r] = w;
+      if (group_of) group_of[w] = j;
+      ++r;
+    }
+    ++j;
+  }
+  return ORC_OK;
+}
+
 /* ---- A6/A7: Eq. 2 and Eq. 3 exact forms ---- */
 int orc_latency(int32_t n, int32_t m, double bytes, double nu, double tau, double out[5]) {
   if (n < 1 || m < 1 || m > n) return ORC_EINVAL;
@@ -360,8 +389,9 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
 /* ---- Local-SESGD: exchange only when (t + 1) mod H == 0 ---- */
 int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                       const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
-                      int64_t H, float *x, float *v) {
+                      int64_t H, int32_t schedule, float *x, float *v) {
   if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || S < 0 || H < 1) return ORC_EINVAL;
+  if (schedule != 0 && schedule != 1) return ORC_EINVAL;
   if (n % m != 0) return ORC_ENOTDIV;
   float *g = (float *)malloc(sizeof(float) * (size_t)n * (size_t)(S > 0 ? S : 1));
   int32_t *canon = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
@@ -373,7 +403,8 @@ int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T
         g[(size_t)i * (size_t)S + (size_t)e] = synth_grad(key, coords ? coords[e] : e);
     }
     if ((t + 1) % H == 0) { /* synchronisation iteration: SESGD step with the groups of t */
-      rc = orc_groups(seed, t, n, m, NULL, canon, NULL);
+      rc = schedule == 1 ? orc_groups_stone(t, n, m, canon, NULL)
+                         : orc_groups(seed, t, n, m, NULL, canon, NULL);
       if (rc == ORC_OK) rc = orc_step_f32(n, m, canon, S, x, v, g, lr, mu, mode);
     } else { /* local iteration: every worker its own singleton group */
       for (int32_t i = 0; i < n; ++i) canon[i] = i;

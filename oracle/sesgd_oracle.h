@@ -85,10 +85,16 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
  * group exchange of iteration t fires only when (t + 1) mod H == 0 (groups of that t); on the
  * other iterations the locally updated parameters are kept (the iteration with m = 1:
  * PARAM x = xh, GRAD v = mu v + g, x = x - lr v).  H = 1 is SESGD; m = n is Local-SGD
- * (the paper's baseline with period 2). */
+ * (the paper's baseline with period 2).  schedule: 0 = orc_groups (R1),
+ * 1 = orc_groups_stone (NEXT-3). */
 int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                       const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
-                      int64_t H, float *x, float *v);
+                      int64_t H, int32_t schedule, float *x, float *v);
+
+/* NEXT-3, alternative reading of R1 (Stone's perfect shuffle): n = 2^d, m = 2^p; at
+ * iteration t worker i's group is every worker equal to i outside index dimensions
+ * (t*p + q) mod d, q < p (canonical form as orc_groups).  schedule 1 of orc_run_local_f32. */
+int orc_groups_stone(int64_t t, int32_t n, int32_t m, int32_t *canon, int32_t *group_of);
 
 /* Algorithm 1's last line: xbar = Ring-AllReduce(x_i; Global), the mean of the n
  * workers' parameters, left fold in ascending worker id then one division by n

@@ -17,6 +17,8 @@ namespace sesgd {
 // canon[n]: canonical partition, group_of[n]: group index per worker.
 void shuffle_exchange_groups(uint64_t seed, int64_t t, int n, int m, int32_t *canon,
                              int32_t *group_of);
+// NEXT-3: Stone's dimension-exchange schedule (n, m powers of two).
+void dimension_exchange_groups(int64_t t, int n, int m, int32_t *canon, int32_t *group_of);
 // Eq. 2 / Eq. 3 exact forms (A6/A7).
 void latency_model(int n, int m, double bytes, double nu, double tau, sesgd_cost *out);
 
@@ -170,6 +172,7 @@ struct sesgd_ctx {
   int release_delay = 1;    // SESGD_OPT_RELEASE_DELAY (two-shot kernel)
   int release_every = 3;    // SESGD_OPT_RELEASE_EVERY (two-shot kernel)
   int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
+  int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   int64_t *d_numels = nullptr;  // resident all-bucket launch: numel table [NB]
   bool resident_tables_ok = false;
   // attach
@@ -203,7 +206,6 @@ struct sesgd_ctx {
   bool iter_set = false;
   int64_t t = 0;
   int32_t canon[SESGD_MAX_WORKERS], group_of[SESGD_MAX_WORKERS];
-  int32_t canon_prev[SESGD_MAX_WORKERS], group_of_prev[SESGD_MAX_WORKERS];
   // errors
   unsigned long long *h_err = nullptr;  // pinned mapped error block (8 words)
   unsigned long long *d_err = nullptr;  // device alias of h_err

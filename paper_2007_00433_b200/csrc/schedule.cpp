@@ -78,6 +78,31 @@ void shuffle_exchange_groups(uint64_t seed, int64_t t, int n, int m, int32_t *ca
     }
 }
 
+// NEXT-3 (SESGD_OPT_SCHEDULE = 1): Stone's shuffle-exchange network as the schedule, the
+// deterministic reading of "shuffle-exchange" whose first two iterations for n = 4, m = 2 are
+// the paper's example {0,1},{2,3} -> {0,2},{1,3}.  n = 2^d, m = 2^p: iteration t
+// exchanges index dimensions (t p + q) mod d, q < p; a group is a base worker (zero in those
+// bits) OR-ed with every subset of them.  After d/p iterations of pure averaging every worker
+// holds the exact global mean (hypercube all-reduce).
+void dimension_exchange_groups(int64_t t, int n, int m, int32_t *canon, int32_t *group_of) {
+  const int d = __builtin_ctz(unsigned(n)), p = __builtin_ctz(unsigned(m));
+  unsigned mask = 0;
+  for (int q = 0; q < p; ++q) mask |= 1u << int((t * p + q) % d);
+  int j = 0;
+  for (unsigned base = 0; base < unsigned(n); ++base) {
+    if (base & mask) continue;
+    int r = 0;
+    unsigned sub = 0;
+    do {  // subsets of mask in increasing order
+      const int w = int(base | sub);
+      canon[j * m + r++] = w;
+      if (group_of) group_of[w] = j;
+      sub = (sub - mask) & mask;
+    } while (sub != 0);
+    ++j;
+  }
+}
+
 // Eq. 2: T = 2(n-1)(G/(n nu) + t_tau); Eq. 3 before its approximation
 // (P:179-181): the same ring inside a group of m = n/k members.
 void latency_model(int n, int m, double bytes, double nu, double tau, sesgd_cost *out) {

@@ -172,6 +172,14 @@ void freeze_layout(sesgd_ctx *ctx) {
 // same iterations).  bucket < 0: every bucket in one launch.
 int upload_resident_tables(sesgd_ctx *ctx);
 
+// the canonical partition of iteration t under the context's schedule (SESGD_OPT_SCHEDULE)
+void make_groups(const sesgd_ctx *ctx, int64_t t, int32_t *canon, int32_t *group_of) {
+  if (ctx->schedule == 1)
+    sesgd::dimension_exchange_groups(t, ctx->n, ctx->m, canon, group_of);
+  else
+    sesgd::shuffle_exchange_groups(ctx->seed, t, ctx->n, ctx->m, canon, group_of);
+}
+
 bool local_only_iteration(const sesgd_ctx *ctx) {
   return ctx->local_period > 1 && (ctx->t + 1) % ctx->local_period != 0;
 }
@@ -484,7 +492,7 @@ void sesgd_destroy(sesgd_ctx *ctx) {
 
 int sesgd_groups(const sesgd_ctx *ctx, int64_t iter, int32_t *perm_out, int32_t *group_of_out) {
   if (!ctx || !perm_out || iter < 0) return SESGD_EINVAL;
-  sesgd::shuffle_exchange_groups(ctx->seed, iter, ctx->n, ctx->m, perm_out, group_of_out);
+  make_groups(ctx, iter, perm_out, group_of_out);
   return SESGD_OK;
 }
 
@@ -554,6 +562,14 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       if (value < 1 || value > 16) return fail(ctx, SESGD_EINVAL, "release interval must be in [1, 16]");
       ctx->release_every = int(value);
       return SESGD_OK;
+    case SESGD_OPT_SCHEDULE: {
+      auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "schedule must be 0 or 1");
+      if (value == 1 && (!pow2(ctx->n) || !pow2(ctx->m)))
+        return fail(ctx, SESGD_EINVAL, "the dimension-exchange schedule needs n and group_size powers of two");
+      ctx->schedule = int(value);
+      return SESGD_OK;
+    }
     case SESGD_OPT_LOCAL_PERIOD:
       if (value < 1) return fail(ctx, SESGD_EINVAL, "local period must be >= 1");
       ctx->local_period = value;
@@ -739,10 +755,7 @@ int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter) {
   if (!ctx) return SESGD_EINVAL;
   if (iter < 0) return fail(ctx, SESGD_EINVAL, "iteration must be >= 0");
   if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
-  sesgd::shuffle_exchange_groups(ctx->seed, iter, ctx->n, ctx->m, ctx->canon, ctx->group_of);
-  if (iter >= 2)
-    sesgd::shuffle_exchange_groups(ctx->seed, iter - 2, ctx->n, ctx->m, ctx->canon_prev,
-                                   ctx->group_of_prev);
+  make_groups(ctx, iter, ctx->canon, ctx->group_of);
   ctx->t = iter;
   ctx->iter_set = true;
   return SESGD_OK;

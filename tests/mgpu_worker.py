@@ -34,6 +34,7 @@ def main():
     p.add_argument("--tma", type=int, default=0)
     p.add_argument("--period", type=int, default=1)
     p.add_argument("--final-avg", type=int, default=0)
+    p.add_argument("--schedule", type=int, default=0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -48,7 +49,8 @@ def main():
                       hop_delay_ns=a.hop_ns,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
                                                    (C.OPT_PUSH_TMA, a.tma),
-                                                   (C.OPT_LOCAL_PERIOD, a.period)) if v})
+                                                   (C.OPT_LOCAL_PERIOD, a.period),
+                                                   (C.OPT_SCHEDULE, a.schedule)) if v})
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):

@@ -62,6 +62,29 @@ def test_host_scheduler_bitexact_vs_oracle(n, m):
             C.sesgd_destroy(ctx)
 
 
+@pytest.mark.parametrize("n,m", [(2, 2), (4, 2), (8, 2), (8, 4), (16, 4), (32, 8), (64, 2), (64, 64)])
+def test_dimension_exchange_schedule_bitexact_vs_oracle(n, m):
+    """NEXT-3 (SESGD_OPT_SCHEDULE = 1): the product's dimension-exchange schedule equals the
+    oracle's (independent implementations); non-powers of two are rejected."""
+    ctx = C.sesgd_init(n, m, 42)
+    try:
+        C.sesgd_set_option(ctx, C.OPT_SCHEDULE, C.SCHEDULE_DIMENSION_EXCHANGE)
+        for t in list(range(0, 40)) + [10 ** 6 + 3]:
+            perm, gof = C.sesgd_groups(ctx, t, n)
+            canon, ogof = oracle.groups_stone(t, n, m)
+            assert np.array_equal(perm, canon), (n, m, t)
+            assert np.array_equal(gof, ogof)
+    finally:
+        C.sesgd_destroy(ctx)
+    ctx = C.sesgd_init(12, 3, 42)
+    try:
+        with pytest.raises(C.SesgdError) as e:
+            C.sesgd_set_option(ctx, C.OPT_SCHEDULE, 1)
+        assert e.value.code == C.EINVAL
+    finally:
+        C.sesgd_destroy(ctx)
+
+
 def test_latency_model_matches_oracle():
     """Row a7: Eq. 2 / Eq. 3 exact forms equal the oracle's, bit for bit."""
     rng = np.random.default_rng(5)

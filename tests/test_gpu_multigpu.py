@@ -29,7 +29,7 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0):
+            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -41,6 +41,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
+               "--schedule", str(schedule),
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -277,3 +278,17 @@ def test_two_gpus_local_sesgd_final_average(tmp_path, n, m, period, path):
     oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=period)
     _compare(V, v)
     _compare(X, oracle.global_average(x))
+
+
+@pytest.mark.parametrize("gpus,n,m", [(2, 4, 2), (2, 8, 4), (4, 8, 2)])
+def test_dimension_exchange_schedule_multigpu(tmp_path, gpus, n, m):
+    """NEXT-3 over NVLink (K4): Stone's dimension-exchange schedule, the oracle's bits."""
+    buckets = [65537, 3]
+    T = 6
+    X, V = _launch(tmp_path, gpus, n, m, T, buckets, schedule=1)
+    x = np.tile(synth.x0_host(sum(buckets)), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1,
+                     schedule=oracle.SCHED_STONE)
+    _compare(X, x)
+    _compare(V, v)

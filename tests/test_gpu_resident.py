@@ -228,3 +228,32 @@ def test_local_sesgd_and_final_global_average(mode, fused):
     X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
     eng.close()
     _compare(X, oracle.global_average(x.copy()))
+
+
+@pytest.mark.parametrize("n,m,period", [(8, 2, 1), (16, 4, 2), (4, 2, 1)])
+def test_dimension_exchange_schedule(n, m, period):
+    """NEXT-3: Stone's dimension-exchange schedule (SESGD_OPT_SCHEDULE = 1), optionally with a
+    local period: the oracle's bits (its own schedule implementation)."""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    T, buckets = 6, [20001, 3]
+    L = sum(buckets)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    eng = SESGDEngine(n, m, buckets, options={C.OPT_SCHEDULE: 1, C.OPT_LOCAL_PERIOD: period})
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(n):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), st)
+    for t in range(T):
+        for s in range(n):
+            for b, Lb in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), s, t, st)
+        eng.step(t, LR, MU)
+    torch.cuda.synchronize()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
+    eng.close()
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, period=period,
+                     schedule=oracle.SCHED_STONE)
+    _compare(X, x)

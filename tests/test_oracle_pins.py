@@ -600,3 +600,71 @@ def test_global_average_matches_sequential_mean():
             s = np.float32(s + x32[i, e])
         assert got32[3, e] == np.float32(s / np.float32(16))
     np.testing.assert_allclose(got32[0], exact, rtol=0, atol=16 * 6e-8 * np.abs(x64).max())
+
+
+# ---------------------------------------------------------------- NEXT-3: Stone dimension exchange
+def test_stone_schedule_paper_example():
+    """P:176-177: "at iteration t the groups are {0,1},{2,3}; at t+1 it may be {0,2},{1,3}"."""
+    c0, _ = oracle.groups_stone(0, 4, 2)
+    c1, _ = oracle.groups_stone(1, 4, 2)
+    assert c0.tolist() == [0, 1, 2, 3] and c1.tolist() == [0, 2, 1, 3]
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64])
+def test_stone_schedule_partitions_and_exact_mean(n):
+    """Every iteration is a canonical equal partition; the product of the averaging matrices W_t
+    over d/p consecutive iterations is exactly J/n in rational arithmetic (the shuffle-exchange
+    network all-reduce: every worker holds the global mean), for every m = 2^p dividing d."""
+    from fractions import Fraction
+    d = n.bit_length() - 1
+    for p in range(1, d + 1):
+        m = 1 << p
+        if d % p:
+            continue
+        for t0 in range(3):
+            prod = [[Fraction(int(i == j)) for j in range(n)] for i in range(n)]
+            for t in range(t0, t0 + d // p):
+                canon, gof = oracle.groups_stone(t, n, m)
+                groups = [canon[j * m:(j + 1) * m].tolist() for j in range(n // m)]
+                assert sorted(sum(groups, [])) == list(range(n))
+                assert all(g == sorted(g) for g in groups)
+                assert [g[0] for g in groups] == sorted(g[0] for g in groups)
+                W = [[Fraction(int(gof[i] == gof[j]), m) for j in range(n)] for i in range(n)]
+                prod = [[sum(W[i][k] * prod[k][j] for k in range(n)) for j in range(n)] for i in range(n)] \
+                    if n <= 16 else prod
+            if n <= 16:
+                assert all(prod[i][j] == Fraction(1, n) for i in range(n) for j in range(n))
+
+
+def test_stone_schedule_pure_averaging_reaches_global_mean():
+    """lr = 0, distinct x_0 per worker: after log2(n) / p iterations of the oracle step, every
+    worker equals the global mean (fp64, within rounding of math.fsum / n)."""
+    n, m, L = 16, 2, 23
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, L))
+    exact = np.array([math.fsum(x[:, e]) / n for e in range(L)])
+    v = np.zeros_like(x)
+    for t in range(4):
+        canon, _ = oracle.groups_stone(t, n, m)
+        oracle.step(n, m, canon, x, v, np.zeros_like(x), 0.0, 0.0)
+    np.testing.assert_allclose(x, np.tile(exact, (n, 1)), rtol=0, atol=1e-15)
+
+
+def test_stone_schedule_errors_and_run():
+    """Non-powers of two are rejected; run_local(schedule=STONE, period=1) is the iteration loop
+    of oracle.step over groups_stone."""
+    with pytest.raises(oracle.OracleError):
+        oracle.groups_stone(0, 6, 2)
+    with pytest.raises(oracle.OracleError):
+        oracle.groups_stone(0, 8, 3)
+    n, m, T, L = 8, 2, 5, 33
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, SEED, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1,
+                     schedule=oracle.SCHED_STONE)
+    y = np.tile(synth.x0_host(L), (n, 1))
+    w = np.zeros_like(y)
+    for t in range(T):
+        canon, _ = oracle.groups_stone(t, n, m)
+        oracle.step(n, m, canon, y, w, _grads(n, t, L, np.float32), 0.1, 0.9)
+    assert np.array_equal(x, y) and np.array_equal(v, w)
