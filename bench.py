@@ -137,10 +137,19 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def cfg_label(workload, n, m):
+    """BASELINE.json config the run corresponds to (configs[1] = cfg2, configs[2] = cfg3)."""
+    if workload == "resnet50" and n == 8 and m == 2:
+        return "cfg2"
+    if workload == "vgg16" and n == 16 and m == 4:
+        return "cfg3"
+    return "custom"
+
+
 # ---------------------------------------------------------------- CPU oracle leg
-def cpu_oracle_rate(n, m, budget_s, mode):
+def cpu_oracle_rate(n, m, budget_s, mode, L_total, workload):
     """Time the oracle as it stands (single-threaded C) on a bounded coordinate sample of the
-    same workload.  Returns (GB/s, sample description, seconds)."""
+    same workload (L_total fp32 per worker).  Returns (GB/s, sample description, seconds)."""
     import numpy as np
 
     import oracle
@@ -148,7 +157,7 @@ def cpu_oracle_rate(n, m, budget_s, mode):
     omode = oracle.MODE_PARAM if mode == "param" else oracle.MODE_GRAD
 
     def run(S, T, t0=0):
-        coords = np.arange(S, dtype=np.int64) * 7 % 25557032
+        coords = np.arange(S, dtype=np.int64) * 7 % L_total
         x = np.tile(synth.x0_host(S, coords=coords), (n, 1))
         v = np.zeros_like(x)
         t = time.perf_counter()
@@ -158,11 +167,11 @@ def cpu_oracle_rate(n, m, budget_s, mode):
     probe_S, probe_T = 20000, 2
     dt = run(probe_S, probe_T)
     rate = n * probe_S * probe_T / dt  # worker-elements / s
-    S = int(max(1000, min(25557032, rate * budget_s / (n * 4))))
+    S = int(max(1000, min(L_total, rate * budget_s / (n * 4))))
     T = int(max(4, min(100, rate * budget_s / (n * S))))
     dt = run(S, T)
     gbs = BYTES_PER_WORKER_ELEM * n * S * T / dt / 1e9
-    sample = (f"n={n}, m={m}: {S} of 25,557,032 coordinates x {T} iterations "
+    sample = (f"{workload}, n={n}, m={m}: {S} of {L_total:,} coordinates x {T} iterations "
               f"({n * S * T:.3g} worker-elements, {dt:.1f} s, single-threaded C oracle, fp32-emulate)")
     return gbs, sample, dt
 
@@ -175,7 +184,9 @@ def run_reference(args):
 
     import oracle
     import synth
+    from paper_2007_00433_b200.workloads import WORKLOADS
     n, m = args.n, args.group_size
+    L_total = int(sum(WORKLOADS[args.workload]))
     omode = oracle.MODE_PARAM if args.mode == "param" else oracle.MODE_GRAD
     # each step: one oracle iteration over a bounded coordinate sample of the workload
     steps, warm = args.steps, args.warmup
@@ -187,7 +198,7 @@ def run_reference(args):
     t = time.perf_counter()
     oracle.run(n, m, SEED, 1, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, coords=coords)
     rate = n * S0 / (time.perf_counter() - t)
-    S = int(max(1000, min(25557032, rate * per_step_budget / n)))
+    S = int(max(1000, min(L_total, rate * per_step_budget / n)))
     coords = np.arange(S, dtype=np.int64)
     x = np.tile(synth.x0_host(S, coords=coords), (n, 1))
     v = np.zeros_like(x)
@@ -198,12 +209,13 @@ def run_reference(args):
         oracle.run(n, m, SEED, 1, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, t0=t, coords=coords)
     dt = time.perf_counter() - t0
     gbs = BYTES_PER_WORKER_ELEM * n * S * steps / dt / 1e9
-    sample = f"n={n}, m={m}: {S} of 25,557,032 coordinates per step, 1 iteration per step"
+    sample = f"{args.workload}, n={n}, m={m}: {S} of {L_total:,} coordinates per step, 1 iteration per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"cfg2 sample: {sample}", "n": n, "group_size": m, "mode": args.mode},
+        "config": {"workload": f"{cfg_label(args.workload, n, m)} sample: {sample}", "n": n, "group_size": m,
+                   "mode": args.mode},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -384,7 +396,7 @@ def run_sesgd(args):
     lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, 1.5e-6)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        gbs, sample, _ = cpu_oracle_rate(n, m, args.cpu_seconds, args.mode)
+        gbs, sample, _ = cpu_oracle_rate(n, m, args.cpu_seconds, args.mode, L, args.workload)
         cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample}
     clocks = clk.summary()
     if world > 1:
@@ -395,7 +407,7 @@ def run_sesgd(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {
-                "workload": (f"cfg2: n={n} workers, group_size={m}, {args.workload} DDP buckets "
+                "workload": (f"{cfg_label(args.workload, n, m)}: n={n} workers, group_size={m}, {args.workload} DDP buckets "
                              f"({nb} buckets, {L:,} fp32 per worker), {args.mode.upper()} mode, "
                              f"lr {LR}, momentum {MU}; {r} worker(s) resident per GPU"),
                 "n": n, "group_size": m, "workers_per_gpu": r,

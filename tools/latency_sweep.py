@@ -7,7 +7,8 @@ per-hop latency -- on real NVLink (run under torch.distributed.run, one worker p
 For every group size m | n (m = n is Ring-SGD), every bucket size and every injected hop
 delay, times one sesgd_sync_step through
   * the ring path (K5: the paper's Ring-AllReduce inside each group, 2(m-1) handshakes), and
-  * the one-shot push path (K3: one handshake round),
+  * the one-shot push path (K3: one handshake round), and
+  * the two-shot push path (K4, the default: two handshake rounds),
 as the max over ranks of the median CUDA-event time, and prints it next to the latency
 model of Eq. 2 / Eq. 3 (sesgd_latency_model) evaluated with the measured per-hop latency
 and push bandwidth.  Reproduces the SHAPE of the paper's Fig. 6 / "5x at 5 ms" argument
@@ -48,7 +49,7 @@ def main():
     rows = []
     stream = torch.cuda.current_stream()
     for m in [d for d in range(2, n + 1) if n % d == 0]:
-        for path, pname in ((C.PATH_RING, "ring"), (C.PATH_ONESHOT, "oneshot")):
+        for path, pname in ((C.PATH_RING, "ring"), (C.PATH_ONESHOT, "oneshot"), (C.PATH_TWOSHOT, "twoshot")):
             for hop in hops:
                 eng = SESGDEngine(n, m, sizes, rank=rank, world=world, path=path, hop_delay_ns=hop,
                                   timeout_ms=60000)
@@ -76,7 +77,8 @@ def main():
                     model = C.sesgd_latency_model(n, m, 4.0 * L, a.nu_gbs * 1e9, a.tau_us * 1e-6 + hop * 1e-9)
                     rows.append({"n": n, "m": m, "path": pname, "bytes": 4 * L, "hop_us": hop / 1e3,
                                  "measured_us": float(tt.item()),
-                                 "handshakes_per_call": 2 * (m - 1) if pname == "ring" else (1 if m > 1 else 0),
+                                 "handshakes_per_call": (2 * (m - 1) if pname == "ring" else
+                                                         {"oneshot": 1, "twoshot": 2}[pname] if m > 1 else 0),
                                  "model_group_us": model["sesgd_s"] * 1e6, "model_ring_n_us": model["ring_s"] * 1e6})
                 eng.poll()
                 eng.close()
