@@ -389,7 +389,8 @@ def run_sesgd(args):
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 4 * L * n, "d2h_bytes_per_step": 4 * L * n,
                "ms_per_step": e2e_ms, "steps": args.e2e_steps,
-               "api": "sesgd_sync_step_host (pinned host g in, updated x out, every worker)"}
+               "api": "sesgd_sync_all_host (pinned host g in, updated x out, every worker; H2D / "
+                      "kernels / D2H of different buckets pipelined on copy streams)"}
     eng.poll()
 
     stats = [eng.stats(b) for b in range(nb)]

@@ -225,6 +225,16 @@ SESGD_API int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *str
 SESGD_API int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,
                          const float *const *g_host, float *const *x_host_out, void *stream);
 
+/* Every bucket through host buffers, pipelined: g_host[b * n_local + s] (bucket b, local slot s;
+ * numel_b floats each, pinned) -> device gradients on an internal copy stream, bucket b's
+ * sesgd_sync_step on `stream` as soon as its gradients landed, its parameters -> x_host_out[b *
+ * n_local + s] on a second internal copy stream, so H2D, kernels and D2H of different buckets
+ * overlap (PCIe is full duplex).  When `stream` completes, every copy has completed.  The
+ * device gradients are overwritten only after the work already queued on `stream`.
+ * Errors: as sesgd_sync_step, SESGD_EINVAL (null buffer). */
+SESGD_API int sesgd_sync_all_host(sesgd_ctx *ctx, float lr, float momentum, const float *const *g_host,
+                                  float *const *x_host_out, void *stream);
+
 /* Algorithm 1's last line, xbar <- Ring-AllReduce(x_i; Global), for bucket `bucket`:
  * every LOCAL worker's parameters become (rows[0] (+) rows[1] (+) ... (+) rows[n-1]) (/) n,
  * a left fold in ascending worker id (R7, R10).  rows: host array of n device pointers to the n

@@ -173,6 +173,10 @@ struct sesgd_ctx {
   int release_every = 3;    // SESGD_OPT_RELEASE_EVERY (two-shot kernel)
   int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
+  // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k, ev_out;
+  cudaEvent_t ev_start = nullptr;
   int64_t *d_numels = nullptr;  // resident all-bucket launch: numel table [NB]
   bool resident_tables_ok = false;
   // attach

@@ -487,6 +487,11 @@ void sesgd_destroy(sesgd_ctx *ctx) {
   if (ctx->d_bv) cudaFree(ctx->d_bv);
   if (ctx->d_bg) cudaFree(const_cast<float **>(ctx->d_bg));
   if (ctx->d_numels) cudaFree(ctx->d_numels);
+  for (auto *v : {&ctx->ev_in, &ctx->ev_k, &ctx->ev_out})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   delete ctx;
 }
 
@@ -976,6 +981,62 @@ int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentu
     cudaError_t e = cudaMemcpyAsync(x_host_out[s], b.hx[s], bytes, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H parameter copy");
   }
+  return SESGD_OK;
+}
+
+int sesgd_sync_all_host(sesgd_ctx *ctx, float lr, float momentum, const float *const *g_host,
+                        float *const *x_host_out, void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  if (!g_host || !x_host_out) return fail(ctx, SESGD_EINVAL, "null host buffer table");
+  if (!ctx->attached || !ctx->iter_set) return fail(ctx, SESGD_ESTATE, "attach and begin_iter first");
+  const size_t nb = ctx->buckets.size();
+  if (nb == 0) return fail(ctx, SESGD_ESTATE, "no bucket registered");
+  const int r = ctx->n_local;
+  for (size_t i = 0; i < nb * size_t(r); ++i)
+    if (!g_host[i] || !x_host_out[i]) return fail(ctx, SESGD_EINVAL, "null host buffer");
+  cudaError_t e = cudaSuccess;
+  if (!ctx->copy_in) {
+    e = cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy streams");
+  }
+  for (auto *v : {&ctx->ev_in, &ctx->ev_k, &ctx->ev_out})
+    while (v->size() < nb) {
+      cudaEvent_t ev;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "copy events");
+      v->push_back(ev);
+    }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // H2D of every bucket on copy_in, after the work already queued on `stream`
+  e = cudaEventRecord(ctx->ev_start, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_in, ctx->ev_start, 0);
+  for (size_t b = 0; b < nb && e == cudaSuccess; ++b) {
+    const sesgd_bucket &bk = ctx->buckets[b];
+    for (int s = 0; s < r && e == cudaSuccess; ++s)
+      e = cudaMemcpyAsync(const_cast<float *>(bk.hg[s]), g_host[b * r + s], size_t(bk.numel) * 4,
+                          cudaMemcpyHostToDevice, ctx->copy_in);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_in[b], ctx->copy_in);
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D gradient copies");
+  // bucket b's kernel as soon as its gradients landed; its D2H on copy_out right after it
+  for (size_t b = 0; b < nb; ++b) {
+    e = cudaStreamWaitEvent(st, ctx->ev_in[b], 0);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "wait H2D");
+    const int rc = sesgd_sync_step(ctx, int32_t(b), lr, momentum, stream);
+    if (rc != SESGD_OK) return rc;
+    e = cudaEventRecord(ctx->ev_k[b], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_out, ctx->ev_k[b], 0);
+    const sesgd_bucket &bk = ctx->buckets[b];
+    for (int s = 0; s < r && e == cudaSuccess; ++s)
+      e = cudaMemcpyAsync(x_host_out[b * r + s], bk.hx[s], size_t(bk.numel) * 4, cudaMemcpyDeviceToHost,
+                          ctx->copy_out);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_out[b], ctx->copy_out);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H parameter copies");
+  }
+  e = cudaStreamWaitEvent(st, ctx->ev_out[nb - 1], 0);  // copy_out is in order: every D2H done
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "wait D2H");
   return SESGD_OK;
 }
 

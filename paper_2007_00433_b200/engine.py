@@ -132,10 +132,16 @@ class SESGDEngine:
                 self.sync_step(b, lr, momentum, stream)
 
     def step_host(self, t: int, lr: float, momentum: float, g_host, x_host,
-                  stream: Optional[torch.cuda.Stream] = None):
-        """End-to-end through host buffers: g_host[b][slot] -> device, sync, device x -> x_host[b][slot]."""
+                  stream: Optional[torch.cuda.Stream] = None, pipelined: bool = True):
+        """End-to-end through host buffers: g_host[b][slot] -> device, sync, device x ->
+        x_host[b][slot]; pipelined (sesgd_sync_all_host: H2D / kernels / D2H of different
+        buckets overlap) or one sesgd_sync_step_host per bucket."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.begin_iter(t)
+        if pipelined:
+            C.sesgd_sync_all_host(self.ctx, lr, momentum, [h.data_ptr() for hb in g_host for h in hb],
+                                  [h.data_ptr() for hb in x_host for h in hb], s.cuda_stream)
+            return
         for b in range(len(self.bucket_sizes)):
             C.sesgd_sync_step_host(self.ctx, b, lr, momentum, [h.data_ptr() for h in g_host[b]],
                                    [h.data_ptr() for h in x_host[b]], s.cuda_stream)

@@ -31,7 +31,7 @@ EXPORTED = (
     "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
-    "sesgd_global_average",
+    "sesgd_global_average", "sesgd_sync_all_host",
 )
 
 
@@ -79,6 +79,7 @@ def lib():
             "sesgd_sync_step_host": ([P, i32, f32, f32, P, P, P], ctypes.c_int),
             "sesgd_sync_all": ([P, f32, f32, P], ctypes.c_int),
             "sesgd_global_average": ([P, i32, P, i32, P], ctypes.c_int),
+            "sesgd_sync_all_host": ([P, f32, f32, P, P, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -179,6 +180,13 @@ def sesgd_sync_step_host(ctx, bucket: int, lr: float, momentum: float, g_host_pt
                          stream: int = 0) -> None:
     _check(lib().sesgd_sync_step_host(ctx, bucket, lr, momentum, _ptr_array(g_host_ptrs),
                                       _ptr_array(x_host_ptrs), ctypes.c_void_p(int(stream))), ctx)
+
+
+def sesgd_sync_all_host(ctx, lr: float, momentum: float, g_host_ptrs, x_host_ptrs,
+                        stream: int = 0) -> None:
+    """g_host_ptrs / x_host_ptrs: flat [bucket * n_local + slot] host pointers."""
+    _check(lib().sesgd_sync_all_host(ctx, lr, momentum, _ptr_array(g_host_ptrs),
+                                     _ptr_array(x_host_ptrs), ctypes.c_void_p(int(stream))), ctx)
 
 
 def sesgd_global_average(ctx, bucket: int, n: int, row_ptrs=None, stream: int = 0) -> None:

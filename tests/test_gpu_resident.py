@@ -257,3 +257,32 @@ def test_dimension_exchange_schedule(n, m, period):
     oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, period=period,
                      schedule=oracle.SCHED_STONE)
     _compare(X, x)
+
+
+@pytest.mark.parametrize("pipelined", [True, False])
+def test_host_buffer_path(pipelined):
+    """The end-to-end host-buffer calls (sesgd_sync_all_host pipelined on copy streams, and
+    sesgd_sync_step_host per bucket): pinned host gradients in, updated parameters out, the
+    oracle's bits."""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200.workloads import CONFIG1_BUCKETS
+    n, m, T = 4, 2, 3
+    buckets = list(CONFIG1_BUCKETS)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    eng = SESGDEngine(n, m, buckets)
+    st = torch.cuda.current_stream()
+    for s in range(n):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), st.cuda_stream)
+    g_host = [[torch.empty(Lb).pin_memory() for _ in range(n)] for Lb in buckets]
+    x_host = [[torch.empty(Lb).pin_memory() for _ in range(n)] for Lb in buckets]
+    for t in range(T):
+        for b, Lb in enumerate(buckets):
+            for s in range(n):
+                g_host[b][s].copy_(torch.from_numpy(synth.grad_host(s, t, Lb, e0=int(offs[b]))))
+        eng.step_host(t, LR, MU, g_host, x_host, pipelined=pipelined)
+        torch.cuda.synchronize()
+    X = np.stack([np.concatenate([x_host[b][s].numpy() for b in range(len(buckets))]) for s in range(n)])
+    eng.close()
+    x, _ = _run_oracle(n, m, sum(buckets), T, oracle.MODE_PARAM)
+    _compare(X, x)
