@@ -53,6 +53,7 @@ def parse():
     p.add_argument("--push-tma", type=int, default=0, help="two-shot: TMA bulk pushes (SESGD_OPT_PUSH_TMA)")
     p.add_argument("--release-delay", type=int, default=0, help="two-shot: SESGD_OPT_RELEASE_DELAY")
     p.add_argument("--release-every", type=int, default=0, help="two-shot: SESGD_OPT_RELEASE_EVERY")
+    p.add_argument("--release-stagger", type=int, default=0, help="SESGD_OPT_RELEASE_STAGGER")
     p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot", "ring", "twoshot"])
     p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
     p.add_argument("--comm-batch", type=int, default=0)
@@ -255,7 +256,8 @@ def run_sesgd(args):
                                                  (C.OPT_RESIDENT_UNROLL, args.resident_unroll),
                                                  (C.OPT_PUSH_TMA, args.push_tma),
                                                  (C.OPT_RELEASE_DELAY, args.release_delay),
-                                                 (C.OPT_RELEASE_EVERY, args.release_every)) if v},
+                                                 (C.OPT_RELEASE_EVERY, args.release_every),
+                                                 (C.OPT_RELEASE_STAGGER, args.release_stagger)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
                             "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT}[args.path])
     r = eng.r

@@ -114,6 +114,9 @@ extern "C" {
                                     group_size = 2^p (else SESGD_EINVAL); n = 4, m = 2 gives the
                                     paper's example {0,1},{2,3} -> {0,2},{1,3}; set it
                                     identically on every rank, before sesgd_begin_iter */
+#define SESGD_OPT_RELEASE_STAGGER 17 /* 1 (default): CTA i takes its flag-release steps at
+                                    (k + i) mod R = 0, so the CTAs sharing an SM fence in turn;
+                                    0: all at k mod R = 0 */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

@@ -88,6 +88,7 @@ struct P2PArgs {
   int lag;                          // COMPUTE folds chunk step k - lag after staging step k
   int release_delay;                // two-shot: steps between a push and its flag release
   int release_every;                // two-shot: chunk steps between flag-release batches
+  int release_stagger;              // offset each CTA's release steps by its index
   int parity;                       // call & 1: receive slots / ready flags double buffer
   int my_rank;
   int bucket, nbuckets;             // bucket of a single-bucket launch, -1 for all buckets
@@ -171,6 +172,7 @@ struct sesgd_ctx {
   int push_tma = 0;         // SESGD_OPT_PUSH_TMA (two-shot kernel)
   int release_delay = 1;    // SESGD_OPT_RELEASE_DELAY (two-shot kernel)
   int release_every = 3;    // SESGD_OPT_RELEASE_EVERY (two-shot kernel)
+  int release_stagger = 1;  // SESGD_OPT_RELEASE_STAGGER
   int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)

@@ -779,7 +779,7 @@ struct Split {
     int64_t out = 0;  // chunk ordinals whose ready flags are released
     uint64_t t_stage = 0, t_fold = 0, t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
     for (int64_t k = 0; k < nk + L; ++k) {
-      if (k % R == 0 || k == nk) {
+      if ((k + (a.release_stagger ? i : 0)) % R == 0 || k == nk) {
         const int64_t c1 = k < nk ? k : nk;
         release_ready(first, out, c1);
         out = c1;
@@ -1145,7 +1145,9 @@ struct Split {
     uint64_t t_stage = 0, t_red = 0, t_fin = 0, t_rel = 0;
     uint64_t t0 = a.prof ? dev::globaltimer() : 0, tstart = t0;
     for (int64_t k = 0; k < nk + 2 * L; ++k) {
-      if (k % R == 0) {  // pushes of steps <= k - D: RS of ordinals < k-D+1, AG of < k-D-L+1
+      // pushes of steps <= k - D: RS of ordinals < k-D+1, AG of < k-D-L+1; with stagger the CTAs
+      // of an SM take their release steps in turn instead of all at once
+      if ((k + (a.release_stagger ? i : 0)) % R == 0) {
         const int64_t rs1 = clampk(k - D + 1), ag1 = clampk(k - D - L + 1);
         int newer = 0;
         if constexpr (TMA)

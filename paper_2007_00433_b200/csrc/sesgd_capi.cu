@@ -379,6 +379,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.lag = twoshot ? (ctx->fold_lag + 1) / 2 : ctx->fold_lag;  // two-shot: per round
   a.release_delay = ctx->release_delay;
   a.release_every = ctx->release_every;
+  a.release_stagger = ctx->release_stagger;
   a.parity = int(call & 1);
   a.my_rank = ctx->rank;
   a.bucket = bucket;
@@ -578,6 +579,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
     case SESGD_OPT_LOCAL_PERIOD:
       if (value < 1) return fail(ctx, SESGD_EINVAL, "local period must be >= 1");
       ctx->local_period = value;
+      return SESGD_OK;
+    case SESGD_OPT_RELEASE_STAGGER:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "release stagger must be 0 or 1");
+      ctx->release_stagger = int(value);
       return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");
