@@ -396,6 +396,8 @@ def run_sesgd(args):
     eng.poll()
 
     stats = [eng.stats(b) for b in range(nb)]
+    # consistency of the workers' parameters after the run (K9), outside the timed region
+    css, cmx = eng.consensus(stream)
     lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, 1.5e-6)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -435,6 +437,9 @@ def run_sesgd(args):
                 "model_ratio": lat["ratio"],
             },
             "paper_context": PAPER_CONTEXT,
+            "consistency": {"after_iterations": t_next, "sum_sq_dev_from_mean": css,
+                            "rms_dev": (css / (n * L)) ** 0.5, "max_abs_dev": cmx,
+                            "note": "SESGD keeps the workers consistent (P:430-433); x0 ~ U[-1/8, 1/8)"},
         }
         print(json.dumps(line), flush=True)
     eng.close()

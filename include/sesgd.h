@@ -248,6 +248,16 @@ SESGD_API int sesgd_sync_all_host(sesgd_ctx *ctx, float lr, float momentum, cons
 SESGD_API int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *const *rows,
                                    int32_t nrows, void *stream);
 
+/* Consistency of the workers' parameters (the question of Fig. 7b), bucket
+ * `bucket`: with xbar the binary64 mean of the n workers' parameters,
+ *   out_dev[0] += sum_i sum_e (x_i[e] - xbar[e])^2      (n x the consensus distance)
+ *   out_dev[1]  = max(out_dev[1], max_i,e |x_i[e] - xbar[e]|)
+ * out_dev: 2 doubles of caller-owned device memory (zero them before the first bucket; calls
+ * accumulate across buckets).  rows as in sesgd_global_average (NULL: all workers local).
+ * Asynchronous on `stream` (K9, binary64 accumulation).  Errors: as sesgd_global_average. */
+SESGD_API int sesgd_consensus(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,
+                              double *out_dev, void *stream);
+
 /* Non-blocking check of the latched device error word: SESGD_OK or SESGD_ETIMEOUT. */
 SESGD_API int sesgd_poll(sesgd_ctx *ctx);
 

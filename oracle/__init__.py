@@ -86,6 +86,8 @@ def lib():
         L.orc_global_average_f32.restype = ctypes.c_int
         L.orc_global_average_f64.argtypes = [i32, i64, P]
         L.orc_global_average_f64.restype = ctypes.c_int
+        L.orc_consensus.argtypes = [i32, i64, P, P]
+        L.orc_consensus.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -244,3 +246,11 @@ def global_average(x):
           np.dtype(np.float64): lib().orc_global_average_f64}[x.dtype]
     _check(fn(x.shape[0], x.shape[1], _ptr(x)))
     return x
+
+
+def consensus(x):
+    """(sum of squared deviations from the worker mean, max abs deviation) of float32 x (n, L)."""
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.zeros(2, np.float64)
+    _check(lib().orc_consensus(x.shape[0], x.shape[1], _ptr(x), _ptr(out)))
+    return float(out[0]), float(out[1])

@@ -438,3 +438,25 @@ int orc_global_average_f64(int32_t n, int64_t L, double *x) {
   }
   return ORC_OK;
 }
+
+/* ---- NEXT-4: consistency of the workers' parameters (Fig. 7b's question) ----
+ * out[0] = sum_i sum_e (x_i[e] - xbar[e])^2   (xbar = mean over the n workers, binary64)
+ * out[1] = max_i max_e |x_i[e] - xbar[e]|
+ * the consensus distance of decentralised SGD is out[0] / n. */
+int orc_consensus(int32_t n, int64_t L, const float *x, double out[2]) {
+  if (n < 1 || L < 0 || !out || (L > 0 && !x)) return ORC_EINVAL;
+  double ss = 0.0, mx = 0.0;
+  for (int64_t e = 0; e < L; ++e) {
+    double mean = 0.0;
+    for (int32_t i = 0; i < n; ++i) mean += (double)x[(size_t)i * (size_t)L + (size_t)e];
+    mean /= (double)n;
+    for (int32_t i = 0; i < n; ++i) {
+      double d = (double)x[(size_t)i * (size_t)L + (size_t)e] - mean;
+      ss += d * d;
+      if (fabs(d) > mx) mx = fabs(d);
+    }
+  }
+  out[0] = ss;
+  out[1] = mx;
+  return ORC_OK;
+}

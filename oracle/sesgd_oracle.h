@@ -102,6 +102,10 @@ int orc_groups_stone(int64_t t, int32_t n, int32_t m, int32_t *canon, int32_t *g
 int orc_global_average_f32(int32_t n, int64_t L, float *x);
 int orc_global_average_f64(int32_t n, int64_t L, double *x);
 
+/* Consistency of the n workers' parameters x [n*L]: out[0] = sum over workers and
+ * elements of (x_i - xbar)^2, out[1] = max |x_i - xbar|, in binary64 (xbar = worker mean). */
+int orc_consensus(int32_t n, int64_t L, const float *x, double out[2]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,8 @@ struct AverageArgs {
   int64_t numel;
 };
 cudaError_t launch_average(const AverageArgs &a, bool vec, int sm_count, cudaStream_t stream);
+// K9: consistency metric (rows only; outs unused): out[0] += sum (x - mean)^2, out[1] = max |x - mean|
+cudaError_t launch_consensus(const AverageArgs &a, double *out, int sm_count, cudaStream_t stream);
 int resident_occupancy(int mode, bool vec, int m, int unroll);
 
 // K3: one-shot push over NVLink, SM-specialised (COMM CTAs + COMPUTE CTAs), see p2p.cu.

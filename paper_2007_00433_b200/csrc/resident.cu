@@ -286,6 +286,45 @@ __global__ void __launch_bounds__(kThreads) k8_average(const __grid_constant__ A
   }
 }
 
+// K9: consistency of the workers' parameters: per element, the binary64 mean of
+// the n rows, then out[0] += sum (x_i - mean)^2 and out[1] = max(out[1], |x_i - mean|) over the
+// launch (warp-shuffle + shared-memory block reduction, one double atomic per CTA; the max via
+// the order-preserving bit pattern of non-negative doubles).
+__global__ void __launch_bounds__(kThreads) k9_consensus(const __grid_constant__ AverageArgs a,
+                                                         double *out) {
+  double ss = 0.0, mx = 0.0;
+  for (int64_t e = int64_t(blockIdx.x) * kThreads + threadIdx.x; e < a.numel;
+       e += int64_t(gridDim.x) * kThreads) {
+    double mean = 0.0;
+    for (int i = 0; i < a.nrows; ++i) mean += double(__ldcs(a.rows[i] + e));
+    mean /= double(a.nrows);
+    for (int i = 0; i < a.nrows; ++i) {
+      const double d = double(__ldcs(a.rows[i] + e)) - mean;
+      ss += d * d;
+      mx = fmax(mx, fabs(d));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double s_ss[kThreads / 32], s_mx[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    s_ss[threadIdx.x >> 5] = ss;
+    s_mx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kThreads / 32; ++w) {
+      ss += s_ss[w];
+      mx = fmax(mx, s_mx[w]);
+    }
+    atomicAdd(out, ss);
+    atomicMax(reinterpret_cast<unsigned long long *>(out + 1),
+              static_cast<unsigned long long>(__double_as_longlong(mx)));
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_average(const AverageArgs &a, bool vec, int sm_count, cudaStream_t stream) {
@@ -296,6 +335,13 @@ cudaError_t launch_average(const AverageArgs &a, bool vec, int sm_count, cudaStr
   const void *k = vec ? reinterpret_cast<const void *>(&k8_average<4>)
                       : reinterpret_cast<const void *>(&k8_average<1>);
   return cudaLaunchKernel(k, dim3(unsigned(blocks)), dim3(kThreads), args, 0, stream);
+}
+
+cudaError_t launch_consensus(const AverageArgs &a, double *out, int sm_count, cudaStream_t stream) {
+  int64_t blocks = (a.numel + kThreads - 1) / kThreads;
+  blocks = blocks < 1 ? 1 : (blocks > int64_t(sm_count) * 4 ? int64_t(sm_count) * 4 : blocks);
+  k9_consensus<<<unsigned(blocks), kThreads, 0, stream>>>(a, out);
+  return cudaGetLastError();
 }
 
 int resident_block_threads() { return kThreads; }

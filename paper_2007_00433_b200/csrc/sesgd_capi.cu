@@ -965,6 +965,33 @@ int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *const *row
   return SESGD_OK;
 }
 
+int sesgd_consensus(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,
+                    double *out_dev, void *stream) {
+  if (!ctx || !out_dev) return SESGD_EINVAL;
+  if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
+  if (bucket < 0 || size_t(bucket) >= ctx->buckets.size() || !ctx->buckets[bucket].registered)
+    return fail(ctx, SESGD_EINVAL, "bucket not registered");
+  if (nrows != ctx->n) return fail(ctx, SESGD_EINVAL, "nrows must equal n (every worker's parameters)");
+  sesgd_bucket &b = ctx->buckets[bucket];
+  if (b.numel == 0) return SESGD_OK;
+  sesgd::AverageArgs a{};
+  for (int i = 0; i < ctx->n; ++i) {
+    if (rows) {
+      if (!rows[i]) return fail(ctx, SESGD_EINVAL, "null row pointer");
+      a.rows[i] = rows[i];
+    } else {
+      if (ctx->n_local != ctx->n)
+        return fail(ctx, SESGD_EINVAL, "rows may be NULL only when every worker is local");
+      a.rows[i] = b.hx[ctx->slot_of[i]];
+    }
+  }
+  a.nrows = ctx->n;
+  a.numel = b.numel;
+  cudaError_t e = sesgd::launch_consensus(a, out_dev, ctx->sm_count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch consensus");
+  return SESGD_OK;
+}
+
 int sesgd_sync_step_host(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum,
                          const float *const *g_host, float *const *x_host_out, void *stream) {
   if (!ctx) return SESGD_EINVAL;

@@ -167,6 +167,27 @@ class SESGDEngine:
                 C.sesgd_global_average(self.ctx, b, self.n, ptrs, s.cuda_stream)
         self._gathered = gathered  # alive until the next call (the kernels read it on s)
 
+    def _gathered_rows(self, stream):
+        """every rank's parameters, all-gathered (data movement only): [n, total] on this GPU"""
+        import torch.distributed as dist
+        with torch.cuda.stream(stream):
+            local = torch.stack(self.x_flat)  # [r, total]
+            gathered = torch.empty((self.world,) + tuple(local.shape), dtype=local.dtype, device=self.device)
+            dist.all_gather_into_tensor(gathered, local, group=self.group)
+        return gathered.view(self.n, -1)  # worker w = rank w // r, slot w % r: ascending id
+
+    def consensus(self, stream: Optional[torch.cuda.Stream] = None):
+        """Consistency of the workers' parameters (K9): (sum over workers and elements of
+        (x_i - xbar)^2, max |x_i - xbar|), binary64."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        out = torch.zeros(2, dtype=torch.float64, device=self.device)
+        rows = None if self.world == 1 else self._gathered_rows(s)
+        for b in range(len(self.bucket_sizes)):
+            ptrs = None if rows is None else [rows[w].data_ptr() + 4 * self.offsets[b] for w in range(self.n)]
+            C.sesgd_consensus(self.ctx, b, self.n, out.data_ptr(), ptrs, s.cuda_stream)
+        s.synchronize()
+        return float(out[0]), float(out[1])
+
     def groups(self, t: int):
         return C.sesgd_groups(self.ctx, t, self.n)
 

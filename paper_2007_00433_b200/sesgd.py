@@ -32,7 +32,7 @@ EXPORTED = (
     "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
-    "sesgd_global_average", "sesgd_sync_all_host",
+    "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus",
 )
 
 
@@ -81,6 +81,7 @@ def lib():
             "sesgd_sync_all": ([P, f32, f32, P], ctypes.c_int),
             "sesgd_global_average": ([P, i32, P, i32, P], ctypes.c_int),
             "sesgd_sync_all_host": ([P, f32, f32, P, P, P], ctypes.c_int),
+            "sesgd_consensus": ([P, i32, P, i32, P, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -188,6 +189,13 @@ def sesgd_sync_all_host(ctx, lr: float, momentum: float, g_host_ptrs, x_host_ptr
     """g_host_ptrs / x_host_ptrs: flat [bucket * n_local + slot] host pointers."""
     _check(lib().sesgd_sync_all_host(ctx, lr, momentum, _ptr_array(g_host_ptrs),
                                      _ptr_array(x_host_ptrs), ctypes.c_void_p(int(stream))), ctx)
+
+
+def sesgd_consensus(ctx, bucket: int, n: int, out_dev_ptr: int, row_ptrs=None, stream: int = 0) -> None:
+    """Accumulates (sum of squared deviations, max abs deviation) into 2 device doubles."""
+    rows = _ptr_array(row_ptrs) if row_ptrs is not None else None
+    _check(lib().sesgd_consensus(ctx, bucket, rows, n, ctypes.c_void_p(int(out_dev_ptr)),
+                                 ctypes.c_void_p(int(stream))), ctx)
 
 
 def sesgd_global_average(ctx, bucket: int, n: int, row_ptrs=None, stream: int = 0) -> None:

@@ -35,6 +35,7 @@ def main():
     p.add_argument("--period", type=int, default=1)
     p.add_argument("--final-avg", type=int, default=0)
     p.add_argument("--schedule", type=int, default=0)
+    p.add_argument("--consensus", type=int, default=0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -67,8 +68,9 @@ def main():
     X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
     V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
     stats = eng.stats(0)
+    cons = np.array(eng.consensus() if a.consensus else (0.0, 0.0))
     np.savez(f"{a.out}.rank{rank}.npz", X=X, V=V, workers=np.array(eng.local_workers),
-             flag_messages=stats["flag_messages"], payload=stats["payload_bytes_in"])
+             flag_messages=stats["flag_messages"], payload=stats["payload_bytes_in"], cons=cons)
     dist.barrier()
     eng.close()
     dist.destroy_process_group()

@@ -29,7 +29,7 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0):
+            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -41,7 +41,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
-               "--schedule", str(schedule),
+               "--schedule", str(schedule), "--consensus", str(consensus),
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -292,3 +292,15 @@ def test_dimension_exchange_schedule_multigpu(tmp_path, gpus, n, m):
                      schedule=oracle.SCHED_STONE)
     _compare(X, x)
     _compare(V, v)
+
+
+def test_two_gpus_consensus_metric(tmp_path):
+    """NEXT-4 across GPUs: all-gathered rows + K9 on every rank equal the oracle's metric."""
+    buckets = [65537, 3]
+    n, m, T = 4, 2, 6
+    _launch(tmp_path, 2, n, m, T, buckets, consensus=1)
+    x, _ = _oracle(n, m, sum(buckets), T, 0)
+    oss, omx = oracle.consensus(x)
+    for r in range(2):
+        ss, mx = np.load(str(tmp_path / "res") + f".rank{r}.npz")["cons"]
+        assert abs(ss - oss) <= 1e-9 * oss and abs(mx - omx) <= 1e-12 * omx

@@ -286,3 +286,31 @@ def test_host_buffer_path(pipelined):
     eng.close()
     x, _ = _run_oracle(n, m, sum(buckets), T, oracle.MODE_PARAM)
     _compare(X, x)
+
+
+def test_consensus_metric():
+    """NEXT-4: the device consistency metric (K9, binary64) equals the oracle's on the state after
+    10 SESGD iterations, and is exactly 0 right after the final global average."""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200.workloads import CONFIG1_BUCKETS
+    n, m, T = 8, 2, 10
+    buckets = list(CONFIG1_BUCKETS)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    eng = SESGDEngine(n, m, buckets)
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(n):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), st)
+    for t in range(T):
+        for s in range(n):
+            for b, Lb in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), s, t, st)
+        eng.step(t, LR, MU)
+    ss, mx = eng.consensus()
+    x, _ = _run_oracle(n, m, sum(buckets), T, oracle.MODE_PARAM)
+    oss, omx = oracle.consensus(x)
+    assert ss > 0 and abs(ss - oss) <= 1e-9 * oss
+    assert abs(mx - omx) <= 1e-12 * omx
+    eng.global_average()
+    assert eng.consensus() == (0.0, 0.0)
+    eng.close()

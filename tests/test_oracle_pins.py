@@ -668,3 +668,32 @@ def test_stone_schedule_errors_and_run():
         canon, _ = oracle.groups_stone(t, n, m)
         oracle.step(n, m, canon, y, w, _grads(n, t, L, np.float32), 0.1, 0.9)
     assert np.array_equal(x, y) and np.array_equal(v, w)
+
+
+# ---------------------------------------------------------------- NEXT-4: consistency metric
+def test_consensus_metric_definition():
+    """Zero for identical workers; [0], [2] -> 2 and 1; equals the pairwise form
+    (1/(2n)) sum_{i,j} ||x_i - x_j||^2 (brute force, exact fractions on dyadic data)."""
+    assert oracle.consensus(np.tile(np.float32([1.5, -2.0]), (4, 1))) == (0.0, 0.0)
+    assert oracle.consensus(np.array([[0.0], [2.0]], np.float32)) == (2.0, 1.0)
+    from fractions import Fraction
+    rng = np.random.default_rng(9)
+    x = (rng.integers(-64, 64, size=(6, 11)) / 8).astype(np.float32)
+    n = x.shape[0]
+    pair = sum(Fraction(float(x[i, e]) - float(x[j, e])) ** 2
+               for i in range(n) for j in range(n) for e in range(x.shape[1])) / (2 * n)
+    ss, mx = oracle.consensus(x)
+    assert abs(ss - float(pair)) <= 1e-12 * float(pair)
+    assert mx == float(np.abs(x.astype(np.float64) - x.astype(np.float64).mean(0)).max())
+
+
+def test_consensus_group_average_contracts_and_matches_paper_claim():
+    """P:432-433 ("parameters of each worker maintain highly consistent"): under SESGD the
+    consensus distance stays small relative to independent SGD (m = 1), and an exchange with
+    m = n makes it exactly 0."""
+    n, L, T = 8, 500, 20
+    xs, _ = _run_local(n, 2, T, L, 1)
+    xi, _ = _run_local(n, 1, T, L, 1)
+    xr, _ = _run_local(n, n, T, L, 1)
+    assert oracle.consensus(xs)[0] < 0.2 * oracle.consensus(xi)[0]
+    assert oracle.consensus(xr) == (0.0, 0.0)
