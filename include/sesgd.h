@@ -258,6 +258,14 @@ SESGD_API int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *
 SESGD_API int sesgd_consensus(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,
                               double *out_dev, void *stream);
 
+/* Weight decay folded into every update (the paper trains with 5e-4 / 1e-4; R20): the
+ * gradient term of the momentum step becomes d = g (+) wd (x) x, as torch.optim.SGD's
+ * weight_decay -- PARAM: v <- mu v + (g + wd x) before the local step; GRAD: v <- mu v +
+ * (gbar + wd x) with the worker's own x after the group mean.  Default 0 (bit-identical to no
+ * decay).  Applies to the following sesgd_sync_step / sync_all calls.  Errors: SESGD_EINVAL
+ * (negative or not finite). */
+SESGD_API int sesgd_set_weight_decay(sesgd_ctx *ctx, float weight_decay);
+
 /* Non-blocking check of the latched device error word: SESGD_OK or SESGD_ETIMEOUT. */
 SESGD_API int sesgd_poll(sesgd_ctx *ctx);
 

@@ -78,7 +78,10 @@ def lib():
                                        ctypes.c_float, i32, P, P]
         L.orc_run_ring_f32.restype = ctypes.c_int
         L.orc_run_local_f32.argtypes = [i32, i32, u64, i64, i64, i64, P, u64, ctypes.c_float,
-                                        ctypes.c_float, i32, i64, i32, P, P]
+                                        ctypes.c_float, i32, i64, i32, ctypes.c_float, P, P]
+        L.orc_step_wd_f32.argtypes = [i32, i32, P, i64, P, P, P, ctypes.c_float, ctypes.c_float,
+                                      ctypes.c_float, i32]
+        L.orc_step_wd_f32.restype = ctypes.c_int
         L.orc_groups_stone.argtypes = [i64, i32, i32, P, P]
         L.orc_groups_stone.restype = ctypes.c_int
         L.orc_run_local_f32.restype = ctypes.c_int
@@ -168,6 +171,15 @@ def step(n, m, canon, x, v, g, lr, mu, mode=MODE_PARAM):
         raise TypeError(x.dtype)
 
 
+def step_wd(n, m, canon, x, v, g, lr, mu, wd, mode=MODE_PARAM):
+    """One binary32 iteration with weight decay (float32 arrays, in place)."""
+    canon = np.ascontiguousarray(canon, np.int32)
+    g = np.ascontiguousarray(g, np.float32)
+    assert x.dtype == np.float32 and x.flags.c_contiguous and v.flags.c_contiguous
+    _check(lib().orc_step_wd_f32(n, m, _ptr(canon), x.shape[-1], _ptr(x), _ptr(v), _ptr(g),
+                                 float(lr), float(mu), float(wd), mode))
+
+
 def slice_of(L: int, m: int, e: int) -> int:
     return int(lib().orc_slice_of(L, m, e))
 
@@ -222,7 +234,7 @@ def groups_stone(t: int, n: int, m: int):
 
 
 def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0, coords=None,
-              schedule=SCHED_RANDOM):
+              schedule=SCHED_RANDOM, weight_decay=0.0):
     """Local-SESGD: T iterations where the group exchange fires only when
     (t + 1) % period == 0; float32 x, v (n, S) in place.  period = 1 is `run`; m = n is
     Local-SGD."""
@@ -234,7 +246,7 @@ def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0
         cp = _ptr(coords)
     assert x.dtype == np.float32 and x.flags.c_contiguous and v.flags.c_contiguous
     _check(lib().orc_run_local_f32(n, m, seed, t0, T, S, cp, s_g, float(lr), float(mu), mode,
-                                   int(period), int(schedule), _ptr(x), _ptr(v)))
+                                   int(period), int(schedule), float(weight_decay), _ptr(x), _ptr(v)))
     return x, v
 
 

@@ -156,6 +156,14 @@ int orc_latency(int32_t n, int32_t m, double bytes, double nu, double tau, doubl
 /* ---- A2/A5 (Eq. 6) and Eq. 5 variant: one iteration, binary32 ---- */
 int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
                  const float *g, float lr, float mu, int32_t mode) {
+  return orc_step_wd_f32(n, m, canon, L, x, v, g, lr, mu, 0.0f, mode);
+}
+
+/* as orc_step_f32, with torch.optim.SGD's weight decay on the gradient term (R20):
+ * d = g + wd * x (skipped when wd == 0), then v = mu v + d; GRAD mode decays the group mean
+ * with the worker's own x */
+int orc_step_wd_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                    const float *g, float lr, float mu, float wd, int32_t mode) {
   if (n < 1 || m < 1 || m > n || L < 0 || !canon) return ORC_EINVAL;
   if (n % m != 0) return ORC_ENOTDIV;
   int32_t k = n / m;
@@ -166,8 +174,10 @@ int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x
     for (int32_t i = 0; i < n; ++i) {
       for (int64_t e = 0; e < L; ++e) {
         size_t at = (size_t)i * (size_t)L + (size_t)e;
+        float d = g[at];
+        if (wd != 0.0f) d = d + wd * x[at];
         float mv = mu * v[at];
-        float vn = mv + g[at];
+        float vn = mv + d;
         float step = lr * vn;
         v[at] = vn;
         xh[at] = x[at] - step;
@@ -195,8 +205,10 @@ int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x
         float gb = s / fm;
         for (int32_t r = 0; r < m; ++r) {
           size_t at = (size_t)G[r] * (size_t)L + (size_t)e;
+          float d = gb;
+          if (wd != 0.0f) d = d + wd * x[at];
           float mv = mu * v[at];
-          float vn = mv + gb;
+          float vn = mv + d;
           float step = lr * vn;
           v[at] = vn;
           x[at] = x[at] - step;
@@ -389,7 +401,7 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
 /* ---- Local-SESGD: exchange only when (t + 1) mod H == 0 ---- */
 int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                       const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
-                      int64_t H, int32_t schedule, float *x, float *v) {
+                      int64_t H, int32_t schedule, float wd, float *x, float *v) {
   if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || S < 0 || H < 1) return ORC_EINVAL;
   if (schedule != 0 && schedule != 1) return ORC_EINVAL;
   if (n % m != 0) return ORC_ENOTDIV;
@@ -405,10 +417,10 @@ int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T
     if ((t + 1) % H == 0) { /* synchronisation iteration: SESGD step with the groups of t */
       rc = schedule == 1 ? orc_groups_stone(t, n, m, canon, NULL)
                          : orc_groups(seed, t, n, m, NULL, canon, NULL);
-      if (rc == ORC_OK) rc = orc_step_f32(n, m, canon, S, x, v, g, lr, mu, mode);
+      if (rc == ORC_OK) rc = orc_step_wd_f32(n, m, canon, S, x, v, g, lr, mu, wd, mode);
     } else { /* local iteration: every worker its own singleton group */
       for (int32_t i = 0; i < n; ++i) canon[i] = i;
-      rc = orc_step_f32(n, 1, canon, S, x, v, g, lr, mu, mode);
+      rc = orc_step_wd_f32(n, 1, canon, S, x, v, g, lr, mu, wd, mode);
     }
   }
   free(g);

@@ -57,6 +57,11 @@ int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x
                  const float *g, float lr, float mu, int32_t mode);
 int orc_step_f64(int32_t n, int32_t m, const int32_t *canon, int64_t L, double *x, double *v,
                  const double *g, double lr, double mu, int32_t mode);
+/* The same binary32 iteration with torch.optim.SGD's weight decay (R20): the momentum
+ * step's gradient term is d = g + wd * x (not applied when wd == 0); GRAD mode: d = gbar + wd * x
+ * with the worker's own x. */
+int orc_step_wd_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                    const float *g, float lr, float mu, float wd, int32_t mode);
 
 /* The same iteration with the group mean computed by the paper's Ring-AllReduce (Sec. 2.2,
  * P:99-104) in ring order: members in ascending id form the ring; element e lies in slice
@@ -86,10 +91,10 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
  * other iterations the locally updated parameters are kept (the iteration with m = 1:
  * PARAM x = xh, GRAD v = mu v + g, x = x - lr v).  H = 1 is SESGD; m = n is Local-SGD
  * (the paper's baseline with period 2).  schedule: 0 = orc_groups (R1),
- * 1 = orc_groups_stone (NEXT-3). */
+ * 1 = orc_groups_stone (NEXT-3).  wd: weight decay as orc_step_wd_f32. */
 int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                       const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
-                      int64_t H, int32_t schedule, float *x, float *v);
+                      int64_t H, int32_t schedule, float wd, float *x, float *v);
 
 /* NEXT-3, alternative reading of R1 (Stone's perfect shuffle): n = 2^d, m = 2^p; at
  * iteration t worker i's group is every worker equal to i outside index dimensions

@@ -11,6 +11,11 @@ namespace dev {
 __device__ __forceinline__ float momentum(float mu, float v, float g) {
   return __fadd_rn(__fmul_rn(mu, v), g);  // v <- mu (x) v (+) g        (R8)
 }
+// weight decay on the gradient term before momentum, as torch.optim.SGD (R20):
+// d = g (+) wd (x) x; wd == 0 returns g unchanged (keeps the sign of a -0 gradient)
+__device__ __forceinline__ float decay(float g, float wd, float x) {
+  return wd == 0.f ? g : __fadd_rn(g, __fmul_rn(wd, x));
+}
 __device__ __forceinline__ float sgd(float x, float lr, float v) {
   return __fsub_rn(x, __fmul_rn(lr, v));  // x <- x (-) lr (x) v        (Alg.1 line 7)
 }

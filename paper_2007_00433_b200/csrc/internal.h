@@ -32,6 +32,7 @@ struct ResidentArgs {
   const float *const *g;  // [n_local]
   int64_t numel;
   float lr, mu;
+  float wd;               // weight decay (sesgd_set_weight_decay)
   int m;                  // group size
   int k;                  // groups
   int nb;                 // 0: one bucket (x, v, g, numel); > 0: all buckets via the tables
@@ -84,7 +85,7 @@ struct P2PArgs {
   unsigned long long *err_host;     // mapped host block: [code, kind, cta, seen, target, worker, pos, rank]
   unsigned int *abort_dev;          // device word: set on timeout, skips further waits
   uint64_t *prof;                   // optional per-CTA phase timers [grid][8] (SESGD_OPT_PROFILE)
-  float lr, mu;
+  float lr, mu, wd;
   int n, m, r, grid;
   int comm_ctas, comm_batch;        // COMM CTAs (blockIdx < comm_ctas) and chunks per release
   int lag;                          // COMPUTE folds chunk step k - lag after staging step k
@@ -117,7 +118,7 @@ struct RingArgs {
   uint64_t timeout_ns, hop_delay_ns;
   unsigned long long *err_host;
   unsigned int *abort_dev;
-  float lr, mu;
+  float lr, mu, wd;
   int parity, steps, m, pos, grid, my_rank, bucket, nbuckets;
   int8_t ring_rank[SESGD_MAX_WORKERS];  // rank of ring position 0..m-1 (ascending worker id)
 };
@@ -177,6 +178,7 @@ struct sesgd_ctx {
   int release_stagger = 1;  // SESGD_OPT_RELEASE_STAGGER
   int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
+  float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_k, ev_out;

@@ -262,7 +262,7 @@ struct Split {
           load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
             x[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
           }
           store_m<W>(vs + e, v, nv);
@@ -321,7 +321,7 @@ struct Split {
           load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], acc[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(acc[q], a.wd, x[q]));
             x[q] = dev::sgd(x[q], a.lr, v[q]);
           }
           store_m<W>(vs + e, v, nv);
@@ -609,7 +609,7 @@ struct Split {
           load_m<W>(a.bx[c.b * a.r + sl] + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
             const float xh = dev::sgd(x[q], a.lr, v[q]);
             acc[q] = (rr == 0) ? xh : __fadd_rn(acc[q], xh);
           }
@@ -631,7 +631,7 @@ struct Split {
           load_m<W>(a.bx[c.b * a.r + sl] + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], acc[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(acc[q], a.wd, x[q]));
             x[q] = dev::sgd(x[q], a.lr, v[q]);
           }
           store_m<W>(a.bv[c.b * a.r + sl] + e, v, nv);
@@ -668,7 +668,7 @@ struct Split {
           load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
             val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
           }
           store_m<W>(vs + e, v, nv);
@@ -727,7 +727,7 @@ struct Split {
           load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], acc[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(acc[q], a.wd, x[q]));
             x[q] = dev::sgd(x[q], a.lr, v[q]);
           }
           store_m<W>(vs + e, v, nv);
@@ -910,7 +910,7 @@ struct Split {
           load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
             val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
           }
           store_m<W>(vs + e, v, nv);
@@ -1025,7 +1025,7 @@ struct Split {
             load_m<W>(xw, x, nv);
 #pragma unroll
             for (int q = 0; q < W; ++q) {
-              v[q] = dev::momentum(a.mu, v[q], acc[q]);
+              v[q] = dev::momentum(a.mu, v[q], dev::decay(acc[q], a.wd, x[q]));
               x[q] = dev::sgd(x[q], a.lr, v[q]);
             }
             store_m<W>(vw, v, nv);
@@ -1085,7 +1085,7 @@ struct Split {
             load_m<W>(xs + e, x, nv);
 #pragma unroll
             for (int q = 0; q < W; ++q) {
-              v[q] = dev::momentum(a.mu, v[q], y[q]);
+              v[q] = dev::momentum(a.mu, v[q], dev::decay(y[q], a.wd, x[q]));
               x[q] = dev::sgd(x[q], a.lr, v[q]);
             }
             store_m<W>(vs + e, v, nv);
@@ -1219,7 +1219,7 @@ struct Split {
           load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], gr[q]);
+            v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
             x[q] = dev::sgd(x[q], a.lr, v[q]);
           }
           store_m<W>(vs + e, v, nv);

@@ -57,13 +57,13 @@ struct Item {
   }
 
   __device__ __forceinline__ void finish(float *const *xp, float *const *vp, int64_t e, float lr,
-                                         float mu) {
+                                         float mu, float wd) {
     if constexpr (!GRAD) {
 #pragma unroll
       for (int r = 0; r < M; ++r)
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          v[r][w] = dev::momentum(mu, v[r][w], g[r][w]);
+          v[r][w] = dev::momentum(mu, v[r][w], dev::decay(g[r][w], wd, x[r][w]));
           x[r][w] = dev::sgd(x[r][w], lr, v[r][w]);  // x_hat, stays in registers
         }
       float mean[W];
@@ -92,7 +92,7 @@ struct Item {
       for (int r = 0; r < M; ++r) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          v[r][w] = dev::momentum(mu, v[r][w], gb[w]);
+          v[r][w] = dev::momentum(mu, v[r][w], dev::decay(gb[w], wd, x[r][w]));
           x[r][w] = dev::sgd(x[r][w], lr, v[r][w]);
         }
         store<W>(vp[r] + e, v[r]);
@@ -116,7 +116,7 @@ __device__ __forceinline__ void item_generic(const ResidentArgs &a, const int8_t
       load<W>(a.x[sl] + e, x);
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        v[w] = dev::momentum(a.mu, v[w], g[w]);
+        v[w] = dev::momentum(a.mu, v[w], dev::decay(g[w], a.wd, x[w]));
         x[w] = dev::sgd(x[w], a.lr, v[w]);
         s[w] = (r == 0) ? x[w] : __fadd_rn(s[w], x[w]);
       }
@@ -141,7 +141,7 @@ __device__ __forceinline__ void item_generic(const ResidentArgs &a, const int8_t
       load<W>(a.x[sl] + e, x);
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        v[w] = dev::momentum(a.mu, v[w], s[w]);
+        v[w] = dev::momentum(a.mu, v[w], dev::decay(s[w], a.wd, x[w]));
         x[w] = dev::sgd(x[w], a.lr, v[w]);
       }
       store<W>(a.v[sl] + e, v);
@@ -158,7 +158,7 @@ struct Unroll {
 };
 
 // One bucket for the group `mem` of this CTA row: grid-stride over W-wide items.
-template <int M, int W, bool GRAD, int U>
+template <int M, int W, bool GRAD, int U, bool WD>
 __device__ __forceinline__ void resident_bucket(const ResidentArgs &a, const int8_t *mem, int m,
                                                 float *const *tx, float *const *tv,
                                                 const float *const *tg, int64_t numel) {
@@ -180,12 +180,12 @@ __device__ __forceinline__ void resident_bucket(const ResidentArgs &a, const int
 #pragma unroll
       for (int u = 0; u < U; ++u) it[u].fetch(xp, vp, gp, (i + u * stride) * W);
 #pragma unroll
-      for (int u = 0; u < U; ++u) it[u].finish(xp, vp, (i + u * stride) * W, a.lr, a.mu);
+      for (int u = 0; u < U; ++u) it[u].finish(xp, vp, (i + u * stride) * W, a.lr, a.mu, WD ? a.wd : 0.f);
     }
     for (; i < nfull; i += stride) {
       Item<M, W, GRAD> it;
       it.fetch(xp, vp, gp, i * W);
-      it.finish(xp, vp, i * W, a.lr, a.mu);
+      it.finish(xp, vp, i * W, a.lr, a.mu, WD ? a.wd : 0.f);
     }
   } else {
     ResidentArgs b = a;  // runtime-m path reads the member tables through the args
@@ -210,47 +210,49 @@ __device__ __forceinline__ void resident_bucket(const ResidentArgs &a, const int
 // a.nb == 0: one bucket (a.x / a.v / a.g, a.numel).  a.nb > 0: every bucket of the iteration
 // in one launch (tables bx/bv/bg[b * n_local + slot], numels[b]); elements are independent, so
 // CTAs flow from one bucket into the next without any barrier (one launch tail per iteration).
-template <int M, int W, bool GRAD, int U>
+// WD: weight decay compiled in (a.wd != 0); the WD = false kernels are the decay-free ones
+template <int M, int W, bool GRAD, int U, bool WD>
 __global__ void __launch_bounds__(kThreads) k6_resident(const __grid_constant__ ResidentArgs a) {
   const int m = M > 0 ? M : a.m;
   const int8_t *mem = a.member_slot + blockIdx.y * m;
   if (a.nb == 0) {
-    resident_bucket<M, W, GRAD, U>(a, mem, m, a.x, a.v, a.g, a.numel);
+    resident_bucket<M, W, GRAD, U, WD>(a, mem, m, a.x, a.v, a.g, a.numel);
   } else {
     for (int b = 0; b < a.nb; ++b)
-      resident_bucket<M, W, GRAD, U>(a, mem, m, a.bx + int64_t(b) * a.n_local,
+      resident_bucket<M, W, GRAD, U, WD>(a, mem, m, a.bx + int64_t(b) * a.n_local,
                                      a.bv + int64_t(b) * a.n_local, a.bg + int64_t(b) * a.n_local,
                                      a.numels[b]);
   }
 }
 
 template <int M, int W, bool GRAD, int U>
-const void *kernel_ptr() {
-  return reinterpret_cast<const void *>(&k6_resident<M, W, GRAD, U>);
+const void *kernel_ptr(bool wd) {
+  return wd ? reinterpret_cast<const void *>(&k6_resident<M, W, GRAD, U, true>)
+            : reinterpret_cast<const void *>(&k6_resident<M, W, GRAD, U, false>);
 }
 
 // unroll 0 = default per M; 1 / 2 / 4 selectable for M = 2 (SESGD_OPT_RESIDENT_UNROLL)
 template <int W, bool GRAD>
-const void *pick_m(int m, int unroll) {
+const void *pick_m(int m, int unroll, bool wd) {
   switch (m) {
-    case 1: return kernel_ptr<1, W, GRAD, Unroll<1>::value>();
+    case 1: return kernel_ptr<1, W, GRAD, Unroll<1>::value>(wd);
     case 2:
       switch (unroll) {
-        case 4: return kernel_ptr<2, W, GRAD, 4>();
-        case 2: return kernel_ptr<2, W, GRAD, 2>();
-        case 8: return kernel_ptr<2, W, GRAD, 8>();
-        default: return kernel_ptr<2, W, GRAD, Unroll<2>::value>();
+        case 4: return kernel_ptr<2, W, GRAD, 4>(wd);
+        case 2: return kernel_ptr<2, W, GRAD, 2>(wd);
+        case 8: return kernel_ptr<2, W, GRAD, 8>(wd);
+        default: return kernel_ptr<2, W, GRAD, Unroll<2>::value>(wd);
       }
-    case 4: return kernel_ptr<4, W, GRAD, Unroll<4>::value>();
-    case 8: return kernel_ptr<8, W, GRAD, Unroll<8>::value>();
-    default: return kernel_ptr<0, W, GRAD, Unroll<0>::value>();
+    case 4: return kernel_ptr<4, W, GRAD, Unroll<4>::value>(wd);
+    case 8: return kernel_ptr<8, W, GRAD, Unroll<8>::value>(wd);
+    default: return kernel_ptr<0, W, GRAD, Unroll<0>::value>(wd);
   }
 }
 
-const void *pick(int mode, bool vec, int m, int unroll) {
+const void *pick(int mode, bool vec, int m, int unroll, bool wd) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
-  if (vec) return grad ? pick_m<4, true>(m, unroll) : pick_m<4, false>(m, unroll);
-  return grad ? pick_m<1, true>(m, unroll) : pick_m<1, false>(m, unroll);
+  if (vec) return grad ? pick_m<4, true>(m, unroll, wd) : pick_m<4, false>(m, unroll, wd);
+  return grad ? pick_m<1, true>(m, unroll, wd) : pick_m<1, false>(m, unroll, wd);
 }
 
 // K8: Algorithm 1's last line, xbar = Ring-AllReduce(x_i; Global): per element, the
@@ -348,7 +350,7 @@ int resident_block_threads() { return kThreads; }
 
 int resident_occupancy(int mode, bool vec, int m, int unroll) {
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode, vec, m, unroll), kThreads,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode, vec, m, unroll, false), kThreads,
                                                     0) != cudaSuccess)
     return 1;
   return blocks > 0 ? blocks : 1;
@@ -358,7 +360,7 @@ cudaError_t launch_resident(const ResidentArgs &a, int mode, bool vec, int grid_
                             cudaStream_t stream) {
   dim3 grid(grid_x, a.k), block(kThreads);
   void *args[] = {const_cast<ResidentArgs *>(&a)};
-  return cudaLaunchKernel(pick(mode, vec, a.m, unroll), grid, block, args, 0, stream);
+  return cudaLaunchKernel(pick(mode, vec, a.m, unroll, a.wd != 0.f), grid, block, args, 0, stream);
 }
 
 }  // namespace sesgd

@@ -81,7 +81,7 @@ struct Ring {
     for (int64_t e = lo + threadIdx.x; e < hi; e += kRingThreads) {
       const float g = __ldcs(a.g + e);
       if constexpr (!GRAD) {
-        const float v = dev::momentum(a.mu, a.v[e], g);
+        const float v = dev::momentum(a.mu, a.v[e], dev::decay(g, a.wd, a.x[e]));
         a.v[e] = v;
         f(e, dev::sgd(a.x[e], a.lr, v));
       } else {
@@ -96,7 +96,7 @@ struct Ring {
       if constexpr (!GRAD) {
         a.x[e] = mean;
       } else {
-        const float v = dev::momentum(a.mu, a.v[e], mean);
+        const float v = dev::momentum(a.mu, a.v[e], dev::decay(mean, a.wd, a.x[e]));
         a.v[e] = v;
         a.x[e] = dev::sgd(a.x[e], a.lr, v);
       }
@@ -152,7 +152,7 @@ struct Ring {
       for (int64_t e = lo + threadIdx.x; e < hi; e += kRingThreads) {
         const float g = __ldcs(a.g + e);
         if constexpr (!GRAD) {
-          const float v = dev::momentum(a.mu, a.v[e], g);
+          const float v = dev::momentum(a.mu, a.v[e], dev::decay(g, a.wd, a.x[e]));
           a.v[e] = v;
           const float mean = __fdiv_rn(__fadd_rn(in[e - base], dev::sgd(a.x[e], a.lr, v)), float(m));
           out[e - base] = mean;
@@ -160,7 +160,7 @@ struct Ring {
         } else {
           const float mean = __fdiv_rn(__fadd_rn(in[e - base], g), float(m));
           out[e - base] = mean;
-          const float v = dev::momentum(a.mu, a.v[e], mean);
+          const float v = dev::momentum(a.mu, a.v[e], dev::decay(mean, a.wd, a.x[e]));
           a.v[e] = v;
           a.x[e] = dev::sgd(a.x[e], a.lr, v);
         }
@@ -188,7 +188,7 @@ struct Ring {
   __device__ void local_only() const {
     for (int64_t e = int64_t(blockIdx.x) * kRingThreads + threadIdx.x; e < a.numel;
          e += int64_t(a.grid) * kRingThreads) {
-      const float v = dev::momentum(a.mu, a.v[e], a.g[e]);
+      const float v = dev::momentum(a.mu, a.v[e], dev::decay(a.g[e], a.wd, a.x[e]));
       a.v[e] = v;
       a.x[e] = dev::sgd(a.x[e], a.lr, v);
     }

@@ -188,6 +188,7 @@ int local_step(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_
   ResidentArgs a{};
   a.lr = lr;
   a.mu = momentum;
+  a.wd = ctx->weight_decay;
   a.m = 1;
   a.k = ctx->n_local;
   a.n_local = ctx->n_local;
@@ -370,6 +371,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.prof = ctx->profile ? ctx->d_prof : nullptr;
   a.lr = lr;
   a.mu = momentum;
+  a.wd = ctx->weight_decay;
   a.n = ctx->n;
   a.m = ctx->m;
   a.r = ctx->n_local;
@@ -601,6 +603,14 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
   }
 }
 
+int sesgd_set_weight_decay(sesgd_ctx *ctx, float weight_decay) {
+  if (!ctx) return SESGD_EINVAL;
+  if (!std::isfinite(weight_decay) || weight_decay < 0.f)
+    return fail(ctx, SESGD_EINVAL, "weight decay must be finite and >= 0");
+  ctx->weight_decay = weight_decay;
+  return SESGD_OK;
+}
+
 int sesgd_attach(sesgd_ctx *ctx, int32_t device, int32_t n_local, const int32_t *local_workers) {
   if (!ctx) return SESGD_EINVAL;
   if (ctx->attached) return fail(ctx, SESGD_ESTATE, "already attached");
@@ -797,6 +807,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     a.numel = b.numel;
     a.lr = lr;
     a.mu = momentum;
+    a.wd = ctx->weight_decay;
     a.m = ctx->m;
     a.k = ctx->n / ctx->m;
     for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
@@ -829,6 +840,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     ra.abort_dev = ctx->d_abort;
     ra.lr = lr;
     ra.mu = momentum;
+    ra.wd = ctx->weight_decay;
     ra.parity = int(b.calls & 1);
     ra.steps = 2 * (ctx->m - 1);
     ra.m = ctx->m;
@@ -894,6 +906,7 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     }
     a.lr = lr;
     a.mu = momentum;
+    a.wd = ctx->weight_decay;
     a.m = ctx->m;
     a.k = ctx->n / ctx->m;
     a.nb = int(ctx->buckets.size());

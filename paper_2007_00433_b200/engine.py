@@ -30,7 +30,8 @@ class SESGDEngine:
                  device: Optional[int] = None, mode: int = C.MODE_PARAM_AVG,
                  rank: int = 0, world: int = 1, process_group=None, path: int = C.PATH_AUTO,
                  grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0,
-                 p2p_variant: int = -1, discard: int = 1, options: Optional[dict] = None):
+                 p2p_variant: int = -1, discard: int = 1, options: Optional[dict] = None,
+                 weight_decay: float = 0.0):
         if n % world != 0:
             raise ValueError("n must be a multiple of the number of ranks")
         self.n, self.m, self.seed = n, group_size, seed
@@ -52,6 +53,8 @@ class SESGDEngine:
         C.sesgd_set_option(self.ctx, C.OPT_DISCARD, discard)
         for opt, val in (options or {}).items():  # extra SESGD_OPT_* (before the layout freezes)
             C.sesgd_set_option(self.ctx, opt, val)
+        if weight_decay:
+            C.sesgd_set_weight_decay(self.ctx, weight_decay)
         C.sesgd_attach(self.ctx, self.device.index, self.local_workers)
 
         self.offsets, total = _aligned_offsets(self.bucket_sizes)

@@ -32,7 +32,7 @@ EXPORTED = (
     "sesgd_attach_peers", "sesgd_begin_iter", "sesgd_sync_step", "sesgd_sync_step_host",
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
-    "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus",
+    "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus", "sesgd_set_weight_decay",
 )
 
 
@@ -82,6 +82,7 @@ def lib():
             "sesgd_global_average": ([P, i32, P, i32, P], ctypes.c_int),
             "sesgd_sync_all_host": ([P, f32, f32, P, P, P], ctypes.c_int),
             "sesgd_consensus": ([P, i32, P, i32, P, P], ctypes.c_int),
+            "sesgd_set_weight_decay": ([P, f32], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -134,6 +135,10 @@ def sesgd_latency_model(n: int, group_size: int, nbytes: float, nu_Bps: float, t
     _check(lib().sesgd_latency_model(n, group_size, float(nbytes), float(nu_Bps), float(tau_s),
                                      ctypes.byref(out)))
     return {f: getattr(out, f) for f, _ in sesgd_cost._fields_}
+
+
+def sesgd_set_weight_decay(ctx, weight_decay: float) -> None:
+    _check(lib().sesgd_set_weight_decay(ctx, float(weight_decay)), ctx)
 
 
 def sesgd_set_option(ctx, option: int, value: int) -> None:

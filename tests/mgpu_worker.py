@@ -36,6 +36,7 @@ def main():
     p.add_argument("--final-avg", type=int, default=0)
     p.add_argument("--schedule", type=int, default=0)
     p.add_argument("--consensus", type=int, default=0)
+    p.add_argument("--wd", type=float, default=0.0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -47,7 +48,7 @@ def main():
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
                       grid=a.grid, timeout_ms=10000, p2p_variant=a.variant, path=a.path,
-                      hop_delay_ns=a.hop_ns,
+                      hop_delay_ns=a.hop_ns, weight_decay=a.wd,
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
                                                    (C.OPT_PUSH_TMA, a.tma),
                                                    (C.OPT_LOCAL_PERIOD, a.period),

@@ -29,7 +29,7 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0):
+            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -41,7 +41,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
-               "--schedule", str(schedule), "--consensus", str(consensus),
+               "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -304,3 +304,19 @@ def test_two_gpus_consensus_metric(tmp_path):
     for r in range(2):
         ss, mx = np.load(str(tmp_path / "res") + f".rank{r}.npz")["cons"]
         assert abs(ss - oss) <= 1e-9 * oss and abs(mx - omx) <= 1e-12 * omx
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n,path", [(4, 4), (4, 2), (2, 3), (2, 4)])
+def test_two_gpus_weight_decay(tmp_path, n, path, mode):
+    """NEXT-4 over NVLink: weight decay in K4 (two-shot), K3 (one-shot) and K5 (ring): the bits of
+    the oracle with the same decay."""
+    buckets = [65537, 3]
+    T, wd = 5, 1e-2
+    X, V = _launch(tmp_path, 2, n, 2, T, buckets, mode, path=path, wd=wd)
+    x = np.tile(synth.x0_host(sum(buckets)), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     weight_decay=wd)
+    _compare(X, x)
+    _compare(V, v)

@@ -314,3 +314,35 @@ def test_consensus_metric():
     eng.global_average()
     assert eng.consensus() == (0.0, 0.0)
     eng.close()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+@pytest.mark.parametrize("n,m", [(8, 2), (6, 3), (4, 1)])
+def test_weight_decay(n, m, mode, fused):
+    """NEXT-4: weight decay folded into the update (sesgd_set_weight_decay; the WD-compiled K6
+    kernels, templated and runtime m), the oracle's bits."""
+    SESGDEngine = _cuda()
+    T, buckets, wd = 5, [30001, 7], 1e-2
+    L = sum(buckets)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    eng = SESGDEngine(n, m, buckets, mode=mode, weight_decay=wd)
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(n):
+        for b, Lb in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), st)
+    for t in range(T):
+        for s in range(n):
+            for b, Lb in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), s, t, st)
+        eng.step(t, LR, MU, fused=fused)
+    torch.cuda.synchronize()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
+    V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(n)])
+    eng.close()
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, period=1, mode=mode,
+                     weight_decay=wd)
+    _compare(X, x)
+    _compare(V, v)

@@ -697,3 +697,51 @@ def test_consensus_group_average_contracts_and_matches_paper_claim():
     xr, _ = _run_local(n, n, T, L, 1)
     assert oracle.consensus(xs)[0] < 0.2 * oracle.consensus(xi)[0]
     assert oracle.consensus(xr) == (0.0, 0.0)
+
+
+# ---------------------------------------------------------------- NEXT-4: weight decay
+def _torch_sgd_wd(x0, grads, lr, mu, wd, dtype=torch.float64):
+    p = torch.nn.Parameter(torch.tensor(x0, dtype=dtype))
+    opt = torch.optim.SGD([p], lr=lr, momentum=mu, dampening=0.0, nesterov=False, weight_decay=wd)
+    for g in grads:
+        p.grad = torch.tensor(g, dtype=dtype)
+        opt.step()
+    return p.detach().numpy()
+
+
+def test_weight_decay_zero_is_identity():
+    n, m, T, L = 8, 2, 5, 97
+    a, va = _run_local(n, m, T, L, 1)
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, SEED, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, weight_decay=0.0)
+    assert np.array_equal(a, x) and np.array_equal(va, v)
+
+
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+def test_weight_decay_m1_is_torch_sgd(mode):
+    """P:325 (wd 5e-4): with m = 1 every worker is torch.optim.SGD(momentum, weight_decay) on its
+    own gradients (float32, within FMA-contraction tolerance)."""
+    n, T, L, wd = 3, 8, 400, 5e-4
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, 1, SEED, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     weight_decay=wd)
+    for i in range(n):
+        ref = _torch_sgd_wd(synth.x0_host(L), [synth.grad_host(i, t, L) for t in range(T)], 0.1, 0.9, wd,
+                            dtype=torch.float32)
+        np.testing.assert_allclose(x[i], ref, rtol=1e-6, atol=1e-8)
+
+
+def test_weight_decay_group_n_is_ring_sgd_with_decay():
+    """m = n: every worker equals torch.optim.SGD(weight_decay) on the global mean gradient (GRAD
+    mode; all workers share x, so gbar + wd x is the decayed mean gradient)."""
+    n, T, L, wd = 4, 6, 300, 1e-2
+    x = np.tile(synth.x0_host(L), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, n, SEED, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1,
+                     mode=oracle.MODE_GRAD, weight_decay=wd)
+    gbars = [np.mean([synth.grad_host(i, t, L).astype(np.float64) for i in range(n)], 0) for t in range(T)]
+    ref = _torch_sgd_wd(synth.x0_host(L).astype(np.float64), gbars, 0.1, 0.9, wd)
+    assert all(np.array_equal(x[0], x[i]) for i in range(n))
+    np.testing.assert_allclose(x[0], ref, rtol=0, atol=2e-7)
