@@ -26,6 +26,44 @@ from .engine import SESGDEngine
 from .workloads import assign_buckets
 
 
+class BucketReadiness:
+    """Host logic of the overlap: a countdown of the gradients each bucket still waits for; a
+    bucket is released only when it and every earlier bucket are complete, so every rank
+    enqueues the same bucket sequence (peers' kernels wait on the same bucket)."""
+
+    def __init__(self, counts):
+        self.counts = [int(c) for c in counts]
+        self.reset()
+
+    def reset(self, counts=None) -> None:
+        if counts is not None:
+            self.counts = [int(c) for c in counts]
+        self.pending = list(self.counts)
+        self.next = 0
+
+    def arrive(self, b: int):
+        """One gradient of bucket b accumulated; returns the buckets now released, in order."""
+        if self.pending[b] <= 0:
+            raise RuntimeError(f"bucket {b} received more gradients than it holds")
+        self.pending[b] -= 1
+        return self.release()
+
+    def release(self):
+        out = []
+        while self.next < len(self.pending) and self.pending[self.next] == 0:
+            out.append(self.next)
+            self.next += 1
+        return out
+
+    def force_all(self):
+        """No hooks (overlap off): every remaining bucket, in order."""
+        self.pending = [0] * len(self.pending)
+        return self.release()
+
+    def done(self) -> bool:
+        return self.next == len(self.pending)
+
+
 def _like(flat: torch.Tensor, p: torch.Tensor) -> torch.Tensor:
     """A view of the flat slice with p's shape and, when p is dense in channels_last, its
     strides (so cuDNN sees the weight layout it was given)."""
@@ -67,8 +105,7 @@ class SESGDDataParallel:
                     p.grad = gview  # gradient accumulates into it (in place)
                     self.bucket_of[id(p)] = b
                     off += k
-        self.pending = [0] * len(self.bucket_params)
-        self.next_bucket = 0
+        self.ready = BucketReadiness([len(b) for b in self.bucket_params])
         self.launched_in_backward = 0
         self.side = torch.cuda.Stream(dev)
         self.done_event = torch.cuda.Event()
@@ -90,33 +127,27 @@ class SESGDDataParallel:
         for g in self.engine.g_flat:
             g.zero_()
         self.engine.begin_iter(self.t)
-        self.pending = list(self._hooked)
-        self.next_bucket = 0
+        self.ready.reset(self._hooked)
         self.launched_in_backward = 0  # buckets whose sync was enqueued from a gradient hook
         self._order = []
 
-    def _launch_ready(self) -> None:
-        # strictly in bucket order on every rank (peers' kernels wait on the same bucket)
-        while self.next_bucket < len(self.pending) and self.pending[self.next_bucket] == 0:
+    def _launch(self, buckets) -> None:
+        for b in buckets:  # in bucket order (BucketReadiness)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
             self.side.wait_event(ev)
-            self.engine.sync_step(self.next_bucket, self.lr, self.momentum, self.side)
-            self.next_bucket += 1
+            self.engine.sync_step(b, self.lr, self.momentum, self.side)
 
     def _on_grad(self, p: torch.Tensor) -> None:
-        self.pending[self.bucket_of[id(p)]] -= 1
         self._order.append(p)
-        self._launch_ready()
-        self.launched_in_backward = self.next_bucket
+        self._launch(self.ready.arrive(self.bucket_of[id(p)]))
+        self.launched_in_backward = self.ready.next
 
     def finish_step(self) -> None:
         """After backward: sync every remaining bucket, then order the compute stream after the
         side stream (the next forward reads the updated parameters)."""
-        if not self.overlap:
-            self.pending = [0] * len(self.pending)
-        self._launch_ready()
-        if self.next_bucket != len(self.pending):
+        self._launch(self.ready.force_all() if not self.overlap else self.ready.release())
+        if not self.ready.done():
             raise RuntimeError("some gradients never arrived; every parameter must receive a gradient")
         self.done_event.record(self.side)
         torch.cuda.current_stream().wait_event(self.done_event)
