@@ -2,7 +2,7 @@
  * sesgd.h -- C ABI of libsesgd.so, the B200-native hot path of Shuffle-Exchange
  * SGD (SESGD, arXiv 2007.00433).
  *
- * Citations: P:n = the paper's PAPER.md line n, S:n = SPEC.md line n; R1..R17 are
+ * Citations: P:n = the paper's PAPER.md line n, S:n = SPEC.md line n; R1..R20 are
  * the readings of the paper listed in DESIGN.md ("Readings").
  *
  * What one iteration computes (Algorithm 1; Eq. 6):

@@ -8,7 +8,7 @@
  * seeded input generator, which holds none of the method's arithmetic.
  *
  * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (both under the
- * read-only reference tree); R1..R17 = readings listed in DESIGN.md.
+ * read-only reference tree); R1..R20 = readings listed in DESIGN.md.
  */
 #ifndef SESGD_ORACLE_H
 #define SESGD_ORACLE_H
