@@ -54,7 +54,7 @@ def parse():
     p.add_argument("--release-delay", type=int, default=0, help="two-shot: SESGD_OPT_RELEASE_DELAY")
     p.add_argument("--release-every", type=int, default=0, help="two-shot: SESGD_OPT_RELEASE_EVERY")
     p.add_argument("--release-stagger", type=int, default=0, help="SESGD_OPT_RELEASE_STAGGER")
-    p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot", "ring", "twoshot"])
+    p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot", "ring", "twoshot", "nvls"])
     p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
     p.add_argument("--comm-batch", type=int, default=0)
     p.add_argument("--fold-lag", type=int, default=0)
@@ -259,7 +259,7 @@ def run_sesgd(args):
                                                  (C.OPT_RELEASE_EVERY, args.release_every),
                                                  (C.OPT_RELEASE_STAGGER, args.release_stagger)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
-                            "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT}[args.path])
+                            "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT, "nvls": C.PATH_NVLS}[args.path])
     r = eng.r
     stream = torch.cuda.current_stream(dev)
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
@@ -337,7 +337,7 @@ def run_sesgd(args):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        kernel = {"twoshot": "k4_twoshot", "ring": "k5_ring"}.get(eff_path, "k3_push")
+        kernel = {"twoshot": "k4_twoshot", "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
         # of them 2(s-1)/s * 4 B per element (co-resident members pre-combine); max over

@@ -71,6 +71,12 @@ extern "C" {
                                  pushes of the slice means (co-resident members are read / updated
                                  in place); a remote member pair exchanges 2/m of a bucket instead of
                                  one-shot's full copy; needs P2P variant 0 (else SESGD_ENOTSUP) */
+#define SESGD_PATH_NVLS 5     /* NVLink SHARP, for group_size = n (Ring-SGD's single group) with one
+                                 worker per GPU: the slice owner reduces every GPU's stage inside
+                                 the NVSwitch (multimem.ld_reduce) and multicasts the mean
+                                 (multimem.st); needs sesgd_attach_multicast.  The switch's
+                                 summation order is unspecified: parity within the north-star
+                                 tolerance, bit-exact only for n = 2 (a + b = b + a) */
 
 /* ---- options for sesgd_set_option ---- */
 #define SESGD_OPT_MODE 1       /* SESGD_MODE_*                                   (default 0) */
@@ -257,6 +263,11 @@ SESGD_API int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *
  * Asynchronous on `stream` (K9, binary64 accumulation).  Errors: as sesgd_global_average. */
 SESGD_API int sesgd_consensus(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,
                               double *out_dev, void *stream);
+
+/* NVLS: the multicast mapping of the symmetric workspaces (e.g. torch symmetric memory's
+ * multicast_ptr of the same allocation whose per-rank pointers went to sesgd_attach_peers), for
+ * SESGD_PATH_NVLS.  Errors: SESGD_EINVAL (NULL), SESGD_ESTATE (peers not attached). */
+SESGD_API int sesgd_attach_multicast(sesgd_ctx *ctx, void *mc_ws);
 
 /* Weight decay folded into every update (the paper trains with 5e-4 / 1e-4; R20): the
  * gradient term of the momentum step becomes d = g (+) wd (x) x, as torch.optim.SGD's

@@ -122,6 +122,30 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 __device__ __forceinline__ void st_release_gpu(uint64_t *p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// NVLS (NVLink SHARP): loads that the NVSwitch reduces over every GPU's copy of a multicast
+// address, and stores it replicates to every GPU (sm_90+ multimem)
+__device__ __forceinline__ void mm_ld_reduce4(const float *mc, float (&r)[4]) {
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+               : "l"(mc)
+               : "memory");
+}
+__device__ __forceinline__ float mm_ld_reduce1(const float *mc) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(mc) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st4(float *mc, const float (&r)[4]) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "f"(r[0]),
+               "f"(r[1]), "f"(r[2]), "f"(r[3])
+               : "memory");
+}
+__device__ __forceinline__ void mm_st1(float *mc, float r) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(r) : "memory");
+}
+// the same memory is accessed through the multicast and the unicast mappings
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
 __device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -877,7 +901,7 @@ struct Split {
   // pushed to the owner's receive slot [p_s].  The owner applies the mean to co-resident members
   // directly (their x, v are on this GPU) and pushes it to remote members.  Groups whose members
   // all live here are updated in registers (slot_kind 1 / 2, as in K3).
-  template <bool TMA, bool MULTI>
+  template <bool TMA, bool MULTI, bool NV = false>
   __device__ void ts_rs_stage(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     const int S = ts_slice();
@@ -920,7 +944,7 @@ struct Split {
         }
         const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
         const int w = G[j];
-        if (!rem<MULTI>(w)) {
+        if (NV || !rem<MULTI>(w)) {  // NVLS: every owner reduces my stage through the switch
           st_slot<W>(stage(s) + c.soff + e, val, nv);  // read in place by the local owner
         } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
           st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
@@ -954,6 +978,7 @@ struct Split {
       }
       __syncwarp();
     }
+    if (a.mc_ws) fence_proxy_alias();  // NVLS: multicast stores before the unicast flags
     dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
     const int64_t nrs = (rs1 - rs0) * pairs, nall = nrs + (ag1 - ag0) * pairs;
     for (int64_t q = threadIdx.x; q < nall; q += 32) {
@@ -981,11 +1006,12 @@ struct Split {
     __syncthreads();
   }
 
-  template <bool TMA, bool MULTI>
+  template <bool TMA, bool MULTI, bool NV = false>
   __device__ void ts_reduce(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     if (TMA && threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();  // entry free (+ sync below)
     ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 1);
+    if constexpr (NV) fence_proxy_alias();  // peers' stages are read through the multicast mapping
     const int64_t len = c.e1 - c.e0;
     for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
       if (MULTI && a.slot_kind[s] != 0) continue;
@@ -997,22 +1023,39 @@ struct Split {
         const int64_t e = c.e0 + o;
         const int nv = (int)min(int64_t(W), hi - o);
         float acc[W];
-        for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
-          const int w = G[rr];
-          const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
-          float y[W];
-          ld_slot<W>(src + c.soff + e, y, nv);
+        if constexpr (NV) {  // the switch sums every GPU's stage (order unspecified: tolerance parity)
+          const float *mc = reinterpret_cast<const float *>(a.mc_ws + a.stage_off) + c.soff + e;
+          if (W == 4 && nv == 4) {
+            mm_ld_reduce4(mc, reinterpret_cast<float(&)[4]>(acc));
+          } else {
+            for (int q = 0; q < W; ++q) acc[q] = (q < nv) ? mm_ld_reduce1(mc + q) : 0.f;
+          }
+        } else {
+          for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
+            const int w = G[rr];
+            const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
+            float y[W];
+            ld_slot<W>(src + c.soff + e, y, nv);
 #pragma unroll
-          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
+            for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
+          }
         }
 #pragma unroll
         for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
+        if constexpr (NV) {  // all-gather: one multicast store reaches every member's slot [p]
+          float *mc = reinterpret_cast<float *>(a.mc_ws + a.recv_off) +
+                      (int64_t(a.parity) * a.m + p) * a.region_floats + c.soff + e;
+          if (W == 4 && nv == 4)
+            mm_st4(mc, reinterpret_cast<float(&)[4]>(acc));
+          else
+            for (int q = 0; q < nv; ++q) mm_st1(mc + q, acc[q]);
+        }
         const bool bulk = TMA && o + nv <= bh;
         if (bulk) st_slot<W>(ent + o, acc, nv);  // all-gather image, bulk-pushed below (r == 1)
         for (int rr = 0; rr < a.m; ++rr) {  // apply to every member: here directly, else push
           const int w = G[rr];
           if (rem<MULTI>(w)) {
-            if (!bulk) st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
+            if (!bulk && !NV) st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
             continue;
           }
           const int sl = a.worker_slot[w];
@@ -1058,10 +1101,11 @@ struct Split {
   }
 
   // the slices owned by remote members: their means arrived in my receive slots
-  template <bool MULTI>
+  template <bool MULTI, bool NV = false>
   __device__ void ts_finish(int64_t g) const {
     const ChunkRef c = locate(g);
     ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 2);
+    if constexpr (NV) fence_proxy_alias();  // the means arrived through the multicast mapping
     const int64_t len = c.e1 - c.e0;
     for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
       if (MULTI && a.slot_kind[s] != 0) continue;
@@ -1118,7 +1162,7 @@ struct Split {
   // last step may still be in flight).  A chunk pushed at step s is released by step
   // s + D + R - 1, so with reduce L >= D + R - 1 steps after rs_stage (and finish L after
   // reduce) every wait targets a flag released at the top of this step or an earlier one.
-  template <bool TMA, bool MULTI>
+  template <bool TMA, bool MULTI, bool NV = false>
   __device__ void compute_twoshot(int i, float *ring) const {
     const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
     const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
@@ -1162,7 +1206,7 @@ struct Split {
         t0 = t1;
       }
       if (k < nk) {
-        ts_rs_stage<TMA, MULTI>(first + k * gc, ring + (q % kPushRing) * kChunk);
+        ts_rs_stage<TMA, MULTI, NV>(first + k * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1171,7 +1215,7 @@ struct Split {
         t0 = t1;
       }
       if (k >= L && k - L < nk) {
-        ts_reduce<TMA, MULTI>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
+        ts_reduce<TMA, MULTI, NV>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1179,7 +1223,7 @@ struct Split {
         t_red += t1 - t0;
         t0 = t1;
       }
-      if (k >= 2 * L && k - 2 * L < nk) ts_finish<MULTI>(first + (k - 2 * L) * gc);
+      if (k >= 2 * L && k - 2 * L < nk) ts_finish<MULTI, NV>(first + (k - 2 * L) * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_fin += t1 - t0;
@@ -1252,14 +1296,14 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
     p.compute_direct(blockIdx.x);
 }
 
-template <int W, bool GRAD, bool TMA, bool MULTI>
+template <int W, bool GRAD, bool TMA, bool MULTI, bool NV = false>
 __global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];  // TMA: kPushRing chunk images
   const Split<W, GRAD> p(a);
   if (a.m == 1)
     p.local_only();
   else
-    p.template compute_twoshot<TMA, MULTI>(blockIdx.x, reinterpret_cast<float *>(dsmem));
+    p.template compute_twoshot<TMA, MULTI, NV>(blockIdx.x, reinterpret_cast<float *>(dsmem));
 }
 
 constexpr size_t kTwoshotTmaSmem = size_t(Split<4, false>::kPushRing) * size_t(kChunk) * 4;  // 48 KiB
@@ -1272,6 +1316,15 @@ const void *pick_twoshot_t(int mode, bool vec) {
                 : reinterpret_cast<const void *>(&k4_twoshot<4, false, TMA, MULTI>);
   return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, TMA, MULTI>)
               : reinterpret_cast<const void *>(&k4_twoshot<1, false, TMA, MULTI>);
+}
+// NVLS: the switch reduces and multicasts (one worker per GPU, one group of all workers)
+const void *pick_nvls(int mode, bool vec) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (vec)
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, false, false, true>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false, false, false, true>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, false, true>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, false, true>);
 }
 // TMA pushes: one worker per GPU only; several workers per GPU: the MULTI kernel
 const void *pick_twoshot(int mode, bool vec, bool tma, bool multi) {
@@ -1328,6 +1381,15 @@ cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec
 }
 
 int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
+  int nv = 0;  // the NVLS kernels must fit the same grid
+  if (!tma && !multi &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nv, pick_nvls(mode, vec), kThreads, 0) == cudaSuccess &&
+      nv > 0) {
+    int base = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&base, pick_twoshot(mode, vec, false, false), kThreads, 0) ==
+            cudaSuccess && base > 0)
+      return nv < base ? nv : base;
+  }
   const void *k = pick_twoshot(mode, vec, tma, multi);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1338,7 +1400,7 @@ int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
 }
 
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream) {
-  const void *k = pick_twoshot(mode, vec, tma, a.r > 1);
+  const void *k = a.mc_ws ? pick_nvls(mode, vec) : pick_twoshot(mode, vec, tma, a.r > 1);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};

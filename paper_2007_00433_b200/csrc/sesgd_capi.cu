@@ -78,7 +78,8 @@ void free_bucket(sesgd_bucket &b) {
 //   [recv_off, ..)      f32 recv    [2 parity][r slot][m position][region]
 // region = stage_slot_floats = sum over buckets of round_up(numel, 64).
 void freeze_layout(sesgd_ctx *ctx) {
-  if (ctx->path == SESGD_PATH_TWOSHOT) ctx->p2p_variant = 0;  // K4 runs on the DIRECT grid
+  if (ctx->path == SESGD_PATH_TWOSHOT || ctx->path == SESGD_PATH_NVLS)
+    ctx->p2p_variant = 0;  // K4 runs on the DIRECT grid
   const int var = ctx->p2p_variant;
   const int chunk = sesgd::p2p_chunk_elems(var);
   const int r = ctx->n_local;
@@ -332,7 +333,7 @@ int upload_tables(sesgd_ctx *ctx) {
 // One one-shot launch over bucket `bucket` (>= 0) or over every bucket (-1, all buckets
 // share the same call history).  Host bookkeeping of calls / launch sequence follows.
 int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st,
-                   bool twoshot = false) {
+                   bool twoshot = false, bool nvls = false) {
   const sesgd_bucket &ref = ctx->buckets[bucket >= 0 ? bucket : 0];
   P2PArgs a{};
   a.meta = ctx->d_meta;
@@ -340,6 +341,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.bv = ctx->d_bv;
   a.bg = ctx->d_bg;
   for (int r = 0; r < ctx->n_ranks; ++r) a.ws[r] = ctx->ws[r];
+  a.mc_ws = nvls ? ctx->mc_ws : nullptr;
   if (bucket >= 0) {
     a.g0 = ref.chunk_base;
     a.g1 = ref.chunk_base + ref.nchunks;
@@ -522,7 +524,7 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->mode = int(value);
       return SESGD_OK;
     case SESGD_OPT_PATH:
-      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_TWOSHOT)
+      if (value < SESGD_PATH_AUTO || value > SESGD_PATH_NVLS)
         return fail(ctx, SESGD_EINVAL, "unknown path");
       if (ctx->peers && value != ctx->path)  // the consumption guards are per path
         return fail(ctx, SESGD_ESTATE, "the path is fixed once peers attach");
@@ -771,6 +773,13 @@ int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, void *cons
   return SESGD_OK;
 }
 
+int sesgd_attach_multicast(sesgd_ctx *ctx, void *mc_ws) {
+  if (!ctx || !mc_ws) return SESGD_EINVAL;
+  if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first");
+  ctx->mc_ws = static_cast<char *>(mc_ws);
+  return SESGD_OK;
+}
+
 int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter) {
   if (!ctx) return SESGD_EINVAL;
   if (iter < 0) return fail(ctx, SESGD_EINVAL, "iteration must be >= 0");
@@ -873,7 +882,11 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
   if (path == SESGD_PATH_TWOSHOT && (ctx->p2p_variant != 0 || (ctx->push_tma && ctx->n_local != 1)))
     return fail(ctx, SESGD_ENOTSUP, "two-shot needs the DIRECT layout; its TMA pushes one worker per GPU");
-  return launch_oneshot(ctx, bucket, lr, momentum, st, path == SESGD_PATH_TWOSHOT);
+  if (path == SESGD_PATH_NVLS && (ctx->p2p_variant != 0 || ctx->n_local != 1 || ctx->m != ctx->n || !ctx->mc_ws))
+    return fail(ctx, SESGD_ENOTSUP,
+                "the NVLS path needs one worker per GPU, group_size = n and sesgd_attach_multicast");
+  return launch_oneshot(ctx, bucket, lr, momentum, st,
+                        path == SESGD_PATH_TWOSHOT || path == SESGD_PATH_NVLS, path == SESGD_PATH_NVLS);
 }
 
 int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
@@ -926,9 +939,11 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     ctx->buckets[0].stats.kernel_launches++;
     return SESGD_OK;
   }
-  const bool twoshot = (path == SESGD_PATH_TWOSHOT);
+  const bool nvls = (path == SESGD_PATH_NVLS);
+  const bool twoshot = (path == SESGD_PATH_TWOSHOT) || nvls;
   bool fuse = (path == SESGD_PATH_ONESHOT ||
-               (twoshot && ctx->p2p_variant == 0 && (!ctx->push_tma || ctx->n_local == 1))) &&
+               (twoshot && ctx->p2p_variant == 0 && (!ctx->push_tma || ctx->n_local == 1)) ||
+               (nvls && ctx->n_local == 1 && ctx->m == ctx->n && ctx->mc_ws)) &&
               ctx->peers;
   for (auto &b : ctx->buckets)  // one launch needs one shared call history
     fuse = fuse && b.calls == ctx->buckets[0].calls && b.seq_hist[0] == ctx->buckets[0].seq_hist[0] &&
@@ -941,7 +956,7 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     return SESGD_OK;
   }
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
-  return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot);
+  return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot, nvls);
 }
 
 int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,

@@ -35,6 +35,7 @@ class SESGDEngine:
         if n % world != 0:
             raise ValueError("n must be a multiple of the number of ranks")
         self.n, self.m, self.seed = n, group_size, seed
+        self.path = path
         self.rank, self.world = rank, world
         self.r = n // world
         self.local_workers = list(range(rank * self.r, (rank + 1) * self.r))
@@ -95,6 +96,11 @@ class SESGDEngine:
         dist.barrier(group=group)
         ptrs = list(self._symm.buffer_ptrs)
         C.sesgd_attach_peers(self.ctx, self.world, self.rank, ptrs, self.worker_rank)
+        if self.path == C.PATH_NVLS:  # NVLink SHARP: the multicast mapping of the same workspace
+            mc = int(self._symm.multicast_ptr)
+            if not mc:
+                raise RuntimeError("SESGD_PATH_NVLS needs NVSwitch multicast (no multicast_ptr)")
+            C.sesgd_attach_multicast(self.ctx, mc)
         dist.barrier(group=group)
 
     # -------------------------------------------------------------- views

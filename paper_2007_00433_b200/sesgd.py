@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libsesgd.so")
 OK, EINVAL, ENOTDIV, ESTATE, ECUDA, ETIMEOUT, ENOMEM, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7
 MAX_WORKERS, MAX_RANKS = 64, 8
 MODE_PARAM_AVG, MODE_GRAD_AVG = 0, 1
-PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT, PATH_RING, PATH_TWOSHOT = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_RESIDENT, PATH_ONESHOT, PATH_RING, PATH_TWOSHOT, PATH_NVLS = 0, 1, 2, 3, 4, 5
 OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS, OPT_P2P_VARIANT, OPT_DISCARD = (
     1, 2, 3, 4, 5, 6, 7)
 OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL, OPT_PUSH_TMA = 8, 9, 10, 11, 12
@@ -33,6 +33,7 @@ EXPORTED = (
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
     "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus", "sesgd_set_weight_decay",
+    "sesgd_attach_multicast",
 )
 
 
@@ -83,6 +84,7 @@ def lib():
             "sesgd_sync_all_host": ([P, f32, f32, P, P, P], ctypes.c_int),
             "sesgd_consensus": ([P, i32, P, i32, P, P], ctypes.c_int),
             "sesgd_set_weight_decay": ([P, f32], ctypes.c_int),
+            "sesgd_attach_multicast": ([P, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -135,6 +137,10 @@ def sesgd_latency_model(n: int, group_size: int, nbytes: float, nu_Bps: float, t
     _check(lib().sesgd_latency_model(n, group_size, float(nbytes), float(nu_Bps), float(tau_s),
                                      ctypes.byref(out)))
     return {f: getattr(out, f) for f, _ in sesgd_cost._fields_}
+
+
+def sesgd_attach_multicast(ctx, mc_ptr: int) -> None:
+    _check(lib().sesgd_attach_multicast(ctx, ctypes.c_void_p(int(mc_ptr))), ctx)
 
 
 def sesgd_set_weight_decay(ctx, weight_decay: float) -> None:

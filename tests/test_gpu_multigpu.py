@@ -320,3 +320,36 @@ def test_two_gpus_weight_decay(tmp_path, n, path, mode):
                      weight_decay=wd)
     _compare(X, x)
     _compare(V, v)
+
+
+# ---------------------------------------------------------------- NVLS (path 5), group_size = n
+def _nvls_or_skip(tmp_path, gpus, n, mode, buckets, T):
+    try:
+        return _launch(tmp_path, gpus, n, n, T, buckets, mode, path=5)
+    except AssertionError as e:
+        if "multicast" in str(e):
+            pytest.skip("no NVSwitch multicast on this box")
+        raise
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_two_gpus_nvls_bitexact(tmp_path, mode):
+    """NVLS with n = m = 2: the switch adds two values (a + b = b + a), so even the in-switch
+    reduction gives the oracle's bits."""
+    buckets = [100003, 7, 4096]
+    X, V = _nvls_or_skip(tmp_path, 2, 2, mode, buckets, 5)
+    x, v = _oracle(2, 2, sum(buckets), 5, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_four_gpus_nvls(tmp_path, mode):
+    """NVLS with n = m = 4 (Ring-SGD's single group): within the north-star tolerance of the
+    oracle (the switch's summation order is unspecified) and every worker byte-identical."""
+    buckets = [200003, 5]
+    X, V = _nvls_or_skip(tmp_path, 4, 4, mode, buckets, 5)
+    x, v = _oracle(4, 4, sum(buckets), 5, mode)
+    np.testing.assert_allclose(X, x, rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(V, v, rtol=1e-5, atol=1e-7)
+    assert all(np.array_equal(X[0], X[i]) for i in range(4))
