@@ -137,12 +137,12 @@ def test_call_order_errors_without_gpu():
         with pytest.raises(C.SesgdError) as e:
             C.sesgd_groups(ctx, -1, 4)
         assert e.value.code == C.EINVAL
-        for opt, val in [(C.OPT_MODE, 7), (C.OPT_PATH, 9), (C.OPT_PATH, C.PATH_TWOSHOT + 1),
+        for opt, val in [(C.OPT_MODE, 7), (C.OPT_PATH, 9), (C.OPT_PATH, C.PATH_NVLS + 1),
                          (C.OPT_TIMEOUT_MS, 0), (99, 0)]:
             with pytest.raises(C.SesgdError) as e:
                 C.sesgd_set_option(ctx, opt, val)
             assert e.value.code == C.EINVAL
-        for p in (C.PATH_AUTO, C.PATH_RESIDENT, C.PATH_ONESHOT, C.PATH_RING, C.PATH_TWOSHOT):
+        for p in (C.PATH_AUTO, C.PATH_RESIDENT, C.PATH_ONESHOT, C.PATH_RING, C.PATH_TWOSHOT, C.PATH_NVLS):
             C.sesgd_set_option(ctx, C.OPT_PATH, p)
         C.sesgd_set_option(ctx, C.OPT_MODE, C.MODE_GRAD_AVG)
         assert "invalid" in C.lib().sesgd_strerror(C.EINVAL).decode()
