@@ -264,6 +264,15 @@ SESGD_API int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *
 SESGD_API int sesgd_consensus(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,
                               double *out_dev, void *stream);
 
+/* Pair-split statistics on the device (the appendix's Monte Carlo: Pr[i, j in different
+ * groups] = n (k - 1) / (k (n - 1))): for every iteration t in [t0, t0 + T) the context's
+ * schedule (seed, n, group_size, SESGD_OPT_SCHEDULE) is evaluated on the GPU (K10, one thread per
+ * t) and counts_dev[min(i,j) * n + max(i,j)] is incremented when workers i and j share a group.
+ * counts_dev: n*n unsigned 64-bit device counters, caller-owned, accumulated (zero them first).
+ * Needs sesgd_attach (device).  Errors: SESGD_EINVAL, SESGD_ESTATE, SESGD_ECUDA. */
+SESGD_API int sesgd_pair_counts(sesgd_ctx *ctx, int64_t t0, int64_t T, unsigned long long *counts_dev,
+                                void *stream);
+
 /* NVLS: the multicast mapping of the symmetric workspaces (e.g. torch symmetric memory's
  * multicast_ptr of the same allocation whose per-rank pointers went to sesgd_attach_peers), for
  * SESGD_PATH_NVLS.  Errors: SESGD_EINVAL (NULL), SESGD_ESTATE (peers not attached). */

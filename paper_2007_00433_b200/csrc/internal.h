@@ -56,6 +56,10 @@ struct AverageArgs {
   int64_t numel;
 };
 cudaError_t launch_average(const AverageArgs &a, bool vec, int sm_count, cudaStream_t stream);
+// K10: pair co-membership counts over iterations [t0, t0 + T): counts[min(i,j) * n + max(i,j)] +=
+// number of iterations in which workers i and j share a group (schedule 0 random, 1 dimension exchange)
+cudaError_t launch_pair_counts(uint64_t seed, int64_t t0, int64_t T, int n, int m, int schedule,
+                               unsigned long long *counts, int sm_count, cudaStream_t stream);
 // K9: consistency metric (rows only; outs unused): out[0] += sum (x - mean)^2, out[1] = max |x - mean|
 cudaError_t launch_consensus(const AverageArgs &a, double *out, int sm_count, cudaStream_t stream);
 int resident_occupancy(int mode, bool vec, int m, int unroll);

@@ -773,6 +773,17 @@ int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, void *cons
   return SESGD_OK;
 }
 
+int sesgd_pair_counts(sesgd_ctx *ctx, int64_t t0, int64_t T, unsigned long long *counts_dev,
+                      void *stream) {
+  if (!ctx || !counts_dev || t0 < 0 || T < 0) return SESGD_EINVAL;
+  if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
+  if (T == 0) return SESGD_OK;
+  cudaError_t e = sesgd::launch_pair_counts(ctx->seed, t0, T, ctx->n, ctx->m, ctx->schedule, counts_dev,
+                                            ctx->sm_count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch pair counts");
+  return SESGD_OK;
+}
+
 int sesgd_attach_multicast(sesgd_ctx *ctx, void *mc_ws) {
   if (!ctx || !mc_ws) return SESGD_EINVAL;
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first");

@@ -33,7 +33,7 @@ EXPORTED = (
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
     "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus", "sesgd_set_weight_decay",
-    "sesgd_attach_multicast",
+    "sesgd_attach_multicast", "sesgd_pair_counts",
 )
 
 
@@ -85,6 +85,7 @@ def lib():
             "sesgd_consensus": ([P, i32, P, i32, P, P], ctypes.c_int),
             "sesgd_set_weight_decay": ([P, f32], ctypes.c_int),
             "sesgd_attach_multicast": ([P, P], ctypes.c_int),
+            "sesgd_pair_counts": ([P, i64, i64, P, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
@@ -137,6 +138,12 @@ def sesgd_latency_model(n: int, group_size: int, nbytes: float, nu_Bps: float, t
     _check(lib().sesgd_latency_model(n, group_size, float(nbytes), float(nu_Bps), float(tau_s),
                                      ctypes.byref(out)))
     return {f: getattr(out, f) for f, _ in sesgd_cost._fields_}
+
+
+def sesgd_pair_counts(ctx, t0: int, T: int, counts_dev_ptr: int, stream: int = 0) -> None:
+    """Accumulate into n*n device u64 counters how often each worker pair shares a group."""
+    _check(lib().sesgd_pair_counts(ctx, t0, T, ctypes.c_void_p(int(counts_dev_ptr)),
+                                   ctypes.c_void_p(int(stream))), ctx)
 
 
 def sesgd_attach_multicast(ctx, mc_ptr: int) -> None:

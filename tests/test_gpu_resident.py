@@ -346,3 +346,51 @@ def test_weight_decay(n, m, mode, fused):
                      weight_decay=wd)
     _compare(X, x)
     _compare(V, v)
+
+
+@pytest.mark.parametrize("n,m,schedule", [(8, 2, 0), (16, 4, 0), (6, 3, 0), (8, 2, 1), (16, 4, 1)])
+def test_pair_counts_on_device(n, m, schedule):
+    """NEXT-4: the schedule evaluated on the device (K10) counts the same co-memberships as the
+    oracle's schedule over 3000 iterations (integers: exact)."""
+    _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    ctx = C.sesgd_init(n, m, 42)
+    try:
+        if schedule:
+            C.sesgd_set_option(ctx, C.OPT_SCHEDULE, 1)
+        C.sesgd_attach(ctx, 0, list(range(n)))
+        counts = torch.zeros(n * n, dtype=torch.int64, device="cuda")
+        t0, T = 17, 3000
+        C.sesgd_pair_counts(ctx, t0, T, counts.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        got = counts.cpu().numpy().reshape(n, n)
+    finally:
+        C.sesgd_destroy(ctx)
+    want = np.zeros((n, n), np.int64)
+    for t in range(t0, t0 + T):
+        gof = oracle.groups_stone(t, n, m)[1] if schedule else oracle.groups(42, t, n, m)[2]
+        for i in range(n):
+            for j in range(i + 1, n):
+                want[i, j] += int(gof[i] == gof[j])
+    assert np.array_equal(got, want)
+
+
+def test_pair_split_probability_on_device():
+    """P5 / P:498 at scale: over 4 M iterations of the random schedule the pair-split frequency of
+    every pair matches n (k - 1) / (k (n - 1)) within 5 sigma (n = 16, k = 4: 0.8)."""
+    _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    n, m, T = 16, 4, 4_000_000
+    ctx = C.sesgd_init(n, m, 42)
+    try:
+        C.sesgd_attach(ctx, 0, list(range(n)))
+        counts = torch.zeros(n * n, dtype=torch.int64, device="cuda")
+        C.sesgd_pair_counts(ctx, 0, T, counts.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        together = counts.cpu().numpy().reshape(n, n)[np.triu_indices(n, 1)]
+    finally:
+        C.sesgd_destroy(ctx)
+    k = n // m
+    p_split = n * (k - 1) / (k * (n - 1))
+    split = T - together
+    sigma = np.sqrt(T * p_split * (1 - p_split))
+    assert abs(p_split - 0.8) < 1e-15
+    assert np.all(np.abs(split - T * p_split) < 5 * sigma)
