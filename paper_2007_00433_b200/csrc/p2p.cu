@@ -1,7 +1,12 @@
-// p2p.cu -- K3: fused local update + ONE-SHOT PUSH intra-group exchange over NVLink,
-// SM-specialised: a few COMM CTAs move data over NVLink while the COMPUTE CTAs
-// stream HBM, in one persistent kernel over a range of chunks (one bucket, or every
-// bucket of the iteration at once with sesgd_sync_all).
+// p2p.cu -- the multi-GPU kernels: fused local update + intra-group exchange over NVLink,
+// one persistent kernel over a range of chunks (one bucket, or every bucket of the
+// iteration at once with sesgd_sync_all):
+//   K4 k4_twoshot (default, "K4 TWO-SHOT" below): reduce-scatter + all-gather pushes, every
+//      member owns a slice of each chunk; variants with TMA bulk pushes, several workers per
+//      GPU (MULTI) and NVLink SHARP (NV: multimem.ld_reduce / multimem.st);
+//   K3 k3_direct: one-shot push from every CTA (DIRECT, below);
+//   K3 k3_split: SM-specialised one-shot, a few COMM CTAs move data over NVLink while the
+//      COMPUTE CTAs stream HBM (described in this header).
 //
 // Each iteration every group G = {a_0 < ... < a_{m-1}} of the shuffle-exchange
 // partition (A1) averages its members' locally-stepped parameters (Eq. 6,
