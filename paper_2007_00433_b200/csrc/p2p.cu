@@ -906,6 +906,107 @@ struct Split {
   // pushed to the owner's receive slot [p_s].  The owner applies the mean to co-resident members
   // directly (their x, v are on this GPU) and pushes it to remote members.  Groups whose members
   // all live here are updated in registers (slot_kind 1 / 2, as in K3).
+  // ---- NVLS (one worker per GPU, group_size = n): chunk g is OWNED by position g mod m.  The
+  // owner waits until every member staged chunk g (RS flags), then reduces the whole chunk in the
+  // NVSwitch with multimem.ld_reduce on the multicast mapping of the stages (kItems 16-byte loads
+  // in flight per thread), divides by m, stores its own x and multicasts the mean into every
+  // member's receive slot [owner] with multimem.st (AG flag).  The other members take the mean
+  // from that slot in nv_finish.  A member's stage of chunk g is read only by the owner, which
+  // releases its AG flag after the read, so the next call's stage cannot overtake it.
+  __device__ void nv_reduce(int64_t g) const {
+    const ChunkRef c = locate(g);
+    const int me = a.my_workers[0];
+    const int p = a.my_pos[0];
+    const int own = int(g % a.m);
+    if (own != p) return;
+    if (threadIdx.x < 32) {
+      for (int j = threadIdx.x; j < a.m; j += 32)
+        if (j != p) wait_geq(a, ready(me, g, j), 2 * uint64_t(a.call) + 1, kWaitReady, me, j);
+    }
+    __syncthreads();
+    fence_proxy_alias();  // peers' stages are read through the multicast mapping
+    const float *mcs = reinterpret_cast<const float *>(a.mc_ws + a.stage_off) + c.soff;
+    float *mcr = reinterpret_cast<float *>(a.mc_ws + a.recv_off) +
+                 (int64_t(a.parity) * a.m + p) * a.region_floats + c.soff;
+    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
+    float acc[kItems][W];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {  // every load in flight before the first use
+      const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+      const int nv = (int)min(int64_t(W), c.e1 - e);
+      if (W == 4 && nv == 4) {
+        mm_ld_reduce4(mcs + e, reinterpret_cast<float(&)[4]>(acc[it]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[it][q] = (q < nv) ? mm_ld_reduce1(mcs + e + q) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+      const int nv = (int)min(int64_t(W), c.e1 - e);
+      if (nv <= 0) continue;
+      float m4[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) m4[q] = __fdiv_rn(acc[it][q], (float)a.m);
+      if (W == 4 && nv == 4)
+        mm_st4(mcr + e, reinterpret_cast<float(&)[4]>(m4));
+      else
+        for (int q = 0; q < nv; ++q) mm_st1(mcr + e + q, m4[q]);
+      if constexpr (!GRAD) {
+        store_m<W>(xs + e, m4, nv);
+      } else {
+        float v[W], x[W];
+        load_m<W>(vs + e, v, nv);
+        load_m<W>(xs + e, x, nv);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          v[q] = dev::momentum(a.mu, v[q], dev::decay(m4[q], a.wd, x[q]));
+          x[q] = dev::sgd(x[q], a.lr, v[q]);
+        }
+        store_m<W>(vs + e, v, nv);
+        store_m<W>(xs + e, x, nv);
+      }
+    }
+    __syncthreads();  // the multicast stores precede the (deferred) AG flag release
+  }
+
+  __device__ void nv_finish(int64_t g) const {
+    const ChunkRef c = locate(g);
+    const int me = a.my_workers[0];
+    const int p = a.my_pos[0];
+    const int own = int(g % a.m);
+    if (own == p) return;  // applied in nv_reduce
+    if (threadIdx.x == 0) wait_geq(a, ready(me, g, own), 2 * uint64_t(a.call) + 2, kWaitReady, me, own);
+    __syncthreads();
+    fence_proxy_alias();  // the mean arrived through the multicast mapping
+    const float *src = recv(me, own) + c.soff;
+    float *xs = a.bx[c.b * a.r], *vs = a.bv[c.b * a.r];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t e = c.e0 + (int64_t(it) * kThreads + threadIdx.x) * W;
+      const int nv = (int)min(int64_t(W), c.e1 - e);
+      if (nv <= 0) continue;
+      float y[W];
+      ld_slot<W>(src + e, y, nv);
+      if constexpr (!GRAD) {
+        store_m<W>(xs + e, y, nv);
+      } else {
+        float v[W], x[W];
+        load_m<W>(vs + e, v, nv);
+        load_m<W>(xs + e, x, nv);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          v[q] = dev::momentum(a.mu, v[q], dev::decay(y[q], a.wd, x[q]));
+          x[q] = dev::sgd(x[q], a.lr, v[q]);
+        }
+        store_m<W>(vs + e, v, nv);
+        store_m<W>(xs + e, x, nv);
+      }
+    }
+    __syncthreads();
+  }
+
   template <bool TMA, bool MULTI, bool NV = false>
   __device__ void ts_rs_stage(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
@@ -992,6 +1093,10 @@ struct Split {
       const int64_t c = (kind == 0 ? rs0 : ag0) + qq / pairs;
       const int pr = int(qq % pairs), s = pr / a.m, j = pr % a.m;
       if ((MULTI && a.slot_kind[s] != 0) || j == a.my_pos[s]) continue;
+      if (a.mc_ws) {  // NVLS: staged -> the chunk's owner only; AG flags only from the owner
+        const int own = int((first + c * gc) % a.m);
+        if (kind == 0 ? (j != own) : (a.my_pos[s] != own)) continue;
+      }
       const int w = group(a.my_workers[s])[j];
       if (rem<MULTI>(w)) st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), e1 + kind);
     }
@@ -1015,8 +1120,11 @@ struct Split {
   __device__ void ts_reduce(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     if (TMA && threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();  // entry free (+ sync below)
+    if constexpr (NV) {
+      nv_reduce(g);
+      return;
+    }
     ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 1);
-    if constexpr (NV) fence_proxy_alias();  // peers' stages are read through the multicast mapping
     const int64_t len = c.e1 - c.e0;
     for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
       if (MULTI && a.slot_kind[s] != 0) continue;
@@ -1028,39 +1136,22 @@ struct Split {
         const int64_t e = c.e0 + o;
         const int nv = (int)min(int64_t(W), hi - o);
         float acc[W];
-        if constexpr (NV) {  // the switch sums every GPU's stage (order unspecified: tolerance parity)
-          const float *mc = reinterpret_cast<const float *>(a.mc_ws + a.stage_off) + c.soff + e;
-          if (W == 4 && nv == 4) {
-            mm_ld_reduce4(mc, reinterpret_cast<float(&)[4]>(acc));
-          } else {
-            for (int q = 0; q < W; ++q) acc[q] = (q < nv) ? mm_ld_reduce1(mc + q) : 0.f;
-          }
-        } else {
-          for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
-            const int w = G[rr];
-            const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
-            float y[W];
-            ld_slot<W>(src + c.soff + e, y, nv);
+        for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
+          const int w = G[rr];
+          const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
+          float y[W];
+          ld_slot<W>(src + c.soff + e, y, nv);
 #pragma unroll
-            for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
-          }
+          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
         }
 #pragma unroll
         for (int q = 0; q < W; ++q) acc[q] = __fdiv_rn(acc[q], (float)a.m);
-        if constexpr (NV) {  // all-gather: one multicast store reaches every member's slot [p]
-          float *mc = reinterpret_cast<float *>(a.mc_ws + a.recv_off) +
-                      (int64_t(a.parity) * a.m + p) * a.region_floats + c.soff + e;
-          if (W == 4 && nv == 4)
-            mm_st4(mc, reinterpret_cast<float(&)[4]>(acc));
-          else
-            for (int q = 0; q < nv; ++q) mm_st1(mc + q, acc[q]);
-        }
         const bool bulk = TMA && o + nv <= bh;
         if (bulk) st_slot<W>(ent + o, acc, nv);  // all-gather image, bulk-pushed below (r == 1)
         for (int rr = 0; rr < a.m; ++rr) {  // apply to every member: here directly, else push
           const int w = G[rr];
           if (rem<MULTI>(w)) {
-            if (!bulk && !NV) st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
+            if (!bulk) st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
             continue;
           }
           const int sl = a.worker_slot[w];
@@ -1109,8 +1200,11 @@ struct Split {
   template <bool MULTI, bool NV = false>
   __device__ void ts_finish(int64_t g) const {
     const ChunkRef c = locate(g);
+    if constexpr (NV) {
+      nv_finish(g);
+      return;
+    }
     ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 2);
-    if constexpr (NV) fence_proxy_alias();  // the means arrived through the multicast mapping
     const int64_t len = c.e1 - c.e0;
     for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
       if (MULTI && a.slot_kind[s] != 0) continue;
