@@ -59,3 +59,22 @@ def test_two_ranks_compute_identical_schedules():
     assert np.array_equal(gathered[0], gathered[1])
     placed = np.sort(np.concatenate(locals_))
     assert np.array_equal(placed, np.arange(16))
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """bench.py --impl reference launched like the driver's N = 2 run (torchrun, two ranks, CPU):
+    rank 0 prints exactly one JSON line with impl = reference, rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--impl", "reference", "--steps", "2", "--warmup", "1"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
