@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--release-delay", type=int, default=0, help="two-shot: SESGD_OPT_RELEASE_DELAY")
     p.add_argument("--release-every", type=int, default=0, help="two-shot: SESGD_OPT_RELEASE_EVERY")
     p.add_argument("--release-stagger", type=int, default=0, help="SESGD_OPT_RELEASE_STAGGER")
+    p.add_argument("--payload-bf16", type=int, default=0, help="two-shot: bf16 reduce-scatter payload")
     p.add_argument("--path", default="auto", choices=["auto", "resident", "oneshot", "ring", "twoshot", "nvls"])
     p.add_argument("--fused", type=int, default=1, help="one-shot: one sesgd_sync_all launch per step")
     p.add_argument("--comm-batch", type=int, default=0)
@@ -257,7 +258,8 @@ def run_sesgd(args):
                                                  (C.OPT_PUSH_TMA, args.push_tma),
                                                  (C.OPT_RELEASE_DELAY, args.release_delay),
                                                  (C.OPT_RELEASE_EVERY, args.release_every),
-                                                 (C.OPT_RELEASE_STAGGER, args.release_stagger)) if v},
+                                                 (C.OPT_RELEASE_STAGGER, args.release_stagger),
+                                                 (C.OPT_PAYLOAD_BF16, args.payload_bf16)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
                             "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT, "nvls": C.PATH_NVLS}[args.path])
     r = eng.r

@@ -2,7 +2,7 @@
  * sesgd.h -- C ABI of libsesgd.so, the B200-native hot path of Shuffle-Exchange
  * SGD (SESGD, arXiv 2007.00433).
  *
- * Citations: P:n = the paper's PAPER.md line n, S:n = SPEC.md line n; R1..R20 are
+ * Citations: P:n = the paper's PAPER.md line n, S:n = SPEC.md line n; R1..R21 are
  * the readings of the paper listed in DESIGN.md ("Readings").
  *
  * What one iteration computes (Algorithm 1; Eq. 6):
@@ -123,6 +123,11 @@ extern "C" {
 #define SESGD_OPT_RELEASE_STAGGER 17 /* 1 (default): CTA i takes its flag-release steps at
                                     (k + i) mod R = 0, so the CTAs sharing an SM fence in turn;
                                     0: all at k mod R = 0 */
+#define SESGD_OPT_PAYLOAD_BF16 18  /* 1: the two-shot reduce-scatter carries bf16 (round to nearest
+                                    even) instead of fp32 -- every member's contribution, its own
+                                    included, is rounded before the fold, which and the mean stay
+                                    fp32 (R21; a lossy variant, compare with the oracle's
+                                    payload_bf16 mode); one worker per GPU, LSU pushes */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

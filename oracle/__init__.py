@@ -82,6 +82,11 @@ def lib():
         L.orc_step_wd_f32.argtypes = [i32, i32, P, i64, P, P, P, ctypes.c_float, ctypes.c_float,
                                       ctypes.c_float, i32]
         L.orc_step_wd_f32.restype = ctypes.c_int
+        L.orc_run_ext_f32.argtypes = [i32, i32, u64, i64, i64, i64, P, u64, ctypes.c_float,
+                                      ctypes.c_float, i32, i64, i32, ctypes.c_float, i32, P, P]
+        L.orc_run_ext_f32.restype = ctypes.c_int
+        L.orc_round_bf16.argtypes = [ctypes.c_float]
+        L.orc_round_bf16.restype = ctypes.c_float
         L.orc_groups_stone.argtypes = [i64, i32, i32, P, P]
         L.orc_groups_stone.restype = ctypes.c_int
         L.orc_run_local_f32.restype = ctypes.c_int
@@ -234,7 +239,7 @@ def groups_stone(t: int, n: int, m: int):
 
 
 def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0, coords=None,
-              schedule=SCHED_RANDOM, weight_decay=0.0):
+              schedule=SCHED_RANDOM, weight_decay=0.0, payload_bf16=False):
     """Local-SESGD: T iterations where the group exchange fires only when
     (t + 1) % period == 0; float32 x, v (n, S) in place.  period = 1 is `run`; m = n is
     Local-SGD."""
@@ -245,8 +250,9 @@ def run_local(n, m, seed, T, x, v, *, s_g, lr, mu, period, mode=MODE_PARAM, t0=0
         assert coords.shape == (S,)
         cp = _ptr(coords)
     assert x.dtype == np.float32 and x.flags.c_contiguous and v.flags.c_contiguous
-    _check(lib().orc_run_local_f32(n, m, seed, t0, T, S, cp, s_g, float(lr), float(mu), mode,
-                                   int(period), int(schedule), float(weight_decay), _ptr(x), _ptr(v)))
+    _check(lib().orc_run_ext_f32(n, m, seed, t0, T, S, cp, s_g, float(lr), float(mu), mode,
+                                 int(period), int(schedule), float(weight_decay), int(bool(payload_bf16)),
+                                 _ptr(x), _ptr(v)))
     return x, v
 
 
@@ -266,3 +272,8 @@ def consensus(x):
     out = np.zeros(2, np.float64)
     _check(lib().orc_consensus(x.shape[0], x.shape[1], _ptr(x), _ptr(out)))
     return float(out[0]), float(out[1])
+
+
+def round_bf16(f: float) -> float:
+    """bfloat16 round to nearest even of a binary32 value (the payload reading R21)."""
+    return float(lib().orc_round_bf16(float(f)))

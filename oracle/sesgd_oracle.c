@@ -164,7 +164,25 @@ int orc_step_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x
  * with the worker's own x */
 int orc_step_wd_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
                     const float *g, float lr, float mu, float wd, int32_t mode) {
+  return orc_step_ext_f32(n, m, canon, L, x, v, g, lr, mu, wd, 0, mode);
+}
+
+/* bfloat16 round to nearest even (the payload reading R21): keep the top 16 bits of the
+ * binary32 pattern after adding half an ulp of bf16 plus the tie-breaking bit */
+float orc_round_bf16(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return f; /* inf / nan unchanged */
+  u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+int orc_step_ext_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                     const float *g, float lr, float mu, float wd, int32_t payload_bf16, int32_t mode) {
   if (n < 1 || m < 1 || m > n || L < 0 || !canon) return ORC_EINVAL;
+  const int rnd = payload_bf16 && m > 1; /* only exchanged values are rounded */
   if (n % m != 0) return ORC_ENOTDIV;
   int32_t k = n / m;
   const float fm = (float)m;
@@ -189,7 +207,12 @@ int orc_step_wd_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float
       const int32_t *G = canon + (size_t)j * m;
       for (int64_t e = 0; e < L; ++e) {
         float s = xh[(size_t)G[0] * (size_t)L + (size_t)e];
-        for (int32_t r = 1; r < m; ++r) s = s + xh[(size_t)G[r] * (size_t)L + (size_t)e];
+        if (rnd) s = orc_round_bf16(s);
+        for (int32_t r = 1; r < m; ++r) {
+          float h = xh[(size_t)G[r] * (size_t)L + (size_t)e];
+          if (rnd) h = orc_round_bf16(h);
+          s = s + h;
+        }
         float mean = s / fm;
         for (int32_t r = 0; r < m; ++r) x[(size_t)G[r] * (size_t)L + (size_t)e] = mean;
       }
@@ -201,7 +224,12 @@ int orc_step_wd_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float
       const int32_t *G = canon + (size_t)j * m;
       for (int64_t e = 0; e < L; ++e) {
         float s = g[(size_t)G[0] * (size_t)L + (size_t)e];
-        for (int32_t r = 1; r < m; ++r) s = s + g[(size_t)G[r] * (size_t)L + (size_t)e];
+        if (rnd) s = orc_round_bf16(s);
+        for (int32_t r = 1; r < m; ++r) {
+          float h = g[(size_t)G[r] * (size_t)L + (size_t)e];
+          if (rnd) h = orc_round_bf16(h);
+          s = s + h;
+        }
         float gb = s / fm;
         for (int32_t r = 0; r < m; ++r) {
           size_t at = (size_t)G[r] * (size_t)L + (size_t)e;
@@ -402,6 +430,12 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
 int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                       const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
                       int64_t H, int32_t schedule, float wd, float *x, float *v) {
+  return orc_run_ext_f32(n, m, seed, t0, T, S, coords, s_g, lr, mu, mode, H, schedule, wd, 0, x, v);
+}
+
+int orc_run_ext_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
+                    const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode, int64_t H,
+                    int32_t schedule, float wd, int32_t payload_bf16, float *x, float *v) {
   if (n < 1 || m < 1 || m > n || t0 < 0 || T < 0 || S < 0 || H < 1) return ORC_EINVAL;
   if (schedule != 0 && schedule != 1) return ORC_EINVAL;
   if (n % m != 0) return ORC_ENOTDIV;
@@ -417,10 +451,10 @@ int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T
     if ((t + 1) % H == 0) { /* synchronisation iteration: SESGD step with the groups of t */
       rc = schedule == 1 ? orc_groups_stone(t, n, m, canon, NULL)
                          : orc_groups(seed, t, n, m, NULL, canon, NULL);
-      if (rc == ORC_OK) rc = orc_step_wd_f32(n, m, canon, S, x, v, g, lr, mu, wd, mode);
+      if (rc == ORC_OK) rc = orc_step_ext_f32(n, m, canon, S, x, v, g, lr, mu, wd, payload_bf16, mode);
     } else { /* local iteration: every worker its own singleton group */
       for (int32_t i = 0; i < n; ++i) canon[i] = i;
-      rc = orc_step_wd_f32(n, 1, canon, S, x, v, g, lr, mu, wd, mode);
+      rc = orc_step_ext_f32(n, 1, canon, S, x, v, g, lr, mu, wd, payload_bf16, mode);
     }
   }
   free(g);

@@ -8,7 +8,7 @@
  * seeded input generator, which holds none of the method's arithmetic.
  *
  * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (both under the
- * read-only reference tree); R1..R20 = readings listed in DESIGN.md.
+ * read-only reference tree); R1..R21 = readings listed in DESIGN.md.
  */
 #ifndef SESGD_ORACLE_H
 #define SESGD_ORACLE_H
@@ -62,6 +62,12 @@ int orc_step_f64(int32_t n, int32_t m, const int32_t *canon, int64_t L, double *
  * with the worker's own x. */
 int orc_step_wd_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
                     const float *g, float lr, float mu, float wd, int32_t mode);
+/* ... and the bf16-payload reading (R21): with payload_bf16 = 1 and m > 1 every contribution to
+ * a group fold (xh in PARAM, g in GRAD) is first rounded to bfloat16 (round to nearest even);
+ * the fold, the mean and the update stay binary32. */
+int orc_step_ext_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, float *x, float *v,
+                     const float *g, float lr, float mu, float wd, int32_t payload_bf16, int32_t mode);
+float orc_round_bf16(float f);
 
 /* The same iteration with the group mean computed by the paper's Ring-AllReduce (Sec. 2.2,
  * P:99-104) in ring order: members in ascending id form the ring; element e lies in slice
@@ -95,6 +101,10 @@ int orc_run_f64(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int6
 int orc_run_local_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
                       const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode,
                       int64_t H, int32_t schedule, float wd, float *x, float *v);
+
+int orc_run_ext_f32(int32_t n, int32_t m, uint64_t seed, int64_t t0, int64_t T, int64_t S,
+                    const int64_t *coords, uint64_t s_g, float lr, float mu, int32_t mode, int64_t H,
+                    int32_t schedule, float wd, int32_t payload_bf16, float *x, float *v);
 
 /* NEXT-3, alternative reading of R1 (Stone's perfect shuffle): n = 2^d, m = 2^p; at
  * iteration t worker i's group is every worker equal to i outside index dimensions

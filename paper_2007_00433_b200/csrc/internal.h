@@ -78,6 +78,7 @@ struct P2PArgs {
   const float *const *bg;
   char *ws[SESGD_MAX_RANKS];        // every rank's workspace, mapped here
   char *mc_ws;                      // NVLS: multicast mapping of the workspaces (nullptr: none)
+  int payload_bf16;                 // two-shot reduce-scatter values as bf16 (SESGD_OPT_PAYLOAD_BF16)
   int64_t g0, g1;                   // global chunk range of this launch
   int64_t total_chunks;             // chunks of all buckets (flag array stride)
   int64_t region_floats;            // floats of one stage / receive region (all buckets)
@@ -183,6 +184,7 @@ struct sesgd_ctx {
   int release_stagger = 1;  // SESGD_OPT_RELEASE_STAGGER
   int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
   char *mc_ws = nullptr;    // sesgd_attach_multicast (SESGD_PATH_NVLS)
+  int payload_bf16 = 0;     // SESGD_OPT_PAYLOAD_BF16
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)

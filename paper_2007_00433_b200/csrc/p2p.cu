@@ -48,6 +48,8 @@
 // point to a strictly smaller chunk (or an earlier step of the same chunk), so the
 // smallest unfinished step can always progress: no deadlock.  Flags are never reset.
 // Every spin has a %globaltimer timeout that latches SESGD_ETIMEOUT.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -150,6 +152,38 @@ __device__ __forceinline__ void mm_st1(float *mc, float r) {
 }
 // the same memory is accessed through the multicast and the unicast mappings
 __device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
+// bf16 payload (SESGD_OPT_PAYLOAD_BF16): a slice's reduce-scatter values travel as bf16, packed in
+// the first half of that slice's own float range, so they never overlap the fp32 all-gather data
+// that other slices receive in the same slot.  Round to nearest even, as __float2bfloat16_rn.
+template <int W>
+__device__ __forceinline__ void st_bf(__nv_bfloat16 *p, const float (&r)[W], int nvalid) {
+  if constexpr (W == 4) {
+    if (nvalid == 4) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(r[0], r[1]), hi = __floats2bfloat162_rn(r[2], r[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<unsigned int *>(&lo);
+      u.y = *reinterpret_cast<unsigned int *>(&hi);
+      *reinterpret_cast<uint2 *>(p) = u;
+      return;
+    }
+  }
+  for (int q = 0; q < W; ++q)
+    if (q < nvalid) p[q] = __float2bfloat16_rn(r[q]);
+}
+template <int W>
+__device__ __forceinline__ void ld_bf(const __nv_bfloat16 *p, float (&r)[W], int nvalid) {
+  if constexpr (W == 4) {
+    if (nvalid == 4) {
+      const uint2 u = __ldcg(reinterpret_cast<const uint2 *>(p));
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+      r[0] = a.x; r[1] = a.y; r[2] = b.x; r[3] = b.y;
+      return;
+    }
+  }
+  for (int q = 0; q < W; ++q) r[q] = (q < nvalid) ? __bfloat162float(p[q]) : 0.f;
+}
 
 __device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -1007,7 +1041,7 @@ struct Split {
     __syncthreads();
   }
 
-  template <bool TMA, bool MULTI, bool NV = false>
+  template <bool TMA, bool MULTI, bool NV = false, bool BF = false>
   __device__ void ts_rs_stage(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     const int S = ts_slice();
@@ -1050,6 +1084,12 @@ struct Split {
         }
         const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
         const int w = G[j];
+        if constexpr (BF) {  // one worker per GPU: own slice -> own stage, others -> their slot
+          const int64_t lo = ts_lo(j, len);
+          float *base = ((j == p) ? stage(0) : recv(w, p)) + c.soff + c.e0 + lo;
+          st_bf<W>(reinterpret_cast<__nv_bfloat16 *>(base) + (o - lo), val, nv);
+          continue;
+        }
         if (NV || !rem<MULTI>(w)) {  // NVLS: every owner reduces my stage through the switch
           st_slot<W>(stage(s) + c.soff + e, val, nv);  // read in place by the local owner
         } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
@@ -1116,7 +1156,7 @@ struct Split {
     __syncthreads();
   }
 
-  template <bool TMA, bool MULTI, bool NV = false>
+  template <bool TMA, bool MULTI, bool NV = false, bool BF = false>
   __device__ void ts_reduce(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     if (TMA && threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();  // entry free (+ sync below)
@@ -1140,7 +1180,10 @@ struct Split {
           const int w = G[rr];
           const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
           float y[W];
-          ld_slot<W>(src + c.soff + e, y, nv);
+          if constexpr (BF)
+            ld_bf<W>(reinterpret_cast<const __nv_bfloat16 *>(src + c.soff + c.e0 + lo) + (o - lo), y, nv);
+          else
+            ld_slot<W>(src + c.soff + e, y, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? y[q] : __fadd_rn(acc[q], y[q]);
         }
@@ -1261,7 +1304,7 @@ struct Split {
   // last step may still be in flight).  A chunk pushed at step s is released by step
   // s + D + R - 1, so with reduce L >= D + R - 1 steps after rs_stage (and finish L after
   // reduce) every wait targets a flag released at the top of this step or an earlier one.
-  template <bool TMA, bool MULTI, bool NV = false>
+  template <bool TMA, bool MULTI, bool NV = false, bool BF = false>
   __device__ void compute_twoshot(int i, float *ring) const {
     const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
     const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
@@ -1305,7 +1348,7 @@ struct Split {
         t0 = t1;
       }
       if (k < nk) {
-        ts_rs_stage<TMA, MULTI, NV>(first + k * gc, ring + (q % kPushRing) * kChunk);
+        ts_rs_stage<TMA, MULTI, NV, BF>(first + k * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1314,7 +1357,7 @@ struct Split {
         t0 = t1;
       }
       if (k >= L && k - L < nk) {
-        ts_reduce<TMA, MULTI, NV>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
+        ts_reduce<TMA, MULTI, NV, BF>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1395,14 +1438,14 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
     p.compute_direct(blockIdx.x);
 }
 
-template <int W, bool GRAD, bool TMA, bool MULTI, bool NV = false>
+template <int W, bool GRAD, bool TMA, bool MULTI, bool NV = false, bool BF = false>
 __global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];  // TMA: kPushRing chunk images
   const Split<W, GRAD> p(a);
   if (a.m == 1)
     p.local_only();
   else
-    p.template compute_twoshot<TMA, MULTI, NV>(blockIdx.x, reinterpret_cast<float *>(dsmem));
+    p.template compute_twoshot<TMA, MULTI, NV, BF>(blockIdx.x, reinterpret_cast<float *>(dsmem));
 }
 
 constexpr size_t kTwoshotTmaSmem = size_t(Split<4, false>::kPushRing) * size_t(kChunk) * 4;  // 48 KiB
@@ -1424,6 +1467,15 @@ const void *pick_nvls(int mode, bool vec) {
                 : reinterpret_cast<const void *>(&k4_twoshot<4, false, false, false, true>);
   return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, false, true>)
               : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, false, true>);
+}
+// bf16 payload: one worker per GPU, LSU pushes
+const void *pick_bf16(int mode, bool vec) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (vec)
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, false, false, false, true>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false, false, false, false, true>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, false, false, true>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, false, false, true>);
 }
 // TMA pushes: one worker per GPU only; several workers per GPU: the MULTI kernel
 const void *pick_twoshot(int mode, bool vec, bool tma, bool multi) {
@@ -1499,7 +1551,8 @@ int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
 }
 
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream) {
-  const void *k = a.mc_ws ? pick_nvls(mode, vec) : pick_twoshot(mode, vec, tma, a.r > 1);
+  const void *k = a.mc_ws ? pick_nvls(mode, vec)
+                 : a.payload_bf16 ? pick_bf16(mode, vec) : pick_twoshot(mode, vec, tma, a.r > 1);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};

@@ -342,6 +342,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.bg = ctx->d_bg;
   for (int r = 0; r < ctx->n_ranks; ++r) a.ws[r] = ctx->ws[r];
   a.mc_ws = nvls ? ctx->mc_ws : nullptr;
+  a.payload_bf16 = (twoshot && !nvls) ? ctx->payload_bf16 : 0;
   if (bucket >= 0) {
     a.g0 = ref.chunk_base;
     a.g1 = ref.chunk_base + ref.nchunks;
@@ -587,6 +588,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
     case SESGD_OPT_RELEASE_STAGGER:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "release stagger must be 0 or 1");
       ctx->release_stagger = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_PAYLOAD_BF16:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "bf16 payload must be 0 or 1");
+      ctx->payload_bf16 = int(value);
       return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");
@@ -893,6 +898,8 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
   if (path == SESGD_PATH_TWOSHOT && (ctx->p2p_variant != 0 || (ctx->push_tma && ctx->n_local != 1)))
     return fail(ctx, SESGD_ENOTSUP, "two-shot needs the DIRECT layout; its TMA pushes one worker per GPU");
+  if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->n_local != 1 || ctx->push_tma))
+    return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path, one worker per GPU, LSU pushes");
   if (path == SESGD_PATH_NVLS && (ctx->p2p_variant != 0 || ctx->n_local != 1 || ctx->m != ctx->n || !ctx->mc_ws))
     return fail(ctx, SESGD_ENOTSUP,
                 "the NVLS path needs one worker per GPU, group_size = n and sesgd_attach_multicast");
@@ -966,6 +973,8 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     }
     return SESGD_OK;
   }
+  if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->n_local != 1 || ctx->push_tma))
+    return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path, one worker per GPU, LSU pushes");
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
   return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot, nvls);
 }

@@ -37,6 +37,7 @@ def main():
     p.add_argument("--schedule", type=int, default=0)
     p.add_argument("--consensus", type=int, default=0)
     p.add_argument("--wd", type=float, default=0.0)
+    p.add_argument("--bf16", type=int, default=0)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -52,7 +53,8 @@ def main():
                       options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
                                                    (C.OPT_PUSH_TMA, a.tma),
                                                    (C.OPT_LOCAL_PERIOD, a.period),
-                                                   (C.OPT_SCHEDULE, a.schedule)) if v})
+                                                   (C.OPT_SCHEDULE, a.schedule),
+                                                   (C.OPT_PAYLOAD_BF16, a.bf16)) if v})
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):

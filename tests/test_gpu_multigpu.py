@@ -29,7 +29,8 @@ def _free_port():
 
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
-            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0):
+            lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
+            bf16=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
@@ -42,6 +43,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
+               "--bf16", str(bf16),
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -353,3 +355,17 @@ def test_four_gpus_nvls(tmp_path, mode):
     np.testing.assert_allclose(X, x, rtol=1e-5, atol=1e-7)
     np.testing.assert_allclose(V, v, rtol=1e-5, atol=1e-7)
     assert all(np.array_equal(X[0], X[i]) for i in range(4))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_two_gpus_bf16_payload(tmp_path, mode):
+    """NEXT-4: the two-shot reduce-scatter in bf16 (SESGD_OPT_PAYLOAD_BF16): the bits of the oracle's
+    payload_bf16 reading (R21), over several iterations and ragged buckets."""
+    buckets = [100003, 7, 4096]
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, mode, path=4, bf16=1)
+    x = np.tile(synth.x0_host(sum(buckets)), (2, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(2, 2, 42, 5, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     payload_bf16=True)
+    _compare(X, x)
+    _compare(V, v)

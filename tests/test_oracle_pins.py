@@ -745,3 +745,51 @@ def test_weight_decay_group_n_is_ring_sgd_with_decay():
     ref = _torch_sgd_wd(synth.x0_host(L).astype(np.float64), gbars, 0.1, 0.9, wd)
     assert all(np.array_equal(x[0], x[i]) for i in range(n))
     np.testing.assert_allclose(x[0], ref, rtol=0, atol=2e-7)
+
+
+# ---------------------------------------------------------------- NEXT-4: bf16 payload (R21)
+def test_round_bf16_matches_torch():
+    """The oracle's bf16 rounding equals torch's float32 -> bfloat16 conversion (round to nearest
+    even) on random values, exact ties and extremes."""
+    rng = np.random.default_rng(4)
+    vals = np.concatenate([rng.standard_normal(5000).astype(np.float32),
+                           (rng.integers(1, 1 << 20, 2000) * 2.0 ** -20 + 1).astype(np.float32),
+                           np.float32([1 + 2 ** -8, 1 + 3 * 2 ** -8, -(1 + 2 ** -8), 0.0, -0.0, 3.4e38,
+                                       1e-40, 65504.0])])
+    want = torch.from_numpy(vals).to(torch.bfloat16).to(torch.float32).numpy()
+    got = np.array([oracle.round_bf16(float(v)) for v in vals], np.float32)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+def test_bf16_payload_step_definition(mode):
+    """R21 on one iteration, n = 4, m = 2: every exchanged contribution is rounded to bf16 before the
+    fold (torch's conversion as the independent reference), the fold / mean / update stay fp32;
+    with m = 1 nothing is exchanged and the payload changes nothing."""
+    n, m, L = 4, 2, 257
+    x0 = np.tile(synth.x0_host(L), (n, 1))
+    g = np.stack([synth.grad_host(i, 0, L) for i in range(n)]).astype(np.float32)
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float32).numpy()  # noqa: E731
+    x = x0.copy()
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, SEED, 1, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     payload_bf16=True)
+    groups = oracle.canonical_groups(SEED, 0, n, m)
+    f = np.float32
+    for a, b in groups:
+        if mode == oracle.MODE_PARAM:
+            va, vb = g[a], g[b]  # v0 = 0: v = 0.9 * 0 + g
+            xa, xb = x0[a] - f(0.1) * va, x0[b] - f(0.1) * vb
+            want = (bf(xa) + bf(xb)) / f(2)
+            assert np.array_equal(x[a], want) and np.array_equal(x[b], want)
+        else:
+            gb = (bf(g[a]) + bf(g[b])) / f(2)
+            assert np.array_equal(v[a], gb) and np.array_equal(x[a], x0[a] - f(0.1) * gb)
+    y = x0.copy()
+    w = np.zeros_like(y)
+    oracle.run_local(n, 1, SEED, 1, y, w, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     payload_bf16=True)
+    z = x0.copy()
+    u = np.zeros_like(z)
+    oracle.run_local(n, 1, SEED, 1, z, u, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode)
+    assert np.array_equal(y, z)
