@@ -72,8 +72,8 @@ extern "C" {
                                  in place); a remote member pair exchanges 2/m of a bucket instead of
                                  one-shot's full copy; needs P2P variant 0 (else SESGD_ENOTSUP) */
 #define SESGD_PATH_NVLS 5     /* NVLink SHARP, for group_size = n (Ring-SGD's single group) with one
-                                 worker per GPU: the slice owner reduces every GPU's stage inside
-                                 the NVSwitch (multimem.ld_reduce) and multicasts the mean
+                                 worker per GPU: chunk g's owner (member g mod n) reduces every GPU's
+                                 stage of it inside the NVSwitch (multimem.ld_reduce) and multicasts the mean
                                  (multimem.st); needs sesgd_attach_multicast.  The switch's
                                  summation order is unspecified: parity within the north-star
                                  tolerance, bit-exact only for n = 2 (a + b = b + a) */
