@@ -1110,7 +1110,7 @@ struct Split {
   // fence per batch (a fence waits for the SM's outstanding remote stores: measured ~8 us per
   // chunk step under load), then relaxed flag stores spread over warp 0's lanes.  TMA (r == 1):
   // the `newer` most recent bulk groups may still be in flight, every older one must have landed.
-  template <bool TMA, bool MULTI>
+  template <bool TMA, bool MULTI, bool NV = false>
   __device__ __forceinline__ void ts_release(int64_t first, int64_t rs0, int64_t rs1, int64_t ag0,
                                              int64_t ag1, int newer) const {
     if (threadIdx.x >= 32 || (rs1 <= rs0 && ag1 <= ag0)) return;
@@ -1124,7 +1124,7 @@ struct Split {
       }
       __syncwarp();
     }
-    if (a.mc_ws) fence_proxy_alias();  // NVLS: multicast stores before the unicast flags
+    if constexpr (NV) fence_proxy_alias();  // NVLS: multicast stores before the unicast flags
     dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
     const int64_t nrs = (rs1 - rs0) * pairs, nall = nrs + (ag1 - ag0) * pairs;
     for (int64_t q = threadIdx.x; q < nall; q += 32) {
@@ -1133,7 +1133,7 @@ struct Split {
       const int64_t c = (kind == 0 ? rs0 : ag0) + qq / pairs;
       const int pr = int(qq % pairs), s = pr / a.m, j = pr % a.m;
       if ((MULTI && a.slot_kind[s] != 0) || j == a.my_pos[s]) continue;
-      if (a.mc_ws) {  // NVLS: staged -> the chunk's owner only; AG flags only from the owner
+      if constexpr (NV) {  // NVLS: staged -> the chunk's owner only; AG flags only from the owner
         const int own = int((first + c * gc) % a.m);
         if (kind == 0 ? (j != own) : (a.my_pos[s] != own)) continue;
       }
@@ -1338,7 +1338,7 @@ struct Split {
         int newer = 0;
         if constexpr (TMA)
           for (int64_t s2 = k - D + 1; s2 < k; ++s2) newer += groups_of(s2);
-        ts_release<TMA, MULTI>(first, rs_out, rs1, ag_out, ag1, newer);
+        ts_release<TMA, MULTI, NV>(first, rs_out, rs1, ag_out, ag1, newer);
         rs_out = rs1;
         ag_out = ag1;
       }
