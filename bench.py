@@ -139,6 +139,24 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def nvlink_algo_bytes(perm, m, r, world, L):
+    """Algorithmic NVLink bytes of one iteration, per GPU per direction, max over GPUs.
+
+    SURVEY.md Sec. 8(d) d2: a group spanning s GPUs costs each of them the bandwidth-optimal
+    group-allreduce bound 2(s-1)/s * 4 B per element (co-resident members pre-combine; s = 1
+    costs nothing).  perm = the iteration's canonical slots (group j = perm[j*m:(j+1)*m]),
+    worker i lives on GPU i // r (r workers per GPU), L = elements per worker.
+    """
+    n = len(perm)
+    per_gpu = [0.0] * world
+    for j in range(n // m):
+        ranks = {int(w) // r for w in perm[j * m:(j + 1) * m]}
+        s_span = len(ranks)
+        for rk in ranks:
+            per_gpu[rk] += 2 * (s_span - 1) / s_span * 4 * L
+    return max(per_gpu)
+
+
 def cfg_label(workload, n, m):
     """BASELINE.json config the run corresponds to (configs[1] = cfg2, configs[2] = cfg3)."""
     if workload == "resnet50" and n == 8 and m == 2:
@@ -344,17 +362,8 @@ def run_sesgd(args):
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
         # of them 2(s-1)/s * 4 B per element (co-resident members pre-combine); max over
         # GPUs, mean over the timed iterations.
-        worker_rank = [i // r for i in range(n)]
-        nvl_steps = []
-        for t in range(t_next - K, t_next):
-            perm, _ = eng.groups(t)
-            per_gpu_b = [0.0] * world
-            for j in range(n // m):
-                ranks = {worker_rank[int(w)] for w in perm[j * m:(j + 1) * m]}
-                s_span = len(ranks)
-                for rk in ranks:
-                    per_gpu_b[rk] += 2 * (s_span - 1) / s_span * 4 * L
-            nvl_steps.append(max(per_gpu_b))
+        nvl_steps = [nvlink_algo_bytes(eng.groups(t)[0], m, r, world, L)
+                     for t in range(t_next - K, t_next)]
         nvl_bytes = sum(nvl_steps) / len(nvl_steps)
         achieved_nvl = nvl_bytes * K / (kern_ms_total * 1e-3) / 1e9
         achieved_hbm = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9

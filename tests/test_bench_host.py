@@ -1,0 +1,73 @@
+"""CPU tests of bench.py's host-side roofline arithmetic (no GPU, no library).
+
+`nvlink_algo_bytes` is the NVLink term of the roofline bench.py reports for N > 1 (SURVEY.md
+Sec. 8(d) d2: a group spanning s GPUs costs each of them 2(s-1)/s * 4 B per element).  Pinned
+here to closed forms (two-GPU pair = NCCL's allreduce busbw bytes, full ring over 8 GPUs,
+groups resident on one GPU) and to a brute-force recount.
+"""
+import itertools
+import random
+
+import pytest
+
+import bench
+
+
+def test_pair_across_two_gpus_is_one_copy():
+    # n = 2, m = 2, one worker per GPU: each GPU sends (and receives) half the bucket twice.
+    assert bench.nvlink_algo_bytes([0, 1], 2, 1, 2, 1000) == 4 * 1000
+
+
+def test_full_ring_over_eight_gpus():
+    # m = n = 8, one worker per GPU: the ring allreduce bound 2 * 7/8 * 4 B per element.
+    assert bench.nvlink_algo_bytes(list(range(8)), 8, 1, 8, 1 << 20) == pytest.approx(7 * (1 << 20))
+
+
+def test_groups_on_one_gpu_cost_nothing():
+    # 8 workers resident on one GPU, or each group's members co-resident on one of 4 GPUs.
+    assert bench.nvlink_algo_bytes(list(range(8)), 2, 8, 1, 123) == 0.0
+    assert bench.nvlink_algo_bytes([0, 1, 2, 3, 4, 5, 6, 7], 2, 2, 4, 123) == 0.0
+
+
+def test_max_over_gpus():
+    # n = 8, m = 2, 2 workers per GPU (4 GPUs): groups {0,2} {1,3} span GPUs 0-1, {4,5} {6,7}
+    # are co-resident.  GPUs 0 and 1 each carry two spanning groups: 2 * 4 B * L.
+    assert bench.nvlink_algo_bytes([0, 2, 1, 3, 4, 5, 6, 7], 2, 2, 4, 10) == 2 * 4 * 10
+
+
+def _brute(perm, m, r, world, L):
+    # Recount per GPU: for every GPU, every group that has a member there and s distinct GPUs.
+    best = 0.0
+    for g in range(world):
+        tot = 0.0
+        for j in range(len(perm) // m):
+            gpus = sorted({w // r for w in perm[j * m:(j + 1) * m]})
+            if g in gpus:
+                tot += (len(gpus) - 1) * 8 * L / len(gpus)
+        best = max(best, tot)
+    return best
+
+
+@pytest.mark.parametrize("n,m,world", [(8, 2, 2), (8, 4, 4), (16, 4, 8), (16, 8, 4), (4, 2, 4)])
+def test_matches_brute_force_recount(n, m, world):
+    rng = random.Random(n * 100 + m * 10 + world)
+    r = n // world
+    for _ in range(200):
+        perm = list(range(n))
+        rng.shuffle(perm)
+        assert bench.nvlink_algo_bytes(perm, m, r, world, 77) == pytest.approx(_brute(perm, m, r, world, 77))
+
+
+def test_span_distribution_config3():
+    # n = 16, m = 4, 2 workers per GPU on 8 GPUs.  Over all 4-subsets
+    # a group spans 4 GPUs with probability C(8,4)*2^4 / C(16,4) = 1120/1820 and 2 GPUs with
+    # C(8,2)/C(16,4) = 28/1820; the per-GPU cost of one group is then 6 B or 4 B per element.
+    spans = {}
+    for grp in itertools.combinations(range(16), 4):
+        s = len({w // 2 for w in grp})
+        spans[s] = spans.get(s, 0) + 1
+    assert spans == {4: 1120, 3: 672, 2: 28}
+    # Groups {0,2,4,6} and {1,3,5,7} both span GPUs 0-3 (6 B each there); {8..11}, {12..15}
+    # span two GPUs each (4 B): the max is GPU 0..3's 12 B per element.
+    assert bench.nvlink_algo_bytes([0, 2, 4, 6] + list(range(8, 16)) + [1, 3, 5, 7], 4, 2, 8, 1) == \
+        pytest.approx(12.0)
