@@ -31,6 +31,7 @@ METRIC = "group sync+update GB/s per GPU & iters/s at 1/2/4/8 B200 (fraction of 
 N_WORKERS, GROUP_SIZE, LR, MU, SEED = 8, 2, 0.1, 0.9, 42
 BYTES_PER_WORKER_ELEM = 20  # algorithmic HBM bytes: read g, v, x; write v, x (fp32)
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md), nominal 900
+TAU_HOP_S = 2.6e-6          # measured one-way flag hop (K7 ping-pong, profiles/r01_latency_sweep_4gpu_v2.json)
 PAPER_CONTEXT = {"speedup_16w_0.1ms": 1.7, "speedup_16w_5ms": 5.0,
                  "source": "PAPER.md:7, P:411, P:436 (K80 + 1 Gbps Ethernet; end-to-end training, not this metric)"}
 
@@ -409,7 +410,7 @@ def run_sesgd(args):
     stats = [eng.stats(b) for b in range(nb)]
     # consistency of the workers' parameters after the run (K9), outside the timed region
     css, cmx = eng.consensus(stream)
-    lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, 1.5e-6)
+    lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, TAU_HOP_S)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gbs, sample, _ = cpu_oracle_rate(n, m, args.cpu_seconds, args.mode, L, args.workload)
@@ -444,7 +445,7 @@ def run_sesgd(args):
             "handshakes": {
                 "sesgd_per_tensor": lat["sesgd_handshakes"], "ring_per_tensor": lat["ring_handshakes"],
                 "kernel_rounds_per_bucket": stats[0]["handshake_rounds"],
-                "model": "Eq.2/Eq.3 exact (sesgd_latency_model), nu=770 GB/s, tau=1.5 us (assumed until K7 probe)",
+                "model": "Eq.2/Eq.3 exact (sesgd_latency_model), nu=770 GB/s, tau=2.6 us (K7 flag ping-pong, profiles/r01_latency_sweep_4gpu_v2.json)",
                 "model_ratio": lat["ratio"],
             },
             "paper_context": PAPER_CONTEXT,
