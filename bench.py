@@ -338,6 +338,10 @@ def run_sesgd(args):
     ms_step = ms_total / K
     launch_ms = [[e0.elapsed_time(e1) for (e0, e1) in ev[k]] for k in range(K)]
     kern_ms_total = max_over_ranks(sum(map(sum, launch_ms)))
+    # per-step kernel time distribution (median and p90), max over ranks
+    step_ms = sorted(sum(row) for row in launch_ms)
+    kern_p50 = max_over_ranks(step_ms[(K - 1) // 2])
+    kern_p90 = max_over_ranks(step_ms[min(K - 1, int(0.9 * K))])
     total_bytes = BYTES_PER_WORKER_ELEM * L * n  # whole job, per step
     value = total_bytes / (ms_step * 1e-3) / 1e9
     per_gpu = value / world
@@ -437,6 +441,7 @@ def run_sesgd(args):
             },
             "iters_per_s": 1e3 / ms_step,
             "gbs_per_gpu": per_gpu,
+            "kernel_ms_per_step": {"p50": kern_p50, "p90": kern_p90},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
