@@ -243,6 +243,33 @@ def test_averaging_matrix_doubly_stochastic():
             np.testing.assert_allclose(x, W @ X, rtol=1e-14, atol=1e-15)
 
 
+@pytest.mark.parametrize("mode", [oracle.MODE_PARAM, oracle.MODE_GRAD])
+@pytest.mark.parametrize("n,m", [(4, 2), (8, 4), (6, 3)])
+def test_dense_matrix_form_with_momentum(n, m, mode):
+    """P12 with lr, momentum != 0: the group-loop oracle equals Algorithm 1 written as dense
+    n x n products over T iterations, distinct x_0 and prior momentum.
+    PARAM (Eq. 6, R8): V <- mu V + G ; X <- W_t (X - lr V)   (momentum stays local).
+    GRAD  (Eq. 5, R8): V <- mu V + W_t G ; X <- X - lr V."""
+    rng = np.random.default_rng(n * 10 + m + mode)
+    L, lr, mu = 5, 0.1, 0.9
+    X = rng.standard_normal((n, L))
+    V = rng.standard_normal((n, L))
+    x, v = X.copy(), V.copy()
+    for t in range(12):
+        G = rng.standard_normal((n, L))
+        W = _W(n, m, t)
+        if mode == oracle.MODE_PARAM:
+            V = mu * V + G
+            X = W @ (X - lr * V)
+        else:
+            V = mu * V + W @ G
+            X = X - lr * V
+        _, canon, _ = oracle.groups(SEED, t, n, m)
+        oracle.step(n, m, canon, x, v, G.copy(), lr, mu, mode)
+        np.testing.assert_allclose(v, V, rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(x, X, rtol=1e-12, atol=1e-13)
+
+
 def test_hand_step(golden_dir):
     """Hand-executed single step at n=4 (Eq. 6 and Eq. 5 variants), exact dyadic values."""
     d = json.load(open(os.path.join(golden_dir, "hand_step_n4.json")))
