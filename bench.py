@@ -140,6 +140,12 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def pcie_probe():
+    """Measured pinned-host copy rates (tools/pcie_probe.py) committed under profiles/, or None."""
+    path = os.path.join(ROOT, "profiles", "r01_pcie_probe_g1.json")
+    return json.load(open(path)) if os.path.exists(path) else None
+
+
 def nvlink_algo_bytes(perm, m, r, world, L):
     """Algorithmic NVLink bytes of one iteration, per GPU per direction, max over GPUs.
 
@@ -409,6 +415,13 @@ def run_sesgd(args):
                "ms_per_step": e2e_ms, "steps": args.e2e_steps,
                "api": "sesgd_sync_all_host (pinned host g in, updated x out, every worker; H2D / "
                       "kernels / D2H of different buckets pipelined on copy streams)"}
+        probe = pcie_probe()
+        if probe is not None:  # the e2e step against its own bound: both copy directions at once
+            bound_ms = 4 * L * r / (probe["both_gbs_per_dir"] * 1e6)
+            e2e["pcie_bound"] = {"ms_per_step": bound_ms, "frac": bound_ms / e2e_ms,
+                                 "gbs_per_dir": probe["both_gbs_per_dir"],
+                                 "source": "tools/pcie_probe.py, profiles/r01_pcie_probe_g1.json "
+                                           "(pinned H2D and D2H of the same bytes concurrently)"}
     eng.poll()
 
     stats = [eng.stats(b) for b in range(nb)]
