@@ -125,7 +125,7 @@ extern "C" {
                                     0: all at k mod R = 0 */
 #define SESGD_OPT_PAYLOAD_BF16 18  /* 1: the two-shot reduce-scatter carries bf16 (round to nearest
                                     even) instead of fp32 -- every member's contribution, its own
-                                    included, is rounded before the fold, which and the mean stay
+                                    included, is rounded before the fold; the fold and the mean stay
                                     fp32 (R21; a lossy variant, compare with the oracle's
                                     payload_bf16 mode); one worker per GPU, LSU pushes */
 
