@@ -127,7 +127,8 @@ extern "C" {
                                     even) instead of fp32 -- every member's contribution, its own
                                     included, is rounded before the fold; the fold and the mean stay
                                     fp32 (R21; a lossy variant, compare with the oracle's
-                                    payload_bf16 mode); one worker per GPU, LSU pushes */
+                                    payload_bf16 mode; all-local groups round too); one or
+                                    several workers per GPU, LSU pushes */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

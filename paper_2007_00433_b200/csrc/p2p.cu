@@ -655,6 +655,9 @@ struct Split {
 
   // A group whose members all live on this GPU: the whole update in registers, like the
   // 1-GPU kernel (no stage, no flags, no fold); run once, by the group's first member.
+  // BF (bf16 payload, R21): every contribution to the fold is rounded to bf16 first, as if it
+  // had crossed NVLink, so all-local groups give the bits of the oracle's payload_bf16 reading.
+  template <bool BF = false>
   __device__ void local_group_update(const ChunkRef &c, const int8_t *G) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
@@ -673,13 +676,17 @@ struct Split {
 #pragma unroll
           for (int q = 0; q < W; ++q) {
             v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
-            const float xh = dev::sgd(x[q], a.lr, v[q]);
+            float xh = dev::sgd(x[q], a.lr, v[q]);
+            if constexpr (BF) xh = __bfloat162float(__float2bfloat16_rn(xh));
             acc[q] = (rr == 0) ? xh : __fadd_rn(acc[q], xh);
           }
           store_m<W>(a.bv[c.b * a.r + sl] + e, v, nv);
         } else {
 #pragma unroll
-          for (int q = 0; q < W; ++q) acc[q] = (rr == 0) ? gr[q] : __fadd_rn(acc[q], gr[q]);
+          for (int q = 0; q < W; ++q) {
+            if constexpr (BF) gr[q] = __bfloat162float(__float2bfloat16_rn(gr[q]));
+            acc[q] = (rr == 0) ? gr[q] : __fadd_rn(acc[q], gr[q]);
+          }
         }
       }
 #pragma unroll
@@ -1054,7 +1061,7 @@ struct Split {
       if (MULTI && a.slot_kind[s] == 2) continue;  // done by its group's first member
       const int8_t *G = group(a.my_workers[s]);
       if (MULTI && a.slot_kind[s] == 1) {
-        local_group_update(c, G);
+        local_group_update<BF>(c, G);
         continue;
       }
       const int p = a.my_pos[s];
@@ -1084,9 +1091,9 @@ struct Split {
         }
         const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
         const int w = G[j];
-        if constexpr (BF) {  // one worker per GPU: own slice -> own stage, others -> their slot
+        if constexpr (BF) {  // packed at the owner's slice: local owner -> my stage, remote -> its slot
           const int64_t lo = ts_lo(j, len);
-          float *base = ((j == p) ? stage(0) : recv(w, p)) + c.soff + c.e0 + lo;
+          float *base = (rem<MULTI>(w) ? recv(w, p) : stage(s)) + c.soff + c.e0 + lo;
           st_bf<W>(reinterpret_cast<__nv_bfloat16 *>(base) + (o - lo), val, nv);
           continue;
         }
@@ -1468,14 +1475,18 @@ const void *pick_nvls(int mode, bool vec) {
   return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, false, true>)
               : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, false, true>);
 }
-// bf16 payload: one worker per GPU, LSU pushes
-const void *pick_bf16(int mode, bool vec) {
+// bf16 payload: LSU pushes, one or several workers per GPU
+template <bool MULTI>
+const void *pick_bf16_t(int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
   if (vec)
-    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, false, false, false, true>)
-                : reinterpret_cast<const void *>(&k4_twoshot<4, false, false, false, false, true>);
-  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, false, false, true>)
-              : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, false, false, true>);
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, false, MULTI, false, true>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false, false, MULTI, false, true>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, MULTI, false, true>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, MULTI, false, true>);
+}
+const void *pick_bf16(int mode, bool vec, bool multi) {
+  return multi ? pick_bf16_t<true>(mode, vec) : pick_bf16_t<false>(mode, vec);
 }
 // TMA pushes: one worker per GPU only; several workers per GPU: the MULTI kernel
 const void *pick_twoshot(int mode, bool vec, bool tma, bool multi) {
@@ -1552,7 +1563,7 @@ int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
 
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream) {
   const void *k = a.mc_ws ? pick_nvls(mode, vec)
-                 : a.payload_bf16 ? pick_bf16(mode, vec) : pick_twoshot(mode, vec, tma, a.r > 1);
+                 : a.payload_bf16 ? pick_bf16(mode, vec, a.r > 1) : pick_twoshot(mode, vec, tma, a.r > 1);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};

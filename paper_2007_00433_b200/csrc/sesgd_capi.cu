@@ -898,8 +898,8 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
   if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first (multi-GPU path)");
   if (path == SESGD_PATH_TWOSHOT && (ctx->p2p_variant != 0 || (ctx->push_tma && ctx->n_local != 1)))
     return fail(ctx, SESGD_ENOTSUP, "two-shot needs the DIRECT layout; its TMA pushes one worker per GPU");
-  if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->n_local != 1 || ctx->push_tma))
-    return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path, one worker per GPU, LSU pushes");
+  if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma))
+    return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path with LSU pushes");
   if (path == SESGD_PATH_NVLS && (ctx->p2p_variant != 0 || ctx->n_local != 1 || ctx->m != ctx->n || !ctx->mc_ws))
     return fail(ctx, SESGD_ENOTSUP,
                 "the NVLS path needs one worker per GPU, group_size = n and sesgd_attach_multicast");
@@ -973,8 +973,8 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     }
     return SESGD_OK;
   }
-  if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->n_local != 1 || ctx->push_tma))
-    return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path, one worker per GPU, LSU pushes");
+  if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma))
+    return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path with LSU pushes");
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
   return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot, nvls);
 }

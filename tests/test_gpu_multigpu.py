@@ -369,3 +369,18 @@ def test_two_gpus_bf16_payload(tmp_path, mode):
                      payload_bf16=True)
     _compare(X, x)
     _compare(V, v)
+
+
+@pytest.mark.parametrize("n,m,mode", [(4, 2, 0), (8, 4, 1), (8, 2, 0)])
+def test_two_gpus_bf16_payload_several_workers_per_gpu(tmp_path, n, m, mode):
+    """NEXT-4: bf16 payload with n/2 workers per GPU (MULTI kernel): co-resident contributions are
+    packed in the contributor's stage, remote ones in the owner's slot, all-local groups round in
+    registers -- every fold equals the oracle's payload_bf16 reading (R21) bit for bit."""
+    buckets = [100003, 7, 4096]
+    X, V = _launch(tmp_path, 2, n, m, 5, buckets, mode, path=4, bf16=1)
+    x = np.tile(synth.x0_host(sum(buckets)), (n, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(n, m, 42, 5, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     payload_bf16=True)
+    _compare(X, x)
+    _compare(V, v)
