@@ -148,3 +148,30 @@ def test_call_order_errors_without_gpu():
         assert "invalid" in C.lib().sesgd_strerror(C.EINVAL).decode()
     finally:
         C.sesgd_destroy(ctx)
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: with the in-tree libsesgd.so absent the binding raises instead of running."""
+    monkeypatch.setattr(C, "_lib", None)
+    monkeypatch.setattr(C, "LIB_PATH", os.path.join(ROOT, "no_such_dir", "libsesgd.so"))
+    with pytest.raises(ImportError):
+        C.lib()
+
+
+def test_product_never_imports_the_oracle():
+    """The oracle is test infrastructure: nothing in the product package (Python or CUDA/C++)
+    imports, links or includes anything under oracle/."""
+    import ast
+    pkg = os.path.join(ROOT, "paper_2007_00433_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            path = os.path.join(dirpath, f)
+            if f.endswith(".py"):
+                tree = ast.parse(open(path).read())
+                for node in ast.walk(tree):
+                    names = ([a.name for a in node.names] if isinstance(node, ast.Import) else
+                             [node.module or ""] if isinstance(node, ast.ImportFrom) else [])
+                    assert not any(n == "oracle" or n.startswith("oracle.") for n in names), path
+            elif f.endswith((".cu", ".cuh", ".cpp", ".h")):
+                src = open(path).read()
+                assert not re.search(r'#include\s*[<"][^>"]*oracle', src), path
