@@ -40,3 +40,17 @@ def test_ddp_wrapper_requires_one_worker_per_rank():
     from paper_2007_00433_b200.ddp import SESGDDataParallel
     with pytest.raises(ValueError):
         SESGDDataParallel(torch.nn.Linear(2, 2), 2, 2, lr=0.1, momentum=0.9, rank=0, world=1)
+
+
+@pytest.mark.parametrize("sizes", [RESNET50_BUCKETS, VGG16_BUCKETS, [699051, 262147, 87378], [0, 1, 0, 7], []])
+def test_fusion_buffer_offsets_are_256B_aligned_and_disjoint(sizes):
+    """bucket b sits at round_up(sum of earlier sizes, 64 floats) -- every bucket
+    256 B aligned (the 128-bit path always applies), buckets never overlap, the buffer holds all."""
+    from paper_2007_00433_b200.engine import _aligned_offsets
+    offs, total = _aligned_offsets(sizes)
+    assert len(offs) == len(sizes)
+    end = 0
+    for o, s in zip(offs, sizes):
+        assert o % 64 == 0 and o >= end and o - end < 64
+        end = o + s
+    assert total >= end and total % 64 == 0 and total - end < 64 + 64
