@@ -164,6 +164,12 @@ def nvlink_algo_bytes(perm, m, r, world, L):
     return max(per_gpu)
 
 
+def workload_desc(workload, n, m, nb, L, mode):
+    """The workload string both arms print in config.workload (same config, same metric)."""
+    return (f"{cfg_label(workload, n, m)}: n={n} workers, group_size={m}, {workload} DDP buckets "
+            f"({nb} buckets, {L:,} fp32 per worker), {mode.upper()} mode, lr {LR}, momentum {MU}")
+
+
 def cfg_label(workload, n, m):
     """BASELINE.json config the run corresponds to (configs[1] = cfg2, configs[2] = cfg3)."""
     if workload == "resnet50" and n == 8 and m == 2:
@@ -241,8 +247,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg_label(args.workload, n, m)} sample: {sample}", "n": n, "group_size": m,
-                   "mode": args.mode},
+        "config": {"workload": workload_desc(args.workload, n, m, len(WORKLOADS[args.workload]), L_total,
+                                             args.mode),
+                   "n": n, "group_size": m, "mode": args.mode, "sample": sample},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -441,9 +448,8 @@ def run_sesgd(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {
-                "workload": (f"{cfg_label(args.workload, n, m)}: n={n} workers, group_size={m}, {args.workload} DDP buckets "
-                             f"({nb} buckets, {L:,} fp32 per worker), {args.mode.upper()} mode, "
-                             f"lr {LR}, momentum {MU}; {r} worker(s) resident per GPU"),
+                "workload": (workload_desc(args.workload, n, m, nb, L, args.mode)
+                             + f"; {r} worker(s) resident per GPU"),
                 "n": n, "group_size": m, "workers_per_gpu": r,
                 "path": "resident (K6)" if resident else {
                     "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P (K4)",

@@ -71,3 +71,10 @@ def test_span_distribution_config3():
     # span two GPUs each (4 B): the max is GPU 0..3's 12 B per element.
     assert bench.nvlink_algo_bytes([0, 2, 4, 6] + list(range(8, 16)) + [1, 3, 5, 7], 4, 2, 8, 1) == \
         pytest.approx(12.0)
+
+
+def test_both_arms_print_the_same_workload():
+    """The reference arm (CPU oracle) and the GPU arm name the same config (BASELINE.json cfg 2)."""
+    d = bench.workload_desc("resnet50", 8, 2, 5, 25557032, "param")
+    assert d == ("cfg2: n=8 workers, group_size=2, resnet50 DDP buckets (5 buckets, 25,557,032 fp32 "
+                 "per worker), PARAM mode, lr 0.1, momentum 0.9")
