@@ -30,3 +30,28 @@ def test_empty_bucket_counts_release_immediately():
     r = BucketReadiness([0, 2, 0])
     assert r.release() == [0]
     assert r.arrive(1) == [] and r.arrive(1) == [1, 2]
+
+
+def test_release_order_property():
+    """Any bucket sizes, any arrival order: every bucket is released exactly once, in index order,
+    and only after all of its gradients and every earlier bucket's have arrived (the in-order
+    launch the per-bucket sync kernels need: buckets are matched across ranks by call order)."""
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.lists(st.integers(0, 4), min_size=1, max_size=8), st.randoms(use_true_random=False))
+    def check(counts, rnd):
+        arrivals = [b for b, c in enumerate(counts) for _ in range(c)]
+        rnd.shuffle(arrivals)
+        r = BucketReadiness(counts)
+        released = list(r.release())
+        seen = [0] * len(counts)
+        for b in arrivals:
+            seen[b] += 1
+            for rb in r.arrive(b):
+                assert rb == len(released)                           # in order, once
+                assert all(seen[q] == counts[q] for q in range(rb + 1))  # complete, with predecessors
+                released.append(rb)
+        assert released == list(range(len(counts))) and r.done()
+
+    check()
