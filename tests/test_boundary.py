@@ -62,6 +62,27 @@ def test_host_scheduler_bitexact_vs_oracle(n, m):
             C.sesgd_destroy(ctx)
 
 
+def test_host_scheduler_bitexact_vs_oracle_random_seeds():
+    """Row a1, property form: any 64-bit seed, any iteration t < 2^62, any m | n <= 64."""
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=400, deadline=None)
+    @given(st.integers(1, 64).flatmap(lambda n: st.tuples(
+        st.just(n), st.sampled_from([d for d in range(1, n + 1) if n % d == 0]))),
+        st.integers(0, 2 ** 64 - 1), st.integers(0, 2 ** 62))
+    def check(nm, seed, t):
+        n, m = nm
+        ctx = C.sesgd_init(n, m, seed)
+        try:
+            perm, gof = C.sesgd_groups(ctx, t, n)
+        finally:
+            C.sesgd_destroy(ctx)
+        _, canon, ogof = oracle.groups(seed, t, n, m)
+        assert np.array_equal(perm, canon) and np.array_equal(gof, ogof)
+
+    check()
+
+
 @pytest.mark.parametrize("n,m", [(2, 2), (4, 2), (8, 2), (8, 4), (16, 4), (32, 8), (64, 2), (64, 64)])
 def test_dimension_exchange_schedule_bitexact_vs_oracle(n, m):
     """NEXT-3 (SESGD_OPT_SCHEDULE = 1): the product's dimension-exchange schedule equals the
