@@ -129,6 +129,13 @@ extern "C" {
                                     fp32 (R21; a lossy variant, compare with the oracle's
                                     payload_bf16 mode; all-local groups round too); one or
                                     several workers per GPU, LSU pushes */
+#define SESGD_OPT_SM_BUDGET 19     /* SMs this context sizes its grids for (0, default: every SM of
+                                    the device).  Loopback ("virtual ranks"): R contexts on ONE GPU,
+                                    each with its own workspace and sesgd_attach_peers given the R
+                                    local workspace pointers, each with budget SMs / R, so that all
+                                    R persistent grids are co-resident and the NVLink-path kernels
+                                    (K3, K4, K5) run against each other through local memory.  Set
+                                    before sesgd_workspace_bytes (the grid fixes the layout) */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

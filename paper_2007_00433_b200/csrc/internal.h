@@ -196,7 +196,9 @@ struct sesgd_ctx {
   // attach
   bool attached = false;
   int device = -1;
-  int sm_count = 0;
+  int sm_count = 0;       // SMs the persistent grids are sized for (SESGD_OPT_SM_BUDGET)
+  int dev_sm_count = 0;   // SMs of the device
+  int sm_budget = 0;      // SESGD_OPT_SM_BUDGET (0: the whole device)
   int n_local = 0;
   std::vector<int32_t> local_workers;
   int8_t slot_of[SESGD_MAX_WORKERS];

@@ -593,6 +593,13 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "bf16 payload must be 0 or 1");
       ctx->payload_bf16 = int(value);
       return SESGD_OK;
+    case SESGD_OPT_SM_BUDGET:
+      if (value < 0) return fail(ctx, SESGD_EINVAL, "SM budget must be >= 0");
+      if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "the SM budget is fixed once the layout freezes");
+      ctx->sm_budget = int(value);
+      if (ctx->attached)
+        ctx->sm_count = ctx->sm_budget > 0 ? std::min(ctx->sm_budget, ctx->dev_sm_count) : ctx->dev_sm_count;
+      return SESGD_OK;
     case SESGD_OPT_PROFILE:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "profile must be 0 or 1");
       ctx->profile = int(value);
@@ -657,7 +664,8 @@ int sesgd_attach(sesgd_ctx *ctx, int32_t device, int32_t n_local, const int32_t 
   ctx->d_err = d;
   ctx->d_abort = ab;
   ctx->device = device;
-  ctx->sm_count = sms;
+  ctx->dev_sm_count = sms;
+  ctx->sm_count = ctx->sm_budget > 0 ? std::min(ctx->sm_budget, sms) : sms;
   ctx->n_local = n_local;
   ctx->local_workers.assign(local_workers, local_workers + n_local);
   std::memcpy(ctx->slot_of, slot_of, sizeof(slot_of));

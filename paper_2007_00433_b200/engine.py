@@ -31,7 +31,7 @@ class SESGDEngine:
                  rank: int = 0, world: int = 1, process_group=None, path: int = C.PATH_AUTO,
                  grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0,
                  p2p_variant: int = -1, discard: int = 1, options: Optional[dict] = None,
-                 weight_decay: float = 0.0):
+                 weight_decay: float = 0.0, loopback: bool = False):
         if n % world != 0:
             raise ValueError("n must be a multiple of the number of ranks")
         self.n, self.m, self.seed = n, group_size, seed
@@ -54,6 +54,11 @@ class SESGDEngine:
         C.sesgd_set_option(self.ctx, C.OPT_DISCARD, discard)
         for opt, val in (options or {}).items():  # extra SESGD_OPT_* (before the layout freezes)
             C.sesgd_set_option(self.ctx, opt, val)
+        self.loopback = bool(loopback and world > 1)
+        self.stream = None  # loopback: this virtual rank's own stream (set below)
+        if self.loopback:  # `world` virtual ranks share this GPU: each sizes its grids for SMs / world
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            C.sesgd_set_option(self.ctx, C.OPT_SM_BUDGET, max(1, sms // world))
         if weight_decay:
             C.sesgd_set_weight_decay(self.ctx, weight_decay)
         C.sesgd_attach(self.ctx, self.device.index, self.local_workers)
@@ -69,7 +74,12 @@ class SESGDEngine:
                                     [t.data_ptr() + 4 * self.offsets[b] for t in self.v_flat],
                                     [t.data_ptr() + 4 * self.offsets[b] for t in self.g_flat])
         self.workspace = None
-        if world > 1:
+        if self.loopback:  # a private workspace; LoopbackGroup attaches the virtual ranks to each other
+            nbytes = C.sesgd_workspace_bytes(self.ctx)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            C.sesgd_workspace_prepare(self.ctx, self.workspace.data_ptr())
+            self.stream = torch.cuda.Stream(device=self.device)
+        elif world > 1:
             self._attach_peers(process_group)
         elif path == C.PATH_ONESHOT:
             # single GPU through the one-shot kernel (profiling / tests): a private workspace
@@ -118,15 +128,20 @@ class SESGDEngine:
         return self.view(self.g_flat[slot], b)
 
     # -------------------------------------------------------------- hot path
+    def default_stream(self) -> torch.cuda.Stream:
+        """the stream calls without an explicit one use: loopback virtual ranks each have their own
+        (their persistent grids must run concurrently), otherwise torch's current stream"""
+        return self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+
     def begin_iter(self, t: int) -> None:
         C.sesgd_begin_iter(self.ctx, t)
 
     def sync_step(self, b: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = stream if stream is not None else self.default_stream()
         C.sesgd_sync_step(self.ctx, b, lr, momentum, s.cuda_stream)
 
     def sync_all(self, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = stream if stream is not None else self.default_stream()
         C.sesgd_sync_all(self.ctx, lr, momentum, s.cuda_stream)
 
     def step(self, t: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None,
@@ -145,7 +160,7 @@ class SESGDEngine:
         """End-to-end through host buffers: g_host[b][slot] -> device, sync, device x ->
         x_host[b][slot]; pipelined (sesgd_sync_all_host: H2D / kernels / D2H of different
         buckets overlap) or one sesgd_sync_step_host per bucket."""
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = stream if stream is not None else self.default_stream()
         self.begin_iter(t)
         if pipelined:
             C.sesgd_sync_all_host(self.ctx, lr, momentum, [h.data_ptr() for hb in g_host for h in hb],
@@ -159,6 +174,8 @@ class SESGDEngine:
         """Algorithm 1's last line: every worker's parameters become the mean over all n
         workers (K8, ascending fold).  Several GPUs: the ranks' parameters are all-gathered
         (data movement only) and every rank averages the n rows locally."""
+        if self.loopback:
+            raise RuntimeError("loopback virtual ranks: use LoopbackGroup.global_average()")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         nb = len(self.bucket_sizes)
         if self.world == 1:
@@ -188,6 +205,8 @@ class SESGDEngine:
     def consensus(self, stream: Optional[torch.cuda.Stream] = None):
         """Consistency of the workers' parameters (K9): (sum over workers and elements of
         (x_i - xbar)^2, max |x_i - xbar|), binary64."""
+        if self.loopback:
+            raise RuntimeError("loopback virtual ranks: use LoopbackGroup.consensus()")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         out = torch.zeros(2, dtype=torch.float64, device=self.device)
         rows = None if self.world == 1 else self._gathered_rows(s)
@@ -216,3 +235,73 @@ class SESGDEngine:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """`world` virtual ranks on ONE GPU (SESGD_OPT_SM_BUDGET): every rank is an SESGDEngine with its
+    own context, buffers, workspace and stream, attached to the others' workspaces through
+    sesgd_attach_peers exactly as NVLink peers are -- so the multi-GPU kernels (K3 one-shot, K4
+    two-shot, K5 ring) with their flags, stage / receive slots and reuse guards run, and are
+    parity-tested, on a single B200.  Peer traffic goes through local HBM instead of NVLink, so
+    loopback timings are not NVLink numbers.  Worker w lives on virtual rank w // (n / world)."""
+
+    def __init__(self, world: int, n: int, group_size: int, bucket_sizes: Sequence[int], **kw):
+        if world < 2:
+            raise ValueError("a loopback group needs >= 2 virtual ranks")
+        self.world = world
+        self.engines = [SESGDEngine(n, group_size, bucket_sizes, rank=r, world=world, loopback=True, **kw)
+                        for r in range(world)]
+        ptrs = [e.workspace.data_ptr() for e in self.engines]
+        torch.cuda.synchronize(self.engines[0].device)
+        for e in self.engines:
+            C.sesgd_attach_peers(e.ctx, world, e.rank, ptrs, e.worker_rank)
+            e._siblings = self.engines
+
+    def __getitem__(self, r: int) -> SESGDEngine:
+        return self.engines[r]
+
+    def __iter__(self):
+        return iter(self.engines)
+
+    def step(self, t: int, lr: float, momentum: float, fused: bool = True) -> None:
+        """one iteration on every virtual rank: each enqueues its launch(es) on its own stream, so
+        the R persistent grids run concurrently and exchange through each other's workspaces"""
+        for e in self.engines:
+            e.step(t, lr, momentum, fused=fused)
+
+    def synchronize(self) -> None:
+        for e in self.engines:
+            e.stream.synchronize()
+
+    def _gather(self):
+        """every virtual rank's parameters after all queued work: [n, total] (data movement only)"""
+        self.synchronize()
+        return torch.cat([torch.stack(e.x_flat) for e in self.engines])
+
+    def global_average(self) -> None:
+        """Algorithm 1's last line on every virtual rank: K8 over the gathered rows"""
+        rows = self._gather()
+        for e in self.engines:
+            for b in range(len(e.bucket_sizes)):
+                ptrs = [rows[w].data_ptr() + 4 * e.offsets[b] for w in range(e.n)]
+                C.sesgd_global_average(e.ctx, b, e.n, ptrs, e.stream.cuda_stream)
+        self.synchronize()
+
+    def consensus(self):
+        """K9 over the gathered rows, on virtual rank 0"""
+        rows = self._gather()
+        e = self.engines[0]
+        out = torch.zeros(2, dtype=torch.float64, device=e.device)
+        for b in range(len(e.bucket_sizes)):
+            ptrs = [rows[w].data_ptr() + 4 * e.offsets[b] for w in range(e.n)]
+            C.sesgd_consensus(e.ctx, b, e.n, out.data_ptr(), ptrs, e.stream.cuda_stream)
+        e.stream.synchronize()
+        return float(out[0]), float(out[1])
+
+    def poll(self) -> None:
+        for e in self.engines:
+            e.poll()
+
+    def close(self) -> None:
+        for e in self.engines:
+            e.close()

@@ -23,7 +23,7 @@ OPT_MODE, OPT_PATH, OPT_TIMEOUT_MS, OPT_GRID, OPT_HOP_DELAY_NS, OPT_P2P_VARIANT,
 OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL, OPT_PUSH_TMA = 8, 9, 10, 11, 12
 OPT_RELEASE_DELAY, OPT_RELEASE_EVERY, OPT_LOCAL_PERIOD, OPT_SCHEDULE = 13, 14, 15, 16
 SCHEDULE_RANDOM, SCHEDULE_DIMENSION_EXCHANGE = 0, 1
-OPT_RELEASE_STAGGER, OPT_PAYLOAD_BF16 = 17, 18
+OPT_RELEASE_STAGGER, OPT_PAYLOAD_BF16, OPT_SM_BUDGET = 17, 18, 19
 
 # every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
 EXPORTED = (

@@ -1,6 +1,8 @@
 """Per-rank body of the multi-GPU parity test (launched by tests/test_gpu_multigpu.py via
-torch.distributed.run).  Runs T SESGD iterations through the one-shot NVLink P2P path
-and saves every local worker's x and v for the parent to compare with the oracle."""
+torch.distributed.run, one process per GPU), or -- with --loopback R -- all R virtual ranks in
+ONE process on ONE GPU (engine.LoopbackGroup: the same kernels, flags and workspaces, peers in
+local memory).  Runs T SESGD iterations through the multi-GPU paths and saves every rank's
+workers' x and v for the parent to compare with the oracle."""
 import argparse
 import os
 import sys
@@ -14,6 +16,61 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2007_00433_b200 import sesgd as C  # noqa: E402
 from paper_2007_00433_b200.engine import SESGDEngine  # noqa: E402
+
+
+def _options(a):
+    return {k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
+                              (C.OPT_PUSH_TMA, a.tma), (C.OPT_LOCAL_PERIOD, a.period),
+                              (C.OPT_SCHEDULE, a.schedule), (C.OPT_PAYLOAD_BF16, a.bf16)) if v}
+
+
+def _padded(idx, buckets, offsets):
+    """global (unpadded) element indices -> the engine's aligned flat layout"""
+    starts = torch.tensor(np.concatenate([[0], np.cumsum(buckets)[:-1]]), device=idx.device)
+    b = torch.searchsorted(starts, idx, right=True) - 1
+    return idx - starts[b] + torch.tensor(offsets, device=idx.device)[b]
+
+
+def _rows(eng, flat, buckets, coords):
+    if coords is None:
+        return np.stack([torch.cat([eng.view(f, b) for b in range(len(buckets))]).cpu().numpy() for f in flat])
+    idx = _padded(torch.from_numpy(coords).to(eng.device), buckets, eng.offsets)
+    return np.stack([f[idx].cpu().numpy() for f in flat])
+
+
+def loopback(a):
+    """R virtual ranks on cuda:0 (SESGD_OPT_SM_BUDGET = SMs / R each, one stream each)"""
+    from paper_2007_00433_b200.engine import LoopbackGroup
+    torch.cuda.set_device(0)
+    buckets = [int(b) for b in a.buckets.split(",")]
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    coords = np.load(a.coords) if a.coords else None
+    grp = LoopbackGroup(a.loopback, a.workers, a.gsize, buckets, seed=42, mode=a.mode, grid=a.grid,
+                        timeout_ms=10000, p2p_variant=a.variant, path=a.path, hop_delay_ns=a.hop_ns,
+                        weight_decay=a.wd, options=_options(a))
+    for eng in grp:
+        st = eng.stream.cuda_stream
+        for s in range(eng.r):
+            for b, L in enumerate(buckets):
+                synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st)
+    for t in range(a.t0, a.t0 + a.iters):
+        for eng in grp:
+            st = eng.stream.cuda_stream
+            for s, w in enumerate(eng.local_workers):
+                for b, L in enumerate(buckets):
+                    synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
+        grp.step(t, 0.1, 0.9, fused=bool(a.fused))
+    if a.final_avg:
+        grp.global_average()
+    grp.synchronize()
+    grp.poll()
+    cons = np.array(grp.consensus() if a.consensus else (0.0, 0.0))
+    for eng in grp:
+        stats = eng.stats(0)
+        np.savez(f"{a.out}.rank{eng.rank}.npz", X=_rows(eng, eng.x_flat, buckets, coords),
+                 V=_rows(eng, eng.v_flat, buckets, coords), workers=np.array(eng.local_workers),
+                 flag_messages=stats["flag_messages"], payload=stats["payload_bytes_in"], cons=cons)
+    grp.close()
 
 
 def main():
@@ -38,8 +95,12 @@ def main():
     p.add_argument("--consensus", type=int, default=0)
     p.add_argument("--wd", type=float, default=0.0)
     p.add_argument("--bf16", type=int, default=0)
+    p.add_argument("--loopback", type=int, default=0)
+    p.add_argument("--coords", default="")
     p.add_argument("--out", required=True)
     a = p.parse_args()
+    if a.loopback:
+        return loopback(a)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -50,11 +111,7 @@ def main():
     eng = SESGDEngine(a.workers, a.gsize, buckets, seed=42, mode=a.mode, rank=rank, world=world,
                       grid=a.grid, timeout_ms=10000, p2p_variant=a.variant, path=a.path,
                       hop_delay_ns=a.hop_ns, weight_decay=a.wd,
-                      options={k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
-                                                   (C.OPT_PUSH_TMA, a.tma),
-                                                   (C.OPT_LOCAL_PERIOD, a.period),
-                                                   (C.OPT_SCHEDULE, a.schedule),
-                                                   (C.OPT_PAYLOAD_BF16, a.bf16)) if v})
+                      options=_options(a))
     st = torch.cuda.current_stream().cuda_stream
     for s in range(eng.r):
         for b, L in enumerate(buckets):
@@ -68,8 +125,9 @@ def main():
         eng.global_average()
     torch.cuda.synchronize()
     eng.poll()
-    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
-    V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    coords = np.load(a.coords) if a.coords else None
+    X = _rows(eng, eng.x_flat, buckets, coords)
+    V = _rows(eng, eng.v_flat, buckets, coords)
     stats = eng.stats(0)
     cons = np.array(eng.consensus() if a.consensus else (0.0, 0.0))
     np.savez(f"{a.out}.rank{rank}.npz", X=X, V=V, workers=np.array(eng.local_workers),

@@ -1,8 +1,13 @@
 """Multi-GPU parity of the NVLink P2P paths (K3 one-shot, K4 two-shot, K5 ring) against the CPU oracle.
 
-Launches tests/mgpu_worker.py under torch.distributed.run on 2 (and, if present, 4)
-GPUs, one process per GPU, and compares every worker's x, v after T iterations with
-the oracle run on the same seeded inputs.  Skipped on boxes with fewer GPUs.
+Every test runs over two transports:
+* ``loopback`` -- the R ranks are virtual ranks on ONE GPU (engine.LoopbackGroup: R contexts, each
+  with its own workspace and stream and SMs / R of the device, attached to each other with
+  sesgd_attach_peers), so the multi-GPU kernels, their flags, stage / receive slots and reuse
+  guards run on a 1-GPU box;
+* ``nvlink`` -- tests/mgpu_worker.py under torch.distributed.run, one process per GPU over
+  NVLink / NVSwitch (skipped on boxes with fewer GPUs).
+Both compare every worker's x, v after T iterations with the oracle on the same seeded inputs.
 """
 import os
 import socket
@@ -16,8 +21,16 @@ import torch
 import oracle
 import synth
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = [pytest.mark.gpu]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_TRANSPORT = "loopback"
+
+
+@pytest.fixture(autouse=True, params=["loopback", pytest.param("nvlink", marks=pytest.mark.multigpu)])
+def transport(request):
+    global _TRANSPORT
+    _TRANSPORT = request.param
+    yield request.param
 
 
 def _free_port():
@@ -30,26 +43,36 @@ def _free_port():
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
             lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
-            bf16=0):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
+            bf16=0, coords=None):
+    """`gpus` ranks: processes on as many GPUs (nvlink) or virtual ranks on cuda:0 (loopback)"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    loop = _TRANSPORT == "loopback"
+    if not loop and torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "res")
+    extra = []
+    if coords is not None:
+        np.save(str(tmp_path / "coords.npy"), np.asarray(coords, np.int64))
+        extra = ["--coords", str(tmp_path / "coords.npy")]
     for _attempt in range(3):  # the rendezvous port can be taken between probe and bind
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
-               "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+        launcher = ([sys.executable] if loop else
+                    [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+                     "--master-addr=127.0.0.1", f"--master-port={_free_port()}"])
+        cmd = [*launcher,
                os.path.join(ROOT, "tests", "mgpu_worker.py"), "--workers", str(n), "--gsize", str(m),
                "--iters", str(T), "--buckets", ",".join(map(str, buckets)), "--mode", str(mode),
                "--t0", str(t0), "--grid", str(grid), "--variant", str(variant), "--fused", str(fused),
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
-               "--bf16", str(bf16),
+               "--bf16", str(bf16), "--loopback", str(gpus if loop else 0), *extra,
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
             break
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
-    X = np.zeros((n, sum(buckets)), np.float32)
+    X = np.zeros((n, sum(buckets) if coords is None else len(coords)), np.float32)
     V = np.zeros_like(X)
     for r in range(gpus):
         d = np.load(f"{out}.rank{r}.npz")
@@ -58,11 +81,47 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
     return X, V
 
 
-def _oracle(n, m, L, T, mode, t0=0):
-    x = np.tile(synth.x0_host(L), (n, 1))
+def _oracle(n, m, L, T, mode, t0=0, coords=None):
+    x = np.tile(synth.x0_host(L, coords=coords), (n, 1))
     v = np.zeros_like(x)
-    oracle.run(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, mode=mode, t0=t0)
+    oracle.run(n, m, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, mode=mode, t0=t0, coords=coords)
     return x, v
+
+
+def _sample(buckets, k=3000, seed=11):
+    """bucket edges and ragged tails plus random interior coordinates (global element indices)"""
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]])
+    edges = np.concatenate([[o, o + 1, o + s - 1, o + s - 2] for o, s in zip(offs, buckets)])
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([edges, rng.integers(0, sum(buckets), k - len(edges))])).astype(np.int64)
+
+
+@pytest.mark.parametrize("gpus", [8, 4, 2])
+def test_resnet50_bench_shape_full_size(tmp_path, gpus):
+    """BASELINE configs[1] at full size in bench.py's launch configuration: n = 8, group_size 2, the
+    five ResNet-50 DDP buckets (25,557,032 fp32), T = 100, one fused launch per iteration on every
+    rank; gpus = 8 is the north star's one worker per GPU (K4), 4 and 2 the bench's N = 4 / N = 2
+    lines (2 and 4 workers per GPU, the MULTI K4).  The oracle replays ~3000 sampled coordinates."""
+    from paper_2007_00433_b200.workloads import RESNET50_BUCKETS
+    buckets = list(RESNET50_BUCKETS)
+    coords = _sample(buckets)
+    X, V = _launch(tmp_path, gpus, 8, 2, 100, buckets, coords=coords)
+    x, v = _oracle(8, 2, sum(buckets), 100, 0, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_vgg16_cfg3_shape_full_size(tmp_path):
+    """BASELINE configs[2] at full size: n = 16 workers, 2 per GPU on 8 ranks, group_size 4 (groups
+    span 1-4 ranks), the six VGG-16 DDP buckets (138,357,544 fp32), 10 iterations, MULTI K4;
+    sampled coordinates against the oracle."""
+    from paper_2007_00433_b200.workloads import VGG16_BUCKETS
+    buckets = list(VGG16_BUCKETS)
+    coords = _sample(buckets)
+    X, V = _launch(tmp_path, 8, 16, 4, 10, buckets, coords=coords)
+    x, v = _oracle(16, 4, sum(buckets), 10, 0, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
 
 
 def _compare(got, want):
@@ -326,6 +385,8 @@ def test_two_gpus_weight_decay(tmp_path, n, path, mode):
 
 # ---------------------------------------------------------------- NVLS (path 5), group_size = n
 def _nvls_or_skip(tmp_path, gpus, n, mode, buckets, T):
+    if _TRANSPORT == "loopback":
+        pytest.skip("NVLS needs an NVSwitch multicast object across GPUs")
     try:
         return _launch(tmp_path, gpus, n, n, T, buckets, mode, path=5)
     except AssertionError as e:
