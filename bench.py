@@ -170,6 +170,15 @@ def workload_desc(workload, n, m, nb, L, mode):
             f"({nb} buckets, {L:,} fp32 per worker), {mode.upper()} mode, lr {LR}, momentum {MU}")
 
 
+def common_config(workload, n, m, mode):
+    """config keys both arms print identically (same workload, same metric): the GPU arm adds
+    its launch keys (workers_per_gpu, path, ...) beside them, never inside `workload`."""
+    from paper_2007_00433_b200.workloads import WORKLOADS
+    buckets = WORKLOADS[workload]
+    return {"workload": workload_desc(workload, n, m, len(buckets), int(sum(buckets)), mode),
+            "n": n, "group_size": m, "mode": mode}
+
+
 def cfg_label(workload, n, m):
     """BASELINE.json config the run corresponds to (configs[1] = cfg2, configs[2] = cfg3)."""
     if workload == "resnet50" and n == 8 and m == 2:
@@ -247,9 +256,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_desc(args.workload, n, m, len(WORKLOADS[args.workload]), L_total,
-                                             args.mode),
-                   "n": n, "group_size": m, "mode": args.mode, "sample": sample},
+        "config": dict(common_config(args.workload, n, m, args.mode), sample=sample),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -448,9 +455,8 @@ def run_sesgd(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {
-                "workload": (workload_desc(args.workload, n, m, nb, L, args.mode)
-                             + f"; {r} worker(s) resident per GPU"),
-                "n": n, "group_size": m, "workers_per_gpu": r,
+                **common_config(args.workload, n, m, args.mode),
+                "workers_per_gpu": r,
                 "path": "resident (K6)" if resident else {
                     "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P (K4)",
                     "ring": "ring inside each group over NVLink P2P (K5)"}.get(

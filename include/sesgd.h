@@ -127,8 +127,9 @@ extern "C" {
                                     even) instead of fp32 -- every member's contribution, its own
                                     included, is rounded before the fold; the fold and the mean stay
                                     fp32 (R21; a lossy variant, compare with the oracle's
-                                    payload_bf16 mode; all-local groups round too); one or
-                                    several workers per GPU, LSU pushes */
+                                    payload_bf16 mode; all-local groups of K4 round too); one
+                                    or several workers per GPU, LSU pushes.  The resident K6 path
+                                    (every worker on one GPU) returns SESGD_ENOTSUP with it set */
 #define SESGD_OPT_SM_BUDGET 19     /* SMs this context sizes its grids for (0, default: every SM of
                                     the device).  Loopback ("virtual ranks"): R contexts on ONE GPU,
                                     each with its own workspace and sesgd_attach_peers given the R

@@ -336,11 +336,12 @@ int orc_step_ring_f32(int32_t n, int32_t m, const int32_t *canon, int64_t L, flo
   for (int32_t j = 0; j < k; ++j) {
     const int32_t *G = canon + (size_t)j * m;
     for (int64_t e = 0; e < L; ++e) {
-      /* Scatter-Reduce: the slice containing e starts at ring position s and travels the
-       * ring, each member adding its own value to what it received */
+      /* Scatter-Reduce: "slice s accumulated in ring order starting from member (s+1) mod m"
+       * (S:263): it starts at ring position s+1 and travels the ring, each member adding its
+       * own value to what it received, so member s adds last and holds the full sum */
       int32_t s = orc_slice_of(L, m, e);
-      float acc = pay[(size_t)G[s] * (size_t)L + (size_t)e];
-      for (int32_t t = 1; t < m; ++t) acc = acc + pay[(size_t)G[(s + t) % m] * (size_t)L + (size_t)e];
+      float acc = pay[(size_t)G[(s + 1) % m] * (size_t)L + (size_t)e];
+      for (int32_t t = 2; t <= m; ++t) acc = acc + pay[(size_t)G[(s + t) % m] * (size_t)L + (size_t)e];
       float mean = acc / fm; /* "division by m applied once after full accumulation" */
       /* All-Gather: every member receives the same mean */
       for (int32_t r = 0; r < m; ++r) {

@@ -13,10 +13,11 @@
 // One worker per GPU.  Slices follow SPEC collectives.slice_bounds:
 // slice s = [floor(sL/m), floor((s+1)L/m)).  CTA j of every member owns the same strip of
 // every slice, so CTA j only waits on CTA j of its ring neighbour (all CTAs co-resident).
-// Scatter-Reduce step t: member p sends slice (p - t) mod m: its own x_hat at t = 0, else
-// (received (+) own x_hat); the member holding the full sum of slice (p + 1) mod m after
-// step m-2 divides by m.  Summation order of slice s is ring order starting at position s
-// (S:263), so results equal the ascending-fold oracle bit-for-bit only for m <= 2.
+// Scatter-Reduce step t: member p sends slice (p - 1 - t) mod m: its own x_hat at t = 0, else
+// (received (+) own x_hat); so slice s is "accumulated in ring order starting from member
+// (s+1) mod m" and member p, adding last, holds the full sum of its own slice p after
+// step m-2 and divides by m.  The ascending-fold oracle agrees bit-for-bit only for m <= 2;
+// the ring-order oracle (orc_step_ring_f32) follows the same S:263 order.
 // Receive buffers: one per (call parity, step), no reuse inside a launch; reuse two calls
 // later is guarded by the receiver's consumed counter.  Every spin has a timeout.
 #include "common.cuh"
@@ -126,7 +127,7 @@ struct Ring {
     __syncthreads();
     // ---- Scatter-Reduce: m - 1 steps
     for (int t = 0; t < m - 1; ++t) {
-      const int s = ((p - t) % m + m) % m;
+      const int s = ((p - 1 - t) % m + m) % m;
       int64_t lo, hi;
       strip(s, lo, hi);
       const int64_t base = slice_lo(s);
@@ -140,8 +141,8 @@ struct Ring {
       }
       signal(t);
     }
-    // the full sum of slice (p + 1) mod m arrives at the last scatter step
-    const int sf = (p + 1) % m;
+    // the full sum of my own slice p arrives at the last scatter step
+    const int sf = p;
     int64_t lo, hi;
     strip(sf, lo, hi);
     int64_t base = slice_lo(sf);
@@ -169,7 +170,7 @@ struct Ring {
     signal(m - 1);
     // ---- All-Gather: m - 1 steps (step index m - 1 + u)
     for (int u = 0; u < m - 1; ++u) {
-      const int s = ((p - u) % m + m) % m;  // slice received at this step
+      const int s = ((p - 1 - u) % m + m) % m;  // slice received at this step
       strip(s, lo, hi);
       base = slice_lo(s);
       await(m - 1 + u);

@@ -833,6 +833,8 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
 
   if (path == SESGD_PATH_RESIDENT) {
     if (!all_local) return fail(ctx, SESGD_ESTATE, "resident path needs all n workers on this GPU");
+    if (ctx->payload_bf16)  // R21 rounds what crosses NVLink; K6 keeps every contribution in fp32
+      return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs a multi-GPU two-shot path (K4), not K6");
     ResidentArgs a{};
     a.x = b.d_x;
     a.v = b.d_v;
@@ -932,6 +934,8 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
   const bool all_local = (ctx->n_local == ctx->n);
   const int path = resolve_path(ctx);
   if (path == SESGD_PATH_RESIDENT && all_local) {  // K6 over every bucket in one launch
+    if (ctx->payload_bf16)
+      return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs a multi-GPU two-shot path (K4), not K6");
     if (!ctx->resident_tables_ok) {
       rc = upload_resident_tables(ctx);
       if (rc != SESGD_OK) return rc;

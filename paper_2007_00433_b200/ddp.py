@@ -80,6 +80,12 @@ class SESGDDataParallel:
                  engine_options: Optional[dict] = None):
         if n != world:
             raise ValueError("SESGDDataParallel runs one worker per process (n == world size)")
+        if overlap and (engine_options or {}).get(C.OPT_P2P_VARIANT, 0) >= 1:
+            # the SM-specialised one-shot kernel (K3 split) has COMM and COMPUTE CTAs of the same
+            # grid wait on each other: launched on a side stream while backward kernels hold SMs,
+            # part of the grid may not become resident (sesgd_capi.cu launches it cooperatively,
+            # so it fails instead of hanging) -- the overlap uses the default K4 path
+            raise ValueError("overlap=True needs the default P2P layout (SESGD_OPT_P2P_VARIANT 0)")
         self.module = module
         self.lr, self.momentum = lr, momentum
         self.overlap = overlap
@@ -105,6 +111,8 @@ class SESGDDataParallel:
                     p.grad = gview  # gradient accumulates into it (in place)
                     self.bucket_of[id(p)] = b
                     off += k
+        if world > 1:
+            self._broadcast_state(module)
         self.ready = BucketReadiness([len(b) for b in self.bucket_params])
         self.launched_in_backward = 0
         self.side = torch.cuda.Stream(dev)
@@ -119,6 +127,21 @@ class SESGDDataParallel:
         if overlap:
             self._hooks = {id(p): p.register_post_accumulate_grad_hook(self._on_grad) for p in self.params}
         self._hooked = [len(b) for b in self.bucket_params]
+
+    def _broadcast_state(self, module: torch.nn.Module) -> None:
+        """Algorithm 1 starts every worker from the same x_0: rank 0's parameters (the
+        fusion buffer, so every bucket at once) and module buffers (BatchNorm running statistics)
+        are broadcast over the process group, as torch DDP does at construction.  Afterwards the
+        buffers stay local to each worker (SESGD averages parameters only, Eq. 6)."""
+        import torch.distributed as dist
+        grp = self.engine.group
+        src = dist.get_global_rank(grp, 0)
+        with torch.no_grad():
+            for t in self.engine.x_flat:
+                dist.broadcast(t, src=src, group=grp)
+            for buf in module.buffers():
+                dist.broadcast(buf, src=src, group=grp)
+        torch.cuda.synchronize(self.engine.device)
 
     # ------------------------------------------------------------------ per step
     def begin_step(self, t: Optional[int] = None) -> None:

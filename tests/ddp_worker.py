@@ -44,7 +44,7 @@ def main():
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
 
-    torch.manual_seed(0)  # identical x_0 on every worker (Alg.1 line 1)
+    torch.manual_seed(rank)  # distinct random init per rank: SESGDDataParallel broadcasts rank 0's x_0
     model = torch.nn.Sequential(torch.nn.Linear(256, 512), torch.nn.ReLU(), torch.nn.Linear(512, 512),
                                 torch.nn.ReLU(), torch.nn.Linear(512, 10)).to(dev)
     # small caps so the MLP spans three buckets (the last layer first, as DDP orders them)
@@ -53,6 +53,8 @@ def main():
                             overlap=bool(a.overlap), static_graph=bool(a.static))
     eng = ddp.engine
     nb = len(ddp.bucket_params)
+    X_init = gather(eng.x_flat[0])  # identical x_0 on every worker (Alg.1 line 1)
+    assert np.array_equal(X_init, np.broadcast_to(X_init[:1], X_init.shape)), "x_0 differs across ranks"
     log = []
     for t in range(a.iters):
         torch.cuda.synchronize()

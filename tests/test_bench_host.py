@@ -78,3 +78,23 @@ def test_both_arms_print_the_same_workload():
     d = bench.workload_desc("resnet50", 8, 2, 5, 25557032, "param")
     assert d == ("cfg2: n=8 workers, group_size=2, resnet50 DDP buckets (5 buckets, 25,557,032 fp32 "
                  "per worker), PARAM mode, lr 0.1, momentum 0.9")
+
+
+def test_reference_arm_json_workload_equals_gpu_arm_config():
+    """The reference arm's emitted config.workload (run here on CPU) is the string the GPU arm
+    emits: both come from bench.common_config, and the GPU arm only adds keys beside it."""
+    import inspect
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(bench.__file__)
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    d = json.loads(res.stdout.strip().splitlines()[-1])
+    want = bench.common_config("resnet50", 8, 2, "param")
+    assert {k: d["config"][k] for k in want} == want
+    src = inspect.getsource(bench.run_sesgd)
+    assert "**common_config(args.workload, n, m, args.mode)" in src
+    assert "workload_desc(" not in src  # nothing appended to the shared string

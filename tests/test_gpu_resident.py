@@ -394,3 +394,19 @@ def test_pair_split_probability_on_device():
     sigma = np.sqrt(T * p_split * (1 - p_split))
     assert abs(p_split - 0.8) < 1e-15
     assert np.all(np.abs(split - T * p_split) < 5 * sigma)
+
+
+def test_bf16_payload_rejected_on_resident_path():
+    """R21 rounds what crosses NVLink (K4); K6 keeps every contribution fp32, so asking for the
+    bf16 payload with every worker resident is refused rather than silently ignored."""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    eng = SESGDEngine(4, 2, [1000], seed=42, options={C.OPT_PAYLOAD_BF16: 1})
+    eng.begin_iter(0)
+    with pytest.raises(C.SesgdError) as ei:
+        eng.sync_all(LR, MU)
+    assert ei.value.code == C.ENOTSUP
+    with pytest.raises(C.SesgdError) as ei:
+        eng.sync_step(0, LR, MU)
+    assert ei.value.code == C.ENOTSUP
+    eng.close()

@@ -515,6 +515,30 @@ def test_ring_mean_worked_example():
     assert np.array_equal(x, np.full((3, 2), 2.0, np.float32))
 
 
+def test_ring_order_starts_each_slice_at_the_next_member():
+    """S:263: "slice s accumulated in ring order starting from member (s+1) mod m".  m = 3,
+    L = 3 (slice s = element s), payloads chosen so that the summation order decides the binary32
+    result: for slice s the members' values are 2^24 at s+1, -2^24 at s+2 and 1 at s.  Starting at
+    s+1: (2^24 + -2^24) + 1 = 1, mean fl(1/3).  Starting at s (the other plausible reading):
+    (1 + 2^24) rounds to 2^24, + -2^24 = 0.  Hand-computed, not re-derived from the oracle."""
+    big = np.float32(2.0 ** 24)
+    x = np.zeros((3, 3), np.float32)
+    for s in range(3):
+        x[(s + 1) % 3, s], x[(s + 2) % 3, s], x[s, s] = big, -big, 1.0
+    v = np.zeros_like(x)
+    g = np.zeros_like(x)
+    oracle.step_ring(3, 3, np.array([0, 1, 2], np.int32), x, v, g, 0.0, 0.0)  # payload = x
+    assert np.array_equal(x, np.full((3, 3), np.float32(1.0) / np.float32(3.0), np.float32))
+    # m = 4, slice s = element s: 2^24 at s+1, 1 at s+2, -2^24 at s+3, 1 at s:
+    # ((2^24 + 1) + -2^24) + 1 = (2^24 - 2^24) + 1 = 1 (the +1 at s+2 is absorbed); mean 1/4
+    x = np.zeros((4, 4), np.float32)
+    for s in range(4):
+        x[(s + 1) % 4, s], x[(s + 2) % 4, s], x[(s + 3) % 4, s], x[s, s] = big, 1.0, -big, 1.0
+    v = np.zeros_like(x)
+    oracle.step_ring(4, 4, np.array([0, 1, 2, 3], np.int32), x, v, np.zeros_like(x), 0.0, 0.0)
+    assert np.array_equal(x, np.full((4, 4), 0.25, np.float32))
+
+
 def test_ring_order_equals_fold_for_two_members_and_is_close_otherwise():
     """m <= 2: ring order and ascending fold are the same binary32 sum (commutativity);
     m > 2: the two differ only by rounding (within the derived bound of the fp64 mean)."""
