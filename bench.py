@@ -62,6 +62,9 @@ def parse():
     p.add_argument("--fold-lag", type=int, default=0)
     p.add_argument("--grid", type=int, default=0, help="CTAs per one-shot launch (0 = auto)")
     p.add_argument("--resident-unroll", type=int, default=0)
+    p.add_argument("--protocol", type=int, default=0, help="two-shot: SESGD_OPT_PROTOCOL")
+    p.add_argument("--experiment", type=int, default=0,
+                   help="SESGD_OPT_EXPERIMENT bits (measurement only: results are wrong)")
     return p.parse_args()
 
 
@@ -298,7 +301,9 @@ def run_sesgd(args):
                                                  (C.OPT_RELEASE_DELAY, args.release_delay),
                                                  (C.OPT_RELEASE_EVERY, args.release_every),
                                                  (C.OPT_RELEASE_STAGGER, args.release_stagger),
-                                                 (C.OPT_PAYLOAD_BF16, args.payload_bf16)) if v},
+                                                 (C.OPT_PAYLOAD_BF16, args.payload_bf16),
+                                                 (C.OPT_EXPERIMENT, args.experiment),
+                                                 (C.OPT_PROTOCOL, args.protocol)) if v},
                       path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
                             "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT, "nvls": C.PATH_NVLS}[args.path])
     r = eng.r
@@ -336,7 +341,16 @@ def run_sesgd(args):
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(launches_per_step)] for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl_ctr = None
+    if world > 1:  # NVLink TX/RX byte counters (NVML) around the timed region, full-speed kernels
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from nvml_nvlink import NvlinkCounters
+            nvl_ctr = NvlinkCounters(local)
+        except Exception:
+            nvl_ctr = None
     barrier()
+    nvl0 = nvl_ctr.read() if nvl_ctr else None
     with ClockSampler(local) as clk:
         start.record(stream)
         for k in range(K):
@@ -353,8 +367,20 @@ def run_sesgd(args):
             t_next += 1
         end.record(stream)
         barrier()
+    nvl1 = nvl_ctr.read() if nvl_ctr else None
     eng.poll()
     ms_total = max_over_ranks(start.elapsed_time(end))
+    nvlink_measured = None
+    if world > 1:  # every rank takes part in the max (-1: counter unavailable on that rank)
+        keys = ("data_tx", "data_rx", "raw_tx", "raw_rx")
+        d = {k: (-1.0 if nvl0 is None or nvl0[k] is None or nvl1[k] is None else (nvl1[k] - nvl0[k]) / K)
+             for k in keys}
+        d = {k: max_over_ranks(v) for k, v in d.items()}
+        if all(v >= 0 for v in d.values()):  # max over ranks of each GPU's bytes per step
+            nvlink_measured = {f"{k}_bytes_per_step": v for k, v in d.items()}
+            nvlink_measured["source"] = ("NVML NVLink throughput counters (field ids 138-141, per-link "
+                                         "KiB, summed over links) read around the timed region; "
+                                         "max over ranks")
     ms_step = ms_total / K
     launch_ms = [[e0.elapsed_time(e1) for (e0, e1) in ev[k]] for k in range(K)]
     kern_ms_total = max_over_ranks(sum(map(sum, launch_ms)))
@@ -401,6 +427,11 @@ def run_sesgd(args):
         else:
             roof = {"bound": "hbm", "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_hbm / hbm_peak, "peak_source": peak_src}
+        if nvlink_measured is not None and nvl_bytes > 0:
+            tx = nvlink_measured["data_tx_bytes_per_step"]
+            nvlink_measured["tx_over_algorithmic"] = tx / nvl_bytes
+            nvlink_measured["tx_gbs"] = tx * K / (kern_ms_total * 1e-3) / 1e9
+        roof.update({"nvlink_measured": nvlink_measured})
         roof.update({"hbm_achieved": achieved_hbm, "nvlink_algo_bytes_per_step": nvl_bytes,
                      "t_roof_us": max(t_hbm, t_nvl) * 1e6, "kernel": kernel})
     roof["traffic"] = traffic_for(kernel, f"{args.workload}_n{n}_m{m}_g{world}")

@@ -137,6 +137,23 @@ extern "C" {
                                     R persistent grids are co-resident and the NVLink-path kernels
                                     (K3, K4, K5) run against each other through local memory.  Set
                                     before sesgd_workspace_bytes (the grid fixes the layout) */
+#define SESGD_OPT_PROTOCOL 21      /* two-shot handshake (set before sesgd_workspace_bytes, identical
+                                    on every rank): 0 (default) = epoch flags released with a
+                                    system-scope fence per batch; 1 = value-carried validity: every
+                                    receive-slot float holds a sentinel NaN (0xFFFFFFFF) until the
+                                    peer's value lands, the receiver polls the values themselves
+                                    and re-arms them (no sender fence, no flag).  A payload equal
+                                    to the sentinel travels as the canonical NaN 0x7FFFFFFF.  fp32
+                                    LSU pushes only (else SESGD_ENOTSUP) */
+#define SESGD_OPT_COOPERATIVE 22   /* 1 (default): the persistent multi-GPU grids (K3, K4, K5) are
+                                    launched cooperatively -- the runtime rejects a grid that cannot
+                                    be co-resident (SESGD_ECUDA) and starts it only when all its CTAs
+                                    fit at once (e.g. beside backward kernels); 0: plain launch */
+#define SESGD_OPT_EXPERIMENT 20    /* MEASUREMENT ONLY -- results are wrong when set: bit 0 drops
+                                    the system-scope fence before the two-shot flag releases,
+                                    bit 1 sends the two-shot pushes to this rank's own receive
+                                    slots instead of the peers' (no NVLink payload).  Bounds what
+                                    the flag protocol and the NVLink traffic cost */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

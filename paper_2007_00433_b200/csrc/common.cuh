@@ -146,4 +146,24 @@ __device__ __forceinline__ void fence_proxy_async_shared() {
 }
 
 }  // namespace dev
+
+// Persistent grids whose CTAs wait on each other or on peer GPUs' CTAs (K3, K4, K5) are launched
+// cooperatively: the runtime rejects a grid that cannot be co-resident (instead of a hang) and
+// starts it only when every CTA can be resident at once, e.g. on a side stream while backward
+// kernels hold SMs (SESGDDataParallel's overlap).
+inline cudaError_t launch_persistent(const void *kernel, unsigned grid, unsigned block, void **args,
+                                     size_t smem, cudaStream_t stream, bool cooperative = true) {
+  if (!cooperative) return cudaLaunchKernel(kernel, dim3(grid), dim3(block), args, smem, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, kernel, args);
+}
 }  // namespace sesgd

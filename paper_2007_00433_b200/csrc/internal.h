@@ -102,6 +102,9 @@ struct P2PArgs {
   int my_rank;
   int bucket, nbuckets;             // bucket of a single-bucket launch, -1 for all buckets
   int discard;                      // drop dead stage / receive lines from L2 (no write-back)
+  int experiment;                   // SESGD_OPT_EXPERIMENT (measurement only)
+  int protocol;                     // SESGD_OPT_PROTOCOL: 0 epoch flags, 1 value-carried (sentinel)
+  int cooperative;                  // SESGD_OPT_COOPERATIVE: cooperative launch (co-residency)
   int8_t my_workers[SESGD_MAX_WORKERS];      // global ids of local slots
   int8_t my_pos[SESGD_MAX_WORKERS];          // position of each local slot in its group
   int8_t slot_kind[SESGD_MAX_WORKERS];       // 0: group has remote members; 1: all-local group,
@@ -126,6 +129,7 @@ struct RingArgs {
   unsigned int *abort_dev;
   float lr, mu, wd;
   int parity, steps, m, pos, grid, my_rank, bucket, nbuckets;
+  int cooperative;
   int8_t ring_rank[SESGD_MAX_WORKERS];  // rank of ring position 0..m-1 (ascending worker id)
 };
 cudaError_t launch_ring(const RingArgs &a, int mode, cudaStream_t stream);
@@ -145,6 +149,10 @@ int p2p_occupancy(int variant, int r, int mode, bool vec, size_t smem);
 // tma: pushes staged in shared memory and sent with cp.async.bulk (SESGD_OPT_PUSH_TMA)
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream);
 int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi);
+// K4W (SESGD_OPT_PROTOCOL = 2): warp-specialised two-shot, one worker per GPU, one CTA per SM
+cudaError_t launch_p2p_ws(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
+int p2p_ws_occupancy(int m);
+int p2p_ws_threads();
 
 }  // namespace sesgd
 
@@ -185,6 +193,9 @@ struct sesgd_ctx {
   int64_t local_period = 1; // SESGD_OPT_LOCAL_PERIOD (Local-SESGD)
   char *mc_ws = nullptr;    // sesgd_attach_multicast (SESGD_PATH_NVLS)
   int payload_bf16 = 0;     // SESGD_OPT_PAYLOAD_BF16
+  int experiment = 0;       // SESGD_OPT_EXPERIMENT
+  int protocol = 0;         // SESGD_OPT_PROTOCOL (two-shot kernel)
+  int cooperative = 1;      // SESGD_OPT_COOPERATIVE
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)

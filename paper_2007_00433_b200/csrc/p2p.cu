@@ -190,7 +190,55 @@ __device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
 }
 
 // what a timed-out wait was waiting for (reported through sesgd_last_error)
-enum WaitKind : int { kWaitConsumed = 1, kWaitReady = 2, kWaitStaged = 3, kWaitSent = 4 };
+enum WaitKind : int { kWaitConsumed = 1, kWaitReady = 2, kWaitStaged = 3, kWaitSent = 4, kWaitData = 6 };
+
+// ---- value-carried validity (SESGD_OPT_PROTOCOL = 1): a receive slot float holds kSentinel until
+// the peer's value lands.  A 32-bit aligned access is single-copy atomic (PTX memory model), so a
+// float is either the sentinel or the whole new value: the receiver polls the data itself and the
+// sender needs no fence and no flag.  kSentinel is a NaN bit pattern GPU arithmetic never produces
+// (canonical NaN is 0x7FFFFFFF); a payload equal to it is sent as the canonical NaN.  After reading,
+// the receiver re-arms the float with kSentinel; the per-launch `consumed` release orders those
+// re-arms before the peer's next use of the slot (two calls later).
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+__device__ __forceinline__ float unsentinel(float v) {
+  return __float_as_uint(v) == kSentinel ? __uint_as_float(0x7FFFFFFFu) : v;
+}
+template <int W>
+__device__ __forceinline__ void st_sent(float *p, const float (&r)[W], int nvalid) {
+  if constexpr (W == 4) {
+    if (nvalid >= 4) {
+      asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(unsentinel(r[0])),
+                   "f"(unsentinel(r[1])), "f"(unsentinel(r[2])), "f"(unsentinel(r[3]))
+                   : "memory");
+      return;
+    }
+  }
+  for (int w = 0; w < W; ++w)
+    if (w < nvalid) asm volatile("st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p + w), "f"(unsentinel(r[w])) : "memory");
+}
+__device__ __forceinline__ float ld_relaxed1(const float *p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ld_relaxed4(const float *p, float (&r)[4]) {
+  asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+               : "l"(p)
+               : "memory");
+}
+template <int W>
+__device__ __forceinline__ void rearm(float *p, int nvalid) {
+  const float s = __uint_as_float(kSentinel);
+  if constexpr (W == 4) {
+    if (nvalid >= 4) {
+      *reinterpret_cast<float4 *>(p) = make_float4(s, s, s, s);
+      return;
+    }
+  }
+  for (int w = 0; w < W; ++w)
+    if (w < nvalid) p[w] = s;
+}
 
 // spin until *p >= target (sys-scope acquire); on timeout the first CTA to give up
 // latches SESGD_ETIMEOUT plus a description of the flag in the host-mapped block
@@ -220,6 +268,53 @@ __device__ uint64_t wait_geq(const P2PArgs &a, const uint64_t *p, uint64_t targe
       return target;
     }
   }
+}
+
+// poll `nvalid` floats at p until none is the sentinel (timeout latches SESGD_ETIMEOUT), then re-arm
+template <int W>
+__device__ __forceinline__ void ld_poll(const P2PArgs &a, float *p, float (&r)[W], int nvalid, int worker,
+                                        int pos) {
+  auto pending = [&]() {
+    bool any = false;
+#pragma unroll
+    for (int w = 0; w < W; ++w) any |= (w < nvalid) && __float_as_uint(r[w]) == kSentinel;
+    return any;
+  };
+  auto load = [&]() {
+    if constexpr (W == 4) {
+      if (nvalid >= 4) {
+        ld_relaxed4(p, r);
+        return;
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) r[w] = (w < nvalid) ? ld_relaxed1(p + w) : 0.f;
+  };
+  load();
+  if (pending()) {
+    const uint64_t t0 = dev::globaltimer();
+    do {
+      if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;
+      if (dev::globaltimer() - t0 > a.timeout_ns) {
+        if (atomicExch(a.abort_dev, 1u) == 0u) {
+          unsigned long long *e = a.err_host;
+          e[1] = (unsigned long long)kWaitData;
+          e[2] = blockIdx.x;
+          e[3] = 0;
+          e[4] = uint64_t(a.call) + 1;
+          e[5] = (unsigned long long)worker;
+          e[6] = (unsigned long long)pos;
+          e[7] = (unsigned long long)a.my_rank;
+          __threadfence_system();
+          atomicExch(e, (unsigned long long)(-SESGD_ETIMEOUT));
+          __threadfence_system();
+        }
+        break;
+      }
+      load();
+    } while (pending());
+  }
+  rearm<W>(p, nvalid);
 }
 
 __device__ __forceinline__ void hop_delay(const P2PArgs &a) {
@@ -272,7 +367,7 @@ struct Split {
     return reinterpret_cast<float *>(a.ws[a.my_rank] + a.stage_off) + int64_t(slot) * a.region_floats;
   }
   __device__ __forceinline__ float *recv(int worker, int pos) const {  // worker's receive slot
-    char *base = a.ws[a.worker_rank[worker]] + a.recv_off;
+    char *base = a.ws[(a.experiment & 2) ? a.my_rank : a.worker_rank[worker]] + a.recv_off;
     const int64_t region = (int64_t(a.parity) * a.r + a.worker_slot[worker]) * a.m + pos;
     return reinterpret_cast<float *>(base) + region * a.region_floats;
   }
@@ -1048,7 +1143,7 @@ struct Split {
     __syncthreads();
   }
 
-  template <bool TMA, bool MULTI, bool NV = false, bool BF = false>
+  template <bool TMA, bool MULTI, bool NV = false, bool BF = false, bool SENT = false>
   __device__ void ts_rs_stage(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     const int S = ts_slice();
@@ -1101,6 +1196,8 @@ struct Split {
           st_slot<W>(stage(s) + c.soff + e, val, nv);  // read in place by the local owner
         } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
           st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
+        } else if constexpr (SENT) {
+          st_sent<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store, validity in the value
         } else {
           st_slot<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store
         }
@@ -1132,7 +1229,8 @@ struct Split {
       __syncwarp();
     }
     if constexpr (NV) fence_proxy_alias();  // NVLS: multicast stores before the unicast flags
-    dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
+    if (!(a.experiment & 1))    // (SESGD_OPT_EXPERIMENT bit 0: measurement only)
+      dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
     const int64_t nrs = (rs1 - rs0) * pairs, nall = nrs + (ag1 - ag0) * pairs;
     for (int64_t q = threadIdx.x; q < nall; q += 32) {
       const int kind = q < nrs ? 0 : 1;
@@ -1163,7 +1261,7 @@ struct Split {
     __syncthreads();
   }
 
-  template <bool TMA, bool MULTI, bool NV = false, bool BF = false>
+  template <bool TMA, bool MULTI, bool NV = false, bool BF = false, bool SENT = false>
   __device__ void ts_reduce(int64_t g, float *ent) const {
     const ChunkRef c = locate(g);
     if (TMA && threadIdx.x == 0) dev::bulk_wait_read<kPushRing - 1>();  // entry free (+ sync below)
@@ -1171,7 +1269,7 @@ struct Split {
       nv_reduce(g);
       return;
     }
-    ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 1);
+    if constexpr (!SENT) ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 1);  // SENT: polled per value below
     const int64_t len = c.e1 - c.e0;
     for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
       if (MULTI && a.slot_kind[s] != 0) continue;
@@ -1185,10 +1283,12 @@ struct Split {
         float acc[W];
         for (int rr = 0; rr < a.m; ++rr) {  // ascending position = ascending worker id
           const int w = G[rr];
-          const float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
+          float *src = rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w]);
           float y[W];
           if constexpr (BF)
             ld_bf<W>(reinterpret_cast<const __nv_bfloat16 *>(src + c.soff + c.e0 + lo) + (o - lo), y, nv);
+          else if (SENT && rem<MULTI>(w))
+            ld_poll<W>(a, src + c.soff + e, y, nv, me, rr);
           else
             ld_slot<W>(src + c.soff + e, y, nv);
 #pragma unroll
@@ -1201,7 +1301,10 @@ struct Split {
         for (int rr = 0; rr < a.m; ++rr) {  // apply to every member: here directly, else push
           const int w = G[rr];
           if (rem<MULTI>(w)) {
-            if (!bulk) st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
+            if constexpr (SENT)
+              st_sent<W>(recv(w, p) + c.soff + e, acc, nv);
+            else if (!bulk)
+              st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
             continue;
           }
           const int sl = a.worker_slot[w];
@@ -1238,6 +1341,7 @@ struct Split {
           for (int64_t o = lo + int64_t(threadIdx.x) * 32; o + 32 <= hi; o += int64_t(kThreads) * 32)
             for (int rr = 0; rr < a.m; ++rr) {
               const int w = G[rr];
+              if (SENT && rem<MULTI>(w)) continue;  // re-armed receive lines stay (not dead)
               discard_l2((rem<MULTI>(w) ? recv(me, rr) : stage(a.worker_slot[w])) + c.soff + c.e0 + o);
             }
         }
@@ -1247,14 +1351,14 @@ struct Split {
   }
 
   // the slices owned by remote members: their means arrived in my receive slots
-  template <bool MULTI, bool NV = false>
+  template <bool MULTI, bool NV = false, bool SENT = false>
   __device__ void ts_finish(int64_t g) const {
     const ChunkRef c = locate(g);
     if constexpr (NV) {
       nv_finish(g);
       return;
     }
-    ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 2);
+    if constexpr (!SENT) ts_wait<MULTI>(g, 2 * uint64_t(a.call) + 2);  // SENT: polled per value
     const int64_t len = c.e1 - c.e0;
     for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
       if (MULTI && a.slot_kind[s] != 0) continue;
@@ -1264,12 +1368,15 @@ struct Split {
       for (int j = 0; j < a.m; ++j) {
         if (j == a.my_pos[s] || !rem<MULTI>(G[j])) continue;
         const int64_t lo = ts_lo(j, len), hi = ts_hi(j, len);
-        const float *src = recv(me, j) + c.soff;
+        float *src = recv(me, j) + c.soff;
         for (int64_t o = lo + int64_t(threadIdx.x) * W; o < hi; o += int64_t(kThreads) * W) {
           const int64_t e = c.e0 + o;
           const int nv = (int)min(int64_t(W), hi - o);
           float y[W];
-          ld_slot<W>(src + e, y, nv);
+          if constexpr (SENT)
+            ld_poll<W>(a, src + e, y, nv, me, j);
+          else
+            ld_slot<W>(src + e, y, nv);
           if constexpr (!GRAD) {
             store_m<W>(xs + e, y, nv);
           } else {
@@ -1288,7 +1395,7 @@ struct Split {
       }
     }
     __syncthreads();
-    if constexpr (W == 4) {
+    if constexpr (W == 4 && !SENT) {  // SENT: the receive lines were re-armed, they stay
       if (a.discard) {
         for (int s = 0; s < (MULTI ? a.r : 1); ++s) {
           if (MULTI && a.slot_kind[s] != 0) continue;
@@ -1311,7 +1418,7 @@ struct Split {
   // last step may still be in flight).  A chunk pushed at step s is released by step
   // s + D + R - 1, so with reduce L >= D + R - 1 steps after rs_stage (and finish L after
   // reduce) every wait targets a flag released at the top of this step or an earlier one.
-  template <bool TMA, bool MULTI, bool NV = false, bool BF = false>
+  template <bool TMA, bool MULTI, bool NV = false, bool BF = false, bool SENT = false>
   __device__ void compute_twoshot(int i, float *ring) const {
     const int64_t first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
     const int64_t nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
@@ -1328,7 +1435,7 @@ struct Split {
     __syncthreads();
     const int D = TMA ? max(a.release_delay, 2) : max(a.release_delay, 1);
     const int R = max(a.release_every, 1);
-    const int L = max(a.lag, D + R - 1);
+    const int L = SENT ? max(a.lag, 1) : max(a.lag, D + R - 1);  // SENT: no release schedule
     auto groups_of = [&](int64_t k) {  // bulk groups committed in step k
       return int(k >= 0 && k < nk) + int(k >= L && k - L < nk);
     };
@@ -1340,7 +1447,11 @@ struct Split {
     for (int64_t k = 0; k < nk + 2 * L; ++k) {
       // pushes of steps <= k - D: RS of ordinals < k-D+1, AG of < k-D-L+1; with stagger the CTAs
       // of an SM take their release steps in turn instead of all at once
-      if ((k + (a.release_stagger ? i : 0)) % R == 0) {
+      if (SENT && a.hop_delay_ns && (k == 0 || k == L)) {  // config 4: one delay per round
+        if (threadIdx.x == 0) hop_delay(a);
+        __syncthreads();
+      }
+      if (!SENT && (k + (a.release_stagger ? i : 0)) % R == 0) {
         const int64_t rs1 = clampk(k - D + 1), ag1 = clampk(k - D - L + 1);
         int newer = 0;
         if constexpr (TMA)
@@ -1355,7 +1466,7 @@ struct Split {
         t0 = t1;
       }
       if (k < nk) {
-        ts_rs_stage<TMA, MULTI, NV, BF>(first + k * gc, ring + (q % kPushRing) * kChunk);
+        ts_rs_stage<TMA, MULTI, NV, BF, SENT>(first + k * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1364,7 +1475,7 @@ struct Split {
         t0 = t1;
       }
       if (k >= L && k - L < nk) {
-        ts_reduce<TMA, MULTI, NV, BF>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
+        ts_reduce<TMA, MULTI, NV, BF, SENT>(first + (k - L) * gc, ring + (q % kPushRing) * kChunk);
         q += TMA ? 1 : 0;
       }
       if (a.prof) {
@@ -1372,7 +1483,7 @@ struct Split {
         t_red += t1 - t0;
         t0 = t1;
       }
-      if (k >= 2 * L && k - 2 * L < nk) ts_finish<MULTI, NV>(first + (k - 2 * L) * gc);
+      if (k >= 2 * L && k - 2 * L < nk) ts_finish<MULTI, NV, SENT>(first + (k - 2 * L) * gc);
       if (a.prof) {
         const uint64_t t1 = dev::globaltimer();
         t_fin += t1 - t0;
@@ -1445,14 +1556,14 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
     p.compute_direct(blockIdx.x);
 }
 
-template <int W, bool GRAD, bool TMA, bool MULTI, bool NV = false, bool BF = false>
+template <int W, bool GRAD, bool TMA, bool MULTI, bool NV = false, bool BF = false, bool SENT = false>
 __global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];  // TMA: kPushRing chunk images
   const Split<W, GRAD> p(a);
   if (a.m == 1)
     p.local_only();
   else
-    p.template compute_twoshot<TMA, MULTI, NV, BF>(blockIdx.x, reinterpret_cast<float *>(dsmem));
+    p.template compute_twoshot<TMA, MULTI, NV, BF, SENT>(blockIdx.x, reinterpret_cast<float *>(dsmem));
 }
 
 constexpr size_t kTwoshotTmaSmem = size_t(Split<4, false>::kPushRing) * size_t(kChunk) * 4;  // 48 KiB
@@ -1487,6 +1598,16 @@ const void *pick_bf16_t(int mode, bool vec) {
 }
 const void *pick_bf16(int mode, bool vec, bool multi) {
   return multi ? pick_bf16_t<true>(mode, vec) : pick_bf16_t<false>(mode, vec);
+}
+// value-carried validity (SESGD_OPT_PROTOCOL = 1): LSU pushes, fp32, one or several workers per GPU
+template <bool MULTI>
+const void *pick_sent_t(int mode, bool vec) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (vec)
+    return grad ? reinterpret_cast<const void *>(&k4_twoshot<4, true, false, MULTI, false, false, true>)
+                : reinterpret_cast<const void *>(&k4_twoshot<4, false, false, MULTI, false, false, true>);
+  return grad ? reinterpret_cast<const void *>(&k4_twoshot<1, true, false, MULTI, false, false, true>)
+              : reinterpret_cast<const void *>(&k4_twoshot<1, false, false, MULTI, false, false, true>);
 }
 // TMA pushes: one worker per GPU only; several workers per GPU: the MULTI kernel
 const void *pick_twoshot(int mode, bool vec, bool tma, bool multi) {
@@ -1539,7 +1660,7 @@ cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
-  return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
+  return launch_persistent(k, unsigned(a.grid), kThreads, args, smem, stream, a.cooperative != 0);
 }
 
 int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
@@ -1558,16 +1679,24 @@ int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {
   int blocks = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, smem) != cudaSuccess)
     return 1;
+  if (!tma) {  // the value-carried protocol's kernels share the grid
+    int sb = 0;
+    const void *ks = multi ? pick_sent_t<true>(mode, vec) : pick_sent_t<false>(mode, vec);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sb, ks, kThreads, 0) == cudaSuccess && sb > 0 && sb < blocks)
+      blocks = sb;
+  }
   return blocks > 0 ? blocks : 1;
 }
 
 cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, cudaStream_t stream) {
   const void *k = a.mc_ws ? pick_nvls(mode, vec)
-                 : a.payload_bf16 ? pick_bf16(mode, vec, a.r > 1) : pick_twoshot(mode, vec, tma, a.r > 1);
+                 : a.payload_bf16 ? pick_bf16(mode, vec, a.r > 1)
+                 : a.protocol == 1 ? (a.r > 1 ? pick_sent_t<true>(mode, vec) : pick_sent_t<false>(mode, vec))
+                                   : pick_twoshot(mode, vec, tma, a.r > 1);
   const size_t smem = tma ? kTwoshotTmaSmem : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
-  return cudaLaunchKernel(k, dim3(a.grid), dim3(kThreads), args, smem, stream);
+  return launch_persistent(k, unsigned(a.grid), kThreads, args, smem, stream, a.cooperative != 0);
 }
 
 }  // namespace sesgd

@@ -223,7 +223,7 @@ int ring_occupancy(int mode) {
 
 cudaError_t launch_ring(const RingArgs &a, int mode, cudaStream_t stream) {
   void *args[] = {const_cast<RingArgs *>(&a)};
-  return cudaLaunchKernel(pick(mode), dim3(a.grid), dim3(kRingThreads), args, 0, stream);
+  return launch_persistent(pick(mode), unsigned(a.grid), kRingThreads, args, 0, stream, a.cooperative != 0);
 }
 
 }  // namespace sesgd

@@ -99,6 +99,7 @@ void freeze_layout(sesgd_ctx *ctx) {
   // every CTA must be co-resident (COMM and COMPUTE wait on each other): grid = SMs x
   // occupancy, with the COMM guard cache (pairs x Gc u64) in dynamic shared memory
   int grid = ctx->sm_count * occupancy(sesgd::p2p_smem_bytes(var, 0, 0));
+  if (ctx->protocol == 2) grid = ctx->sm_count * sesgd::p2p_ws_occupancy(ctx->m);  // K4W: CTA per SM
   if (ctx->grid_opt > 0 && ctx->grid_opt < grid) grid = int(ctx->grid_opt);
   size_t smem = sesgd::p2p_smem_bytes(var, pairs, grid);
   const int grid2 = ctx->sm_count * occupancy(smem);
@@ -120,6 +121,7 @@ void freeze_layout(sesgd_ctx *ctx) {
   h = fnv(h, uint64_t(chunk));
   h = fnv(h, uint64_t(comm));
   h = fnv(h, uint64_t(ctx->comm_batch));
+  h = fnv(h, uint64_t(ctx->protocol));
   for (size_t b = 0; b < ctx->buckets.size(); ++b) {
     sesgd_bucket &bk = ctx->buckets[b];
     bk.stage_bucket_off = off;
@@ -390,6 +392,9 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.bucket = bucket;
   a.nbuckets = int(ctx->buckets.size());
   a.discard = ctx->discard;
+  a.experiment = ctx->experiment;
+  a.protocol = ctx->protocol;
+  a.cooperative = ctx->cooperative;
   for (int s = 0; s < ctx->n_local; ++s) {
     const int me = ctx->local_workers[s];
     a.my_workers[s] = int8_t(me);
@@ -412,9 +417,11 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   bool vec = true;
   for (size_t b = 0; b < ctx->buckets.size(); ++b)
     if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
-  cudaError_t e = twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
-                          : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
-                                                      ctx->guard_smem, st);
+  cudaError_t e = (twoshot && ctx->protocol == 2 && !nvls)
+                      ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
+                  : twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
+                            : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
+                                                        ctx->guard_smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
   // bookkeeping
   int remote_peers = 0;
@@ -608,6 +615,19 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "discard must be 0 or 1");
       ctx->discard = int(value);
       return SESGD_OK;
+    case SESGD_OPT_PROTOCOL:
+      if (value < 0 || value > 2) return fail(ctx, SESGD_EINVAL, "protocol must be 0, 1 or 2");
+      if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "the protocol is fixed once the layout freezes");
+      ctx->protocol = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_COOPERATIVE:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "cooperative must be 0 or 1");
+      ctx->cooperative = int(value);
+      return SESGD_OK;
+    case SESGD_OPT_EXPERIMENT:
+      if (value < 0 || value > 3) return fail(ctx, SESGD_EINVAL, "experiment bits must be in [0, 3]");
+      ctx->experiment = int(value);
+      return SESGD_OK;
     case SESGD_OPT_HOP_DELAY_NS:
       if (value < 0) return fail(ctx, SESGD_EINVAL, "delay must be >= 0");
       ctx->hop_delay_ns = value;
@@ -733,8 +753,12 @@ int sesgd_workspace_prepare(sesgd_ctx *ctx, void *local_ws) {
   int64_t bytes = 0;
   int rc = sesgd_workspace_bytes(ctx, &bytes);
   if (rc != SESGD_OK) return rc;
-  // zero flags (stage contents are don't-care), then the header
+  // zero flags (stage contents are don't-care), then the header; the value-carried protocol
+  // arms every receive float with the sentinel (0xFFFFFFFF)
   cudaError_t e = cudaMemset(local_ws, 0, size_t(ctx->stage_off));
+  if (e == cudaSuccess && ctx->protocol >= 1)
+    e = cudaMemset(static_cast<char *>(local_ws) + ctx->recv_off, 0xFF,
+                   size_t(2 * int64_t(ctx->n_local) * ctx->m * ctx->stage_slot_floats * 4));
   uint64_t hdr[2] = {kMagic, ctx->layout_hash};
   if (e == cudaSuccess) e = cudaMemcpy(local_ws, hdr, sizeof(hdr), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -883,6 +907,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     ra.my_rank = ctx->rank;
     ra.bucket = bucket;
     ra.nbuckets = int(ctx->buckets.size());
+    ra.cooperative = ctx->cooperative;
     const int me = ctx->local_workers[0];
     const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
     for (int q = 0; q < ctx->m; ++q) {
@@ -910,6 +935,10 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     return fail(ctx, SESGD_ENOTSUP, "two-shot needs the DIRECT layout; its TMA pushes one worker per GPU");
   if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma))
     return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path with LSU pushes");
+  if (ctx->protocol >= 1 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma || ctx->payload_bf16))
+    return fail(ctx, SESGD_ENOTSUP, "the value-carried protocol needs the fp32 two-shot path with LSU pushes");
+  if (ctx->protocol == 2 && ctx->n_local != 1)
+    return fail(ctx, SESGD_ENOTSUP, "protocol 2 (warp-specialised K4W) needs one worker per GPU");
   if (path == SESGD_PATH_NVLS && (ctx->p2p_variant != 0 || ctx->n_local != 1 || ctx->m != ctx->n || !ctx->mc_ws))
     return fail(ctx, SESGD_ENOTSUP,
                 "the NVLS path needs one worker per GPU, group_size = n and sesgd_attach_multicast");
@@ -987,6 +1016,10 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
   }
   if (ctx->payload_bf16 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma))
     return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path with LSU pushes");
+  if (ctx->protocol >= 1 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma || ctx->payload_bf16))
+    return fail(ctx, SESGD_ENOTSUP, "the value-carried protocol needs the fp32 two-shot path with LSU pushes");
+  if (ctx->protocol == 2 && ctx->n_local != 1)
+    return fail(ctx, SESGD_ENOTSUP, "protocol 2 (warp-specialised K4W) needs one worker per GPU");
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
   return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot, nvls);
 }

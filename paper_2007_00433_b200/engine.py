@@ -31,7 +31,7 @@ class SESGDEngine:
                  rank: int = 0, world: int = 1, process_group=None, path: int = C.PATH_AUTO,
                  grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0,
                  p2p_variant: int = -1, discard: int = 1, options: Optional[dict] = None,
-                 weight_decay: float = 0.0, loopback: bool = False):
+                 weight_decay: float = 0.0, loopback: bool = False, manual_peers: bool = False):
         if n % world != 0:
             raise ValueError("n must be a multiple of the number of ranks")
         self.n, self.m, self.seed = n, group_size, seed
@@ -79,6 +79,12 @@ class SESGDEngine:
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             C.sesgd_workspace_prepare(self.ctx, self.workspace.data_ptr())
             self.stream = torch.cuda.Stream(device=self.device)
+        elif world > 1 and manual_peers:
+            # the caller maps the peers' workspaces itself (e.g. CUDA IPC, tools/ipc_pair.py) and
+            # calls attach_peers(pointers): no process group, no NCCL
+            nbytes = C.sesgd_workspace_bytes(self.ctx)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            C.sesgd_workspace_prepare(self.ctx, self.workspace.data_ptr())
         elif world > 1:
             self._attach_peers(process_group)
         elif path == C.PATH_ONESHOT:
@@ -112,6 +118,10 @@ class SESGDEngine:
                 raise RuntimeError("SESGD_PATH_NVLS needs NVSwitch multicast (no multicast_ptr)")
             C.sesgd_attach_multicast(self.ctx, mc)
         dist.barrier(group=group)
+
+    def attach_peers(self, ptrs) -> None:
+        """manual_peers: every rank's workspace pointer, mapped in this process"""
+        C.sesgd_attach_peers(self.ctx, self.world, self.rank, list(ptrs), self.worker_rank)
 
     # -------------------------------------------------------------- views
     def view(self, flat: torch.Tensor, b: int) -> torch.Tensor:

@@ -21,7 +21,8 @@ from paper_2007_00433_b200.engine import SESGDEngine  # noqa: E402
 def _options(a):
     return {k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
                               (C.OPT_PUSH_TMA, a.tma), (C.OPT_LOCAL_PERIOD, a.period),
-                              (C.OPT_SCHEDULE, a.schedule), (C.OPT_PAYLOAD_BF16, a.bf16)) if v}
+                              (C.OPT_SCHEDULE, a.schedule), (C.OPT_PAYLOAD_BF16, a.bf16),
+                              (C.OPT_PROTOCOL, a.protocol)) if v}
 
 
 def _padded(idx, buckets, offsets):
@@ -95,6 +96,7 @@ def main():
     p.add_argument("--consensus", type=int, default=0)
     p.add_argument("--wd", type=float, default=0.0)
     p.add_argument("--bf16", type=int, default=0)
+    p.add_argument("--protocol", type=int, default=0)
     p.add_argument("--loopback", type=int, default=0)
     p.add_argument("--coords", default="")
     p.add_argument("--out", required=True)

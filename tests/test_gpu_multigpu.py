@@ -43,7 +43,7 @@ def _free_port():
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
             lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
-            bf16=0, coords=None):
+            bf16=0, coords=None, protocol=0):
     """`gpus` ranks: processes on as many GPUs (nvlink) or virtual ranks on cuda:0 (loopback)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -66,7 +66,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
-               "--bf16", str(bf16), "--loopback", str(gpus if loop else 0), *extra,
+               "--bf16", str(bf16), "--protocol", str(protocol), "--loopback", str(gpus if loop else 0), *extra,
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -443,5 +443,119 @@ def test_two_gpus_bf16_payload_several_workers_per_gpu(tmp_path, n, m, mode):
     v = np.zeros_like(x)
     oracle.run_local(n, m, 42, 5, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
                      payload_bf16=True)
+    _compare(X, x)
+    _compare(V, v)
+
+
+# ---------------------------------------------------------------- K4, value-carried validity
+# SESGD_OPT_PROTOCOL = 1: no flags and no sender fence; every receive float is armed with a
+# sentinel NaN, the receiver polls the values themselves and re-arms them.  Same bits as the
+# oracle (the arithmetic and fold order are K4's).
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_two_gpus_twoshot_value_protocol(tmp_path, mode, fused):
+    buckets = [100003, 7, 40000, 4096]
+    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused, path=4, protocol=1)
+    x, v = _oracle(2, 2, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("lag,grid", [(1, 8), (2, 24), (3, 0), (64, 4)])
+def test_two_gpus_value_protocol_pipeline_shapes(tmp_path, lag, grid):
+    """many chunks per CTA and every lag: slots are re-armed and reused (call parity) across 5
+    iterations, including CTAs whose whole chunk list sits inside one lag"""
+    buckets = [250001, 13, 70000]
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, grid=grid, lag=lag, path=4, protocol=1)
+    x, v = _oracle(2, 2, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("n,m,mode", [(8, 2, 0), (8, 4, 1), (4, 2, 1)])
+def test_two_gpus_value_protocol_several_workers_per_gpu(tmp_path, n, m, mode):
+    """MULTI: co-resident members through the stage, remote ones through re-armed slots"""
+    buckets = [60001, 4097]
+    X, V = _launch(tmp_path, 2, n, m, 6, buckets, mode, path=4, protocol=1)
+    x, v = _oracle(n, m, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_four_gpus_value_protocol(tmp_path, m):
+    buckets = [200003, 5000, 1]
+    X, V = _launch(tmp_path, 4, 4, m, 5, buckets, path=4, protocol=1)
+    x, v = _oracle(4, m, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("gpus", [8, 2])
+def test_value_protocol_resnet50_bench_shape(tmp_path, gpus):
+    """cfg 2 at full size (n = 8, m = 2, 5 ResNet-50 buckets, T = 100) through protocol 1"""
+    from paper_2007_00433_b200.workloads import RESNET50_BUCKETS
+    buckets = list(RESNET50_BUCKETS)
+    coords = _sample(buckets)
+    X, V = _launch(tmp_path, gpus, 8, 2, 100, buckets, coords=coords, path=4, protocol=1)
+    x, v = _oracle(8, 2, sum(buckets), 100, 0, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
+
+
+# ---------------------------------------------------------------- K4W: warp-specialised two-shot
+# SESGD_OPT_PROTOCOL = 2 (one worker per GPU, one CTA per SM): stream / fold / gather warp groups
+# joined only by a shared-memory ring (mbarriers) and by value-carried validity over NVLink.
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_two_gpus_k4w(tmp_path, mode, fused):
+    buckets = [100003, 7, 40000, 4096]
+    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused, path=4, protocol=2)
+    x, v = _oracle(2, 2, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("grid", [1, 3, 8])
+def test_two_gpus_k4w_small_grids(tmp_path, grid):
+    """many chunks per CTA: the ring wraps (S waits for R to free entries) and the receive slots
+    of both call parities are re-armed and reused over 5 iterations"""
+    buckets = [250001, 13, 70000]
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, grid=grid, path=4, protocol=2)
+    x, v = _oracle(2, 2, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("m,mode", [(2, 0), (4, 0), (4, 1)])
+def test_four_gpus_k4w(tmp_path, m, mode):
+    buckets = [200003, 5000, 1]
+    X, V = _launch(tmp_path, 4, 4, m, 5, buckets, mode, path=4, protocol=2)
+    x, v = _oracle(4, m, sum(buckets), 5, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_k4w_resnet50_north_star_shape(tmp_path):
+    """the north star's 8-GPU layout: n = 8 workers, one per rank, group_size 2, the five
+    ResNet-50 buckets at full size, T = 100, through K4W; sampled coordinates vs the oracle"""
+    from paper_2007_00433_b200.workloads import RESNET50_BUCKETS
+    buckets = list(RESNET50_BUCKETS)
+    coords = _sample(buckets)
+    X, V = _launch(tmp_path, 8, 8, 2, 100, buckets, coords=coords, path=4, protocol=2)
+    x, v = _oracle(8, 2, sum(buckets), 100, 0, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("protocol,mode", [(1, 0), (2, 0), (2, 1)])
+def test_two_gpus_value_protocols_weight_decay(tmp_path, protocol, mode):
+    buckets = [65537, 3]
+    T, wd = 5, 1e-2
+    X, V = _launch(tmp_path, 2, 2, 2, T, buckets, mode, path=4, wd=wd, protocol=protocol)
+    x = np.tile(synth.x0_host(sum(buckets)), (2, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(2, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
+                     weight_decay=wd)
     _compare(X, x)
     _compare(V, v)
