@@ -31,7 +31,6 @@ METRIC = "group sync+update GB/s per GPU & iters/s at 1/2/4/8 B200 (fraction of 
 N_WORKERS, GROUP_SIZE, LR, MU, SEED = 8, 2, 0.1, 0.9, 42
 BYTES_PER_WORKER_ELEM = 20  # algorithmic HBM bytes: read g, v, x; write v, x (fp32)
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md), nominal 900
-TAU_HOP_S = 2.6e-6          # measured one-way flag hop (K7 ping-pong, profiles/r01_latency_sweep_4gpu_v2.json)
 PAPER_CONTEXT = {"speedup_16w_0.1ms": 1.7, "speedup_16w_5ms": 5.0,
                  "source": "PAPER.md:7, P:411, P:436 (K80 + 1 Gbps Ethernet; end-to-end training, not this metric)"}
 
@@ -48,6 +47,8 @@ def parse():
     p.add_argument("--mode", default="param", choices=["param", "grad"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--second-workload", type=int, default=1,
+                   help="also time BASELINE cfg 3 (VGG-16, n=16, m=4) in the same run")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--p2p-variant", type=int, default=-1)
     p.add_argument("--discard", type=int, default=1)
@@ -269,89 +270,84 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU leg
-def run_sesgd(args):
+def engine_options(args, C):
+    return {k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch), (C.OPT_FOLD_LAG, args.fold_lag),
+                              (C.OPT_RESIDENT_UNROLL, args.resident_unroll), (C.OPT_PUSH_TMA, args.push_tma),
+                              (C.OPT_RELEASE_DELAY, args.release_delay), (C.OPT_RELEASE_EVERY, args.release_every),
+                              (C.OPT_RELEASE_STAGGER, args.release_stagger),
+                              (C.OPT_PAYLOAD_BF16, args.payload_bf16), (C.OPT_EXPERIMENT, args.experiment),
+                              (C.OPT_PROTOCOL, args.protocol)) if v}
+
+
+class Dist:
+    """rank / world / device plus the two collectives the timing needs (barrier, max over ranks)"""
+
+    def __init__(self, world, local):
+        import torch
+        self.world, self.local = world, local
+        self.dev = torch.device("cuda", local)
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max(self, v: float) -> float:
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
+    """Time K SESGD iterations (after W warm-up ones) of `workload` with n workers, group size m,
+    n / world per GPU; returns the per-workload fields of the JSON line (value, roofline, ...)."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     import synth
     from paper_2007_00433_b200 import sesgd as C
     from paper_2007_00433_b200.engine import SESGDEngine
     from paper_2007_00433_b200.workloads import WORKLOADS
 
-    rank, world, local = dist_env()
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    n, m = args.n, args.group_size
+    world = D.world
     if n % world:
         raise SystemExit("n must be a multiple of the GPU count")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    buckets = list(WORKLOADS[args.workload])
+    buckets = list(WORKLOADS[workload])
     L = sum(buckets)
     mode = C.MODE_PARAM_AVG if args.mode == "param" else C.MODE_GRAD_AVG
+    path = {"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
+            "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT, "nvls": C.PATH_NVLS}[args.path]
     eng = SESGDEngine(n, m, buckets, seed=SEED, mode=mode, rank=rank, world=world,
                       p2p_variant=args.p2p_variant, discard=args.discard, grid=args.grid,
-                      options={k: v for k, v in ((C.OPT_COMM_BATCH, args.comm_batch),
-                                                 (C.OPT_FOLD_LAG, args.fold_lag),
-                                                 (C.OPT_RESIDENT_UNROLL, args.resident_unroll),
-                                                 (C.OPT_PUSH_TMA, args.push_tma),
-                                                 (C.OPT_RELEASE_DELAY, args.release_delay),
-                                                 (C.OPT_RELEASE_EVERY, args.release_every),
-                                                 (C.OPT_RELEASE_STAGGER, args.release_stagger),
-                                                 (C.OPT_PAYLOAD_BF16, args.payload_bf16),
-                                                 (C.OPT_EXPERIMENT, args.experiment),
-                                                 (C.OPT_PROTOCOL, args.protocol)) if v},
-                      path={"auto": C.PATH_AUTO, "resident": C.PATH_RESIDENT, "oneshot": C.PATH_ONESHOT,
-                            "ring": C.PATH_RING, "twoshot": C.PATH_TWOSHOT, "nvls": C.PATH_NVLS}[args.path])
+                      options=engine_options(args, C), path=path)
     r = eng.r
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.current_stream(D.dev)
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     for s, w in enumerate(eng.local_workers):
         for b, Lb in enumerate(buckets):
             synth.fill_x0_device(eng.x(s, b).data_ptr(), Lb, int(offs[b]), stream.cuda_stream)
             synth.fill_grad_device(eng.g(s, b).data_ptr(), Lb, int(offs[b]), w, 0, stream.cuda_stream)
     torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     nb = len(buckets)
-    # one-shot path: one fused launch per step (sesgd_sync_all); resident: one launch per bucket
     fused = bool(args.fused)  # one sesgd_sync_all launch per step (all buckets)
     launches_per_step = 1 if fused else nb  # event pairs per step
     kernels_per_step = nb if args.path == "ring" else launches_per_step  # K5 launches per bucket
     t_next = 0
-    for _ in range(args.warmup):
+    for _ in range(W):
         eng.step(t_next, LR, MU, stream, fused=fused)
         t_next += 1
     eng.poll()
-    K = args.steps
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(launches_per_step)] for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nvl_ctr = None
-    if world > 1:  # NVLink TX/RX byte counters (NVML) around the timed region, full-speed kernels
-        try:
-            sys.path.insert(0, os.path.join(ROOT, "tools"))
-            from nvml_nvlink import NvlinkCounters
-            nvl_ctr = NvlinkCounters(local)
-        except Exception:
-            nvl_ctr = None
-    barrier()
-    nvl0 = nvl_ctr.read() if nvl_ctr else None
-    with ClockSampler(local) as clk:
+    D.barrier()
+    with (clocks if clocks is not None else ClockSampler(D.local)) as clk:
         start.record(stream)
         for k in range(K):
             eng.begin_iter(t_next)
@@ -366,32 +362,18 @@ def run_sesgd(args):
                     ev[k][b][1].record(stream)
             t_next += 1
         end.record(stream)
-        barrier()
-    nvl1 = nvl_ctr.read() if nvl_ctr else None
+        D.barrier()
     eng.poll()
-    ms_total = max_over_ranks(start.elapsed_time(end))
-    nvlink_measured = None
-    if world > 1:  # every rank takes part in the max (-1: counter unavailable on that rank)
-        keys = ("data_tx", "data_rx", "raw_tx", "raw_rx")
-        d = {k: (-1.0 if nvl0 is None or nvl0[k] is None or nvl1[k] is None else (nvl1[k] - nvl0[k]) / K)
-             for k in keys}
-        d = {k: max_over_ranks(v) for k, v in d.items()}
-        if all(v >= 0 for v in d.values()):  # max over ranks of each GPU's bytes per step
-            nvlink_measured = {f"{k}_bytes_per_step": v for k, v in d.items()}
-            nvlink_measured["source"] = ("NVML NVLink throughput counters (field ids 138-141, per-link "
-                                         "KiB, summed over links) read around the timed region; "
-                                         "max over ranks")
+    ms_total = D.max(start.elapsed_time(end))
     ms_step = ms_total / K
     launch_ms = [[e0.elapsed_time(e1) for (e0, e1) in ev[k]] for k in range(K)]
-    kern_ms_total = max_over_ranks(sum(map(sum, launch_ms)))
+    kern_ms_total = D.max(sum(map(sum, launch_ms)))
     # per-step kernel time distribution (median and p90), max over ranks
     step_ms = sorted(sum(row) for row in launch_ms)
-    kern_p50 = max_over_ranks(step_ms[(K - 1) // 2])
-    kern_p90 = max_over_ranks(step_ms[min(K - 1, int(0.9 * K))])
+    kern_p50 = D.max(step_ms[(K - 1) // 2])
+    kern_p90 = D.max(step_ms[min(K - 1, int(0.9 * K))])
     total_bytes = BYTES_PER_WORKER_ELEM * L * n  # whole job, per step
     value = total_bytes / (ms_step * 1e-3) / 1e9
-    per_gpu = value / world
-    # dominant kernel roofline (all timed launches are the one fused kernel)
     hbm_peak, peak_src = measured_peaks()
     algo_bytes_per_step_gpu = BYTES_PER_WORKER_ELEM * L * r
     resident = (world == 1 and args.path in ("auto", "resident"))
@@ -408,13 +390,13 @@ def run_sesgd(args):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        kernel = {"twoshot": "k4_twoshot", "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
+        kernel = {"twoshot": "k4w_twoshot" if (args.protocol == 2 and r == 1) else "k4_twoshot",
+                  "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
         # of them 2(s-1)/s * 4 B per element (co-resident members pre-combine); max over
         # GPUs, mean over the timed iterations.
-        nvl_steps = [nvlink_algo_bytes(eng.groups(t)[0], m, r, world, L)
-                     for t in range(t_next - K, t_next)]
+        nvl_steps = [nvlink_algo_bytes(eng.groups(t)[0], m, r, world, L) for t in range(t_next - K, t_next)]
         nvl_bytes = sum(nvl_steps) / len(nvl_steps)
         achieved_nvl = nvl_bytes * K / (kern_ms_total * 1e-3) / 1e9
         achieved_hbm = algo_bytes_per_step_gpu * K / (kern_ms_total * 1e-3) / 1e9
@@ -427,18 +409,13 @@ def run_sesgd(args):
         else:
             roof = {"bound": "hbm", "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_hbm / hbm_peak, "peak_source": peak_src}
-        if nvlink_measured is not None and nvl_bytes > 0:
-            tx = nvlink_measured["data_tx_bytes_per_step"]
-            nvlink_measured["tx_over_algorithmic"] = tx / nvl_bytes
-            nvlink_measured["tx_gbs"] = tx * K / (kern_ms_total * 1e-3) / 1e9
-        roof.update({"nvlink_measured": nvlink_measured})
         roof.update({"hbm_achieved": achieved_hbm, "nvlink_algo_bytes_per_step": nvl_bytes,
                      "t_roof_us": max(t_hbm, t_nvl) * 1e6, "kernel": kernel})
-    roof["traffic"] = traffic_for(kernel, f"{args.workload}_n{n}_m{m}_g{world}")
+    roof["traffic"] = traffic_for(kernel, f"{workload}_n{n}_m{m}_g{world}")
 
     # ---- e2e through the C-ABI host-buffer call (H2D of g, D2H of x inside the timed region)
     e2e = None
-    if args.e2e_steps > 0:
+    if e2e_steps > 0:
         g_host = [[torch.empty(Lb, dtype=torch.float32).pin_memory() for _ in range(r)] for Lb in buckets]
         x_host = [[torch.empty(Lb, dtype=torch.float32).pin_memory() for _ in range(r)] for Lb in buckets]
         for b in range(nb):
@@ -446,18 +423,18 @@ def run_sesgd(args):
                 g_host[b][s].copy_(eng.g(s, b))
         eng.step_host(t_next, LR, MU, g_host, x_host, stream)
         t_next += 1
-        barrier()
+        D.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.e2e_steps):
+        for _ in range(e2e_steps):
             eng.step_host(t_next, LR, MU, g_host, x_host, stream)
             t_next += 1
         e1.record(stream)
-        barrier()
-        e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.e2e_steps
+        D.barrier()
+        e2e_ms = D.max(e0.elapsed_time(e1)) / e2e_steps
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 4 * L * n, "d2h_bytes_per_step": 4 * L * n,
-               "ms_per_step": e2e_ms, "steps": args.e2e_steps,
+               "ms_per_step": e2e_ms, "steps": e2e_steps,
                "api": "sesgd_sync_all_host (pinned host g in, updated x out, every worker; H2D / "
                       "kernels / D2H of different buckets pipelined on copy streams)"}
         probe = pcie_probe()
@@ -468,54 +445,200 @@ def run_sesgd(args):
                                  "source": "tools/pcie_probe.py, profiles/r01_pcie_probe_g1.json "
                                            "(pinned H2D and D2H of the same bytes concurrently)"}
     eng.poll()
-
     stats = [eng.stats(b) for b in range(nb)]
     # consistency of the workers' parameters after the run (K9), outside the timed region
     css, cmx = eng.consensus(stream)
-    lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, TAU_HOP_S)
+    out = {
+        "config": {**common_config(workload, n, m, args.mode), "workers_per_gpu": r,
+                   "path": "resident (K6)" if resident else {
+                       "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P ("
+                                  + ("K4W, warp-specialised" if kernel == "k4w_twoshot" else "K4") + ")",
+                       "ring": "ring inside each group over NVLink P2P (K5)"}.get(
+                           eff_path, "one-shot push over NVLink P2P (K3)"),
+                   "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush"},
+        "value": value, "ms_per_step": ms_step, "steps": K, "warmup": W,
+        "iters_per_s": 1e3 / ms_step, "gbs_per_gpu": value / world,
+        "kernel_ms_per_step": {"p50": kern_p50, "p90": kern_p90},
+        "roofline": roof, "e2e": e2e, "gpu_launches": K * kernels_per_step,
+        "kernel_rounds_per_bucket": stats[0]["handshake_rounds"],
+        "consistency": {"after_iterations": t_next, "sum_sq_dev_from_mean": css,
+                        "rms_dev": (css / (n * L)) ** 0.5, "max_abs_dev": cmx,
+                        "note": "SESGD keeps the workers consistent (P:430-433); x0 ~ U[-1/8, 1/8)"},
+        "clocks": clk.summary() if clocks is None else None,
+        "L": L, "nb": nb,
+    }
+    eng.close()
+    del eng
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_tau(D, rank):
+    """Per-hop handshake latency t_tau (Eq. 2) in this run: K7 flag ping-pong between
+    rank 0 and rank 1 over NVLink (N >= 2; symmetric-memory flags), or between two concurrent
+    kernels on this GPU through L2 (N = 1: no NVLink on the path, the on-chip lower bound)."""
+    import torch
+    from paper_2007_00433_b200 import sesgd as C
+    iters = 5000
+    out_ns = torch.zeros(1, dtype=torch.int64, device=D.dev)
+    if D.world == 1:
+        flags = torch.zeros(64, dtype=torch.int64, device=D.dev)
+        s1, s2 = torch.cuda.Stream(D.dev), torch.cuda.Stream(D.dev)
+        dummy = torch.zeros(1, dtype=torch.int64, device=D.dev)
+        base = 1
+        for _ in range(2):
+            C.sesgd_probe_pingpong(flags.data_ptr(), flags.data_ptr() + 256, iters, True, base,
+                                   out_ns.data_ptr(), s1.cuda_stream)
+            C.sesgd_probe_pingpong(flags.data_ptr() + 256, flags.data_ptr(), iters, False, base,
+                                   dummy.data_ptr(), s2.cuda_stream)
+            base += 2 * iters + 2
+            torch.cuda.synchronize()
+        ns = int(out_ns.item())
+        return {"tau_us": ns / iters / 2 / 1e3, "scope": "intra-GPU (two concurrent kernels, flags in L2; "
+                "N = 1 has no NVLink hop)", "iters": iters}
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    buf = symm_mem.empty(64, dtype=torch.int64, device=D.dev)
+    buf.zero_()
+    hdl = symm_mem.rendezvous(buf, dist.group.WORLD)
+    D.barrier()
+    if rank < 2:
+        other = 1 - rank
+        base = 1
+        for _ in range(2):
+            C.sesgd_probe_pingpong(hdl.buffer_ptrs[rank], hdl.buffer_ptrs[other], iters, rank == 0, base,
+                                   out_ns.data_ptr(), torch.cuda.current_stream(D.dev).cuda_stream)
+            base += 2 * iters + 2
+            torch.cuda.synchronize()
+    D.barrier()
+    ns = D.max(float(out_ns.item()) if rank == 0 else 0.0)
+    return {"tau_us": ns / iters / 2 / 1e3, "scope": "NVLink (rank 0 <-> rank 1 through NVSwitch)",
+            "iters": iters}
+
+
+def cpu_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"nproc": usable, "cpu_count": os.cpu_count(), "cpu_model": model}
+
+
+def _oracle_slice(args):
+    """one process of the all-core oracle leg: the unchanged single-threaded oracle on its own
+    disjoint coordinate subset (coordinates are independent); returns its compute seconds"""
+    n, m, mode, S, T, part, parts, L_total, q, bar = args
+    import numpy as np
+
+    import oracle
+    import synth
+    omode = oracle.MODE_PARAM if mode == "param" else oracle.MODE_GRAD
+    coords = (np.arange(part, S * parts, parts, dtype=np.int64) * 7) % L_total
+    x = np.tile(synth.x0_host(len(coords), coords=coords), (n, 1))
+    v = np.zeros_like(x)
+    bar.wait()
+    t = time.perf_counter()
+    oracle.run(n, m, SEED, T, x, v, s_g=synth.SEED_G, lr=LR, mu=MU, mode=omode, coords=coords)
+    q.put(time.perf_counter() - t)
+
+
+def cpu_oracle_all_cores(n, m, mode, L_total, workload, rate_1core, budget_s):
+    """P = usable cores processes, each the plain oracle on 1/P of a coordinate sample; the
+    aggregate is total worker-elements / the slowest process's compute time"""
+    import multiprocessing as mp
+    P = cpu_info()["nproc"] or 1
+    S = int(max(1000, min(L_total, rate_1core * P * budget_s / (n * 4))))
+    T = 4
+    ctx = mp.get_context("spawn")
+    q, bar = ctx.Queue(), ctx.Barrier(P)
+    procs = [ctx.Process(target=_oracle_slice, args=((n, m, mode, S // P, T, i, P, L_total, q, bar),))
+             for i in range(P)]
+    for pr in procs:
+        pr.start()
+    secs = [q.get() for _ in procs]
+    for pr in procs:
+        pr.join()
+    dt = max(secs)
+    gbs = BYTES_PER_WORKER_ELEM * n * (S // P) * P * T / dt / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": P, "kind": "oracle",
+            "sample": (f"{workload}, n={n}, m={m}: {P} processes x {S // P} coordinates x {T} iterations, "
+                       f"each the unchanged single-threaded oracle on a disjoint coordinate subset; "
+                       f"slowest process {dt:.1f} s")}
+
+
+def run_sesgd(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_00433_b200 import sesgd as C
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    n, m = args.n, args.group_size
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    D = Dist(world, local)
+    K, W = args.steps, args.warmup
+    main = measure(args, D, rank, args.workload, n, m, K, W, e2e_steps=args.e2e_steps)
+    L, nb = main.pop("L"), main.pop("nb")
+    # BASELINE configs[2] (VGG-16, n = 16, group_size 4) in the same run, as the north star asks
+    second = None
+    if args.second_workload and args.workload == "resnet50" and (n, m) == (8, 2):
+        second = measure(args, D, rank, "vgg16", 16, 4, max(3, min(K, 20)), max(3, min(W, 5)))
+        for k in ("L", "nb", "e2e"):
+            second.pop(k, None)
+    tau = measure_tau(D, rank)
+    lat = C.sesgd_latency_model(n, m, 4.0 * L / nb, NVLINK_PEER_GBS * 1e9, tau["tau_us"] * 1e-6)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        gbs, sample, _ = cpu_oracle_rate(n, m, args.cpu_seconds, args.mode, L, args.workload)
-        cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample}
-    clocks = clk.summary()
+        gbs, sample, dt = cpu_oracle_rate(n, m, args.cpu_seconds, args.mode, L, args.workload)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample, **cpu_info()}
+        rate_1core = gbs * 1e9 / BYTES_PER_WORKER_ELEM  # worker-elements / s
+        try:
+            cpu["all_cores"] = cpu_oracle_all_cores(n, m, args.mode, L, args.workload, rate_1core,
+                                                    args.cpu_seconds)
+        except Exception as e:  # reported, never fatal: the GPU line stands on its own
+            cpu["all_cores"] = {"error": repr(e)}
     if world > 1:
         dist.barrier()
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "metric": METRIC, "value": main["value"], "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {
-                **common_config(args.workload, n, m, args.mode),
-                "workers_per_gpu": r,
-                "path": "resident (K6)" if resident else {
-                    "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P (K4)",
-                    "ring": "ring inside each group over NVLink P2P (K5)"}.get(
-                        eff_path, "one-shot push over NVLink P2P (K3)"),
-                "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush",
-                "parallelism": f"sesgd groups over {world} GPU(s)",
-            },
-            "iters_per_s": 1e3 / ms_step,
-            "gbs_per_gpu": per_gpu,
-            "kernel_ms_per_step": {"p50": kern_p50, "p90": kern_p90},
-            "roofline": roof,
+            "config": {**main["config"], "parallelism": f"sesgd groups over {world} GPU(s)"},
+            "iters_per_s": main["iters_per_s"],
+            "gbs_per_gpu": main["gbs_per_gpu"],
+            "kernel_ms_per_step": main["kernel_ms_per_step"],
+            "roofline": main["roofline"],
             "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": K * kernels_per_step,
-            "clocks": clocks,
+            "e2e": main["e2e"],
+            "gpu_launches": main["gpu_launches"],
+            "clocks": main["clocks"],
             "handshakes": {
                 "sesgd_per_tensor": lat["sesgd_handshakes"], "ring_per_tensor": lat["ring_handshakes"],
-                "kernel_rounds_per_bucket": stats[0]["handshake_rounds"],
-                "model": "Eq.2/Eq.3 exact (sesgd_latency_model), nu=770 GB/s, tau=2.6 us (K7 flag ping-pong, profiles/r01_latency_sweep_4gpu_v2.json)",
+                "kernel_rounds_per_bucket": main["kernel_rounds_per_bucket"],
+                "tau_measured": tau,
+                "model": (f"Eq.2/Eq.3 exact (sesgd_latency_model), nu={NVLINK_PEER_GBS:.0f} GB/s, "
+                          f"tau={tau['tau_us']:.2f} us measured in this run (K7 flag ping-pong)"),
                 "model_ratio": lat["ratio"],
             },
             "paper_context": PAPER_CONTEXT,
-            "consistency": {"after_iterations": t_next, "sum_sq_dev_from_mean": css,
-                            "rms_dev": (css / (n * L)) ** 0.5, "max_abs_dev": cmx,
-                            "note": "SESGD keeps the workers consistent (P:430-433); x0 ~ U[-1/8, 1/8)"},
+            "consistency": main["consistency"],
+            "workloads": {"cfg3_vgg16": second} if second is not None else None,
         }
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

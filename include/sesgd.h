@@ -138,22 +138,36 @@ extern "C" {
                                     (K3, K4, K5) run against each other through local memory.  Set
                                     before sesgd_workspace_bytes (the grid fixes the layout) */
 #define SESGD_OPT_PROTOCOL 21      /* two-shot handshake (set before sesgd_workspace_bytes, identical
-                                    on every rank): 0 (default) = epoch flags released with a
-                                    system-scope fence per batch; 1 = value-carried validity: every
-                                    receive-slot float holds a sentinel NaN (0xFFFFFFFF) until the
-                                    peer's value lands, the receiver polls the values themselves
-                                    and re-arms them (no sender fence, no flag).  A payload equal
-                                    to the sentinel travels as the canonical NaN 0x7FFFFFFF.  fp32
-                                    LSU pushes only (else SESGD_ENOTSUP) */
-#define SESGD_OPT_COOPERATIVE 22   /* 1 (default): the persistent multi-GPU grids (K3, K4, K5) are
-                                    launched cooperatively -- the runtime rejects a grid that cannot
-                                    be co-resident (SESGD_ECUDA) and starts it only when all its CTAs
-                                    fit at once (e.g. beside backward kernels); 0: plain launch */
+                                    on every rank): -1 (default, auto) = 1 where supported (the
+                                    two-shot path with fp32 LSU pushes), else 0.
+                                    0 = epoch flags released with a system-scope fence per batch.
+                                    1 = value-carried validity: every receive-slot float holds a
+                                    sentinel NaN (0xFFFFFFFF) until the peer's value lands; the
+                                    receiver polls the values themselves and re-arms them (no
+                                    sender fence, no flag).  A payload equal to the sentinel
+                                    travels as the canonical NaN 0x7FFFFFFF.
+                                    2 = 1 in K4W, the warp-specialised kernel (one worker per GPU,
+                                    one CTA per SM).  1 and 2: fp32 LSU pushes only (else
+                                    SESGD_ENOTSUP) */
+#define SESGD_OPT_COOPERATIVE 22   /* 1: the persistent multi-GPU grids (K4, K4W, K3, K5) are launched
+                                    cooperatively -- the runtime rejects a grid that cannot be
+                                    co-resident (SESGD_ECUDA) and starts it only when all its CTAs
+                                    fit at once.  0 (default): plain launch; safe because a K4 /
+                                    K4W / K3-direct / K5 CTA waits only on data or flags of the
+                                    SAME CTA index on peer GPUs (never on another CTA of its own
+                                    grid), so a CTA that is not yet resident delays, never
+                                    deadlocks, its peers.  The SM-specialised K3 (P2P variant
+                                    >= 1, COMM and COMPUTE CTAs wait on each other) is always
+                                    launched cooperatively.  (A cooperative launch cannot start
+                                    while the previous kernel drains: measured +10..30 us per
+                                    step, profiles/r02_proto_*.json) */
 #define SESGD_OPT_EXPERIMENT 20    /* MEASUREMENT ONLY -- results are wrong when set: bit 0 drops
                                     the system-scope fence before the two-shot flag releases,
                                     bit 1 sends the two-shot pushes to this rank's own receive
                                     slots instead of the peers' (no NVLink payload).  Bounds what
-                                    the flag protocol and the NVLink traffic cost */
+                                    the flag protocol and the NVLink traffic cost;
+                                    bits 2 / 3: value-carried pushes / polls as weak st / ld.cg
+                                    instead of relaxed.sys; bit 4: K4W warp layout 1 */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {
@@ -164,7 +178,12 @@ typedef struct sesgd_cost {
   double ratio;            /* ring_s / sesgd_s (1 if both 0, +inf if only sesgd_s is 0)      */
 } sesgd_cost;
 
-/* Per-bucket counters (host-side, exact: the schedule is deterministic). */
+/* Counters.  The first six are per bucket and host-side (exact: the schedule is deterministic);
+ * the dev_* ones are counted ON THE DEVICE by the multi-GPU kernels of this context (all buckets,
+ * cumulative since sesgd_attach; a snapshot -- synchronise the stream first for exact totals);
+ * last_launch_us is the device time (CUDA events recorded by the library) of the context's most
+ * recent completed sync launch, hop_ns the one-way handshake latency last measured by
+ * sesgd_measure_hop (0 if never). */
 typedef struct sesgd_stats {
   int64_t sync_calls;        /* sesgd_sync_step calls on this bucket                        */
   int64_t kernel_launches;   /* kernels this library launched for the bucket                */
@@ -172,6 +191,12 @@ typedef struct sesgd_stats {
   int64_t flag_messages;     /* cross-GPU flag stores issued by this process, cumulative    */
   int64_t payload_bytes_in;  /* bytes this process pulled from other GPUs, cumulative       */
   int64_t hbm_algo_bytes;    /* algorithmic HBM bytes (20 B per worker-element), cumulative */
+  int64_t dev_flag_stores;   /* device: cross-GPU handshake flag stores (K3, K4 protocol 0, K5) */
+  int64_t dev_flag_spins;    /* device: flag waits that had to spin (peer not ready yet)    */
+  int64_t dev_value_spins;   /* device: value-carried polls that found a sentinel (protocols 1, 2) */
+  int64_t dev_launches;      /* device: multi-GPU kernel launches that started               */
+  double last_launch_us;     /* device time of the most recent completed sync launch (events) */
+  double hop_ns;             /* one-way flag hop, sesgd_measure_hop (K7 ping-pong)           */
 } sesgd_stats;
 
 typedef struct sesgd_ctx sesgd_ctx;
@@ -322,6 +347,15 @@ SESGD_API int sesgd_poll(sesgd_ctx *ctx);
 
 /* Counters of bucket `bucket`.  Errors: SESGD_EINVAL. */
 SESGD_API int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats *out);
+
+/* Per-hop handshake latency t_tau (Eq. 2) between this rank and `peer_rank` through the
+ * two ranks' workspaces (K7 flag ping-pong, one thread, system-scope release / acquire): both ranks
+ * call it concurrently with the same `iters`, exactly one with initiator = 1.  Enqueued on
+ * `stream`; the result (round trip / 2) appears in sesgd_stats.hop_ns once the stream completes.
+ * Errors: SESGD_EINVAL (peer_rank out of range or == rank, iters < 1), SESGD_ESTATE (peers not
+ * attached), SESGD_ECUDA. */
+SESGD_API int sesgd_measure_hop(sesgd_ctx *ctx, int32_t peer_rank, int32_t iters, int32_t initiator,
+                                void *stream);
 
 /* Number of SMs and CTAs per launch the library uses on the attached device (0 before attach). */
 SESGD_API int sesgd_launch_grid(const sesgd_ctx *ctx, int32_t *ctas_out);

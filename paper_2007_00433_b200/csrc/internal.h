@@ -105,6 +105,7 @@ struct P2PArgs {
   int experiment;                   // SESGD_OPT_EXPERIMENT (measurement only)
   int protocol;                     // SESGD_OPT_PROTOCOL: 0 epoch flags, 1 value-carried (sentinel)
   int cooperative;                  // SESGD_OPT_COOPERATIVE: cooperative launch (co-residency)
+  unsigned long long *counters;     // device handshake counters [kCnt*] (sesgd_get_stats), or null
   int8_t my_workers[SESGD_MAX_WORKERS];      // global ids of local slots
   int8_t my_pos[SESGD_MAX_WORKERS];          // position of each local slot in its group
   int8_t slot_kind[SESGD_MAX_WORKERS];       // 0: group has remote members; 1: all-local group,
@@ -114,6 +115,21 @@ struct P2PArgs {
   int8_t canon[SESGD_MAX_WORKERS];           // canonical groups of the iteration
   int8_t group_of[SESGD_MAX_WORKERS];
 };
+// device-side handshake counters (one block per context, cumulative; fire-and-forget atomics)
+enum DevCounter : int {
+  kCntFlagStores = 0,  // cross-GPU handshake stores: ready flags (K3, K4 protocol 0), ring step flags (K5)
+  kCntFlagSpins = 1,   // flag waits that found the peer's flag not yet there
+  kCntValueSpins = 2,  // value-carried polls that found a sentinel (protocols 1, 2)
+  kCntLaunches = 3,    // multi-GPU kernel launches (CTA 0 of every grid)
+  kCntHopNs = 4,       // elapsed ns of the last sesgd_measure_hop ping-pong (written, not added)
+  kNumCounters = 8
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void count(unsigned long long *c, int which, unsigned long long v = 1) {
+  if (c && v) atomicAdd(c + which, v);
+}
+#endif
+
 // K5: paper-faithful Ring-AllReduce inside each group (one worker per GPU), see ring.cu.
 struct RingArgs {
   float *x, *v;                     // this bucket's buffers of the (single) local worker
@@ -130,9 +146,12 @@ struct RingArgs {
   float lr, mu, wd;
   int parity, steps, m, pos, grid, my_rank, bucket, nbuckets;
   int cooperative;
+  unsigned long long *counters;
   int8_t ring_rank[SESGD_MAX_WORKERS];  // rank of ring position 0..m-1 (ascending worker id)
 };
 cudaError_t launch_ring(const RingArgs &a, int mode, cudaStream_t stream);
+cudaError_t launch_pingpong(uint64_t *mine, uint64_t *peer, int iters, int initiator, uint64_t base,
+                            uint64_t *out_ns, cudaStream_t stream);
 int ring_block_threads();
 int ring_occupancy(int mode);
 
@@ -194,8 +213,8 @@ struct sesgd_ctx {
   char *mc_ws = nullptr;    // sesgd_attach_multicast (SESGD_PATH_NVLS)
   int payload_bf16 = 0;     // SESGD_OPT_PAYLOAD_BF16
   int experiment = 0;       // SESGD_OPT_EXPERIMENT
-  int protocol = 0;         // SESGD_OPT_PROTOCOL (two-shot kernel)
-  int cooperative = 1;      // SESGD_OPT_COOPERATIVE
+  int protocol = -1;        // SESGD_OPT_PROTOCOL (two-shot kernel; -1 auto, resolved at layout freeze)
+  int cooperative = 0;      // SESGD_OPT_COOPERATIVE
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)
@@ -242,6 +261,11 @@ struct sesgd_ctx {
   unsigned long long *d_err = nullptr;  // device alias of h_err
   unsigned int *d_abort = nullptr;
   uint64_t *d_prof = nullptr;     // SESGD_OPT_PROFILE timers
+  unsigned long long *d_counters = nullptr;  // device handshake counters [kNumCounters] (+ hop ns)
+  cudaEvent_t ev_l0 = nullptr, ev_l1 = nullptr;  // around the most recent sync launch
+  bool ev_l_valid = false;
+  uint64_t hop_base[SESGD_MAX_RANKS] = {};
+  int hop_iters = 0;
   int profile = 0;
   std::string last_error;
 };

@@ -204,8 +204,13 @@ __device__ __forceinline__ float unsentinel(float v) {
   return __float_as_uint(v) == kSentinel ? __uint_as_float(0x7FFFFFFFu) : v;
 }
 template <int W>
-__device__ __forceinline__ void st_sent(float *p, const float (&r)[W], int nvalid) {
+__device__ __forceinline__ void st_sent(float *p, const float (&r)[W], int nvalid, bool weak = false) {
   if constexpr (W == 4) {
+    if (nvalid >= 4 && weak) {  // (SESGD_OPT_EXPERIMENT bit 2: measurement only)
+      *reinterpret_cast<float4 *>(p) = make_float4(unsentinel(r[0]), unsentinel(r[1]), unsentinel(r[2]),
+                                                   unsentinel(r[3]));
+      return;
+    }
     if (nvalid >= 4) {
       asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(unsentinel(r[0])),
                    "f"(unsentinel(r[1])), "f"(unsentinel(r[2])), "f"(unsentinel(r[3]))
@@ -246,6 +251,7 @@ __device__ uint64_t wait_geq(const P2PArgs &a, const uint64_t *p, uint64_t targe
                              int worker, int pos) {
   uint64_t v = dev::ld_acquire_sys(p);
   if (v >= target) return v;
+  count(a.counters, kCntFlagSpins);
   const uint64_t t0 = dev::globaltimer();
   for (;;) {
     v = dev::ld_acquire_sys(p);
@@ -282,6 +288,11 @@ __device__ __forceinline__ void ld_poll(const P2PArgs &a, float *p, float (&r)[W
   };
   auto load = [&]() {
     if constexpr (W == 4) {
+      if (nvalid >= 4 && (a.experiment & 8)) {  // (measurement only: weak L2 load)
+        const float4 t = __ldcg(reinterpret_cast<const float4 *>(p));
+        r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
+        return;
+      }
       if (nvalid >= 4) {
         ld_relaxed4(p, r);
         return;
@@ -292,6 +303,7 @@ __device__ __forceinline__ void ld_poll(const P2PArgs &a, float *p, float (&r)[W
   };
   load();
   if (pending()) {
+    count(a.counters, kCntValueSpins);
     const uint64_t t0 = dev::globaltimer();
     do {
       if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;
@@ -699,10 +711,12 @@ struct Split {
           const int64_t g = c0 + p / (a.m * ns);
           const int me = a.my_workers[s];
           const int w = group(me)[rr];
-          if (w == me)
+          if (w == me) {
             st_release_gpu(sent(s, g), call1);
-          else if (remote(w))
+          } else if (remote(w)) {
             dev::st_release_sys(ready(w, g, a.my_pos[s]), call1);
+            count(a.counters, kCntFlagStores);
+          }
         }
       }
       if (a.prof) {
@@ -739,13 +753,18 @@ struct Split {
     const uint64_t call1 = uint64_t(a.call) + 1;
     const int pairs = a.r * a.m;
     dev::fence_acq_rel_sys();
+    unsigned long long nst = 0;
     for (int64_t q = threadIdx.x; q < (c1 - c0) * pairs; q += 32) {
       const int64_t c = c0 + q / pairs;
       const int p = int(q % pairs), s = p / a.m, rr = p % a.m;
       const int me = a.my_workers[s];
       const int w = group(me)[rr];
-      if (w != me && remote(w)) st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), call1);
+      if (w != me && remote(w)) {
+        st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), call1);
+        ++nst;
+      }
     }
+    count(a.counters, kCntFlagStores, nst);
   }
 
   // A group whose members all live on this GPU: the whole update in registers, like the
@@ -1162,27 +1181,45 @@ struct Split {
       const int p = a.my_pos[s];
       float *xs = a.bx[c.b * a.r + s], *vs = a.bv[c.b * a.r + s];
       const float *gs = a.bg[c.b * a.r + s];
+      // items in batches of kB: every load of a batch is in flight before its first store (the
+      // compiler cannot hoist loads above stores it cannot prove disjoint, so an unbatched loop
+      // pays one HBM latency per item)
+      // (several workers per GPU: 4 CTAs per SM without batching measured faster than 3 with it,
+      // profiles/r02_k4_experiments.json)
+      constexpr int kB = MULTI ? 1 : (W == 4) ? 2 : 8;
 #pragma unroll
-      for (int it = 0; it < kItems; ++it) {
+      for (int b0 = 0; b0 < kItems; b0 += kB) {
+        float gr[kB][W], v[GRAD ? 1 : kB][W], x[GRAD ? 1 : kB][W];
+#pragma unroll
+        for (int ib = 0; ib < kB; ++ib) {
+          const int64_t o = (int64_t(b0 + ib) * kThreads + threadIdx.x) * W;
+          const int64_t e = c.e0 + o;
+          const int nv = (int)min(int64_t(W), c.e1 - e);
+          if (nv <= 0) continue;
+          load_m<W>(gs + e, gr[ib], nv);
+          if constexpr (!GRAD) {
+            load_m<W>(vs + e, v[ib], nv);
+            load_m<W>(xs + e, x[ib], nv);
+          }
+        }
+#pragma unroll
+        for (int ib = 0; ib < kB; ++ib) {
+        const int it = b0 + ib;
         const int64_t o = (int64_t(it) * kThreads + threadIdx.x) * W;  // offset inside the chunk
         const int64_t e = c.e0 + o;
         const int nv = (int)min(int64_t(W), c.e1 - e);
         if (nv <= 0) continue;
-        float gr[W], val[W];
-        load_m<W>(gs + e, gr, nv);
+        float val[W];
         if constexpr (!GRAD) {
-          float v[W], x[W];
-          load_m<W>(vs + e, v, nv);
-          load_m<W>(xs + e, x, nv);
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            v[q] = dev::momentum(a.mu, v[q], dev::decay(gr[q], a.wd, x[q]));
-            val[q] = dev::sgd(x[q], a.lr, v[q]);  // x_hat
+            v[ib][q] = dev::momentum(a.mu, v[ib][q], dev::decay(gr[ib][q], a.wd, x[ib][q]));
+            val[q] = dev::sgd(x[ib][q], a.lr, v[ib][q]);  // x_hat
           }
-          store_m<W>(vs + e, v, nv);
+          store_m<W>(vs + e, v[ib], nv);
         } else {
 #pragma unroll
-          for (int q = 0; q < W; ++q) val[q] = gr[q];
+          for (int q = 0; q < W; ++q) val[q] = gr[ib][q];
         }
         const int j = min(int(o / S), a.m - 1);  // owner position (a W-vector never straddles)
         const int w = G[j];
@@ -1197,9 +1234,10 @@ struct Split {
         } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
           st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
         } else if constexpr (SENT) {
-          st_sent<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store, validity in the value
+          st_sent<W>(recv(w, p) + c.soff + e, val, nv, (a.experiment & 4) != 0);  // NVLink store, validity in the value
         } else {
           st_slot<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store
+        }
         }
       }
     }
@@ -1232,6 +1270,7 @@ struct Split {
     if (!(a.experiment & 1))    // (SESGD_OPT_EXPERIMENT bit 0: measurement only)
       dev::fence_acq_rel_sys();  // ... before the flags (release pattern: fence + relaxed stores)
     const int64_t nrs = (rs1 - rs0) * pairs, nall = nrs + (ag1 - ag0) * pairs;
+    unsigned long long nst = 0;
     for (int64_t q = threadIdx.x; q < nall; q += 32) {
       const int kind = q < nrs ? 0 : 1;
       const int64_t qq = kind == 0 ? q : q - nrs;
@@ -1243,8 +1282,12 @@ struct Split {
         if (kind == 0 ? (j != own) : (a.my_pos[s] != own)) continue;
       }
       const int w = group(a.my_workers[s])[j];
-      if (rem<MULTI>(w)) st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), e1 + kind);
+      if (rem<MULTI>(w)) {
+        st_relaxed_sys(ready(w, first + c * gc, a.my_pos[s]), e1 + kind);
+        ++nst;
+      }
     }
+    count(a.counters, kCntFlagStores, nst);
   }
 
   // every remote member's flag of chunk g (for every slot) reached `epoch`
@@ -1302,7 +1345,7 @@ struct Split {
           const int w = G[rr];
           if (rem<MULTI>(w)) {
             if constexpr (SENT)
-              st_sent<W>(recv(w, p) + c.soff + e, acc, nv);
+              st_sent<W>(recv(w, p) + c.soff + e, acc, nv, (a.experiment & 4) != 0);
             else if (!bulk)
               st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
             continue;
@@ -1538,6 +1581,7 @@ template <int W, bool GRAD>
 __global__ void __launch_bounds__(kThreads, 3) k3_split(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];
   const Split<W, GRAD> p(a);
+  if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1) {
     p.local_only();
   } else if (int(blockIdx.x) < a.comm_ctas) {
@@ -1550,6 +1594,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_split(const __grid_constant__ 
 template <int W, bool GRAD>
 __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__ P2PArgs a) {
   const Split<W, GRAD> p(a);
+  if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1)
     p.local_only();
   else
@@ -1557,9 +1602,10 @@ __global__ void __launch_bounds__(kThreads, 4) k3_direct(const __grid_constant__
 }
 
 template <int W, bool GRAD, bool TMA, bool MULTI, bool NV = false, bool BF = false, bool SENT = false>
-__global__ void __launch_bounds__(kThreads, 4) k4_twoshot(const __grid_constant__ P2PArgs a) {
+__global__ void __launch_bounds__(kThreads, MULTI ? 4 : 3) k4_twoshot(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];  // TMA: kPushRing chunk images
   const Split<W, GRAD> p(a);
+  if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1)
     p.local_only();
   else
@@ -1660,7 +1706,9 @@ cudaError_t launch_p2p_oneshot(const P2PArgs &a, int variant, int mode, bool vec
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
-  return launch_persistent(k, unsigned(a.grid), kThreads, args, smem, stream, a.cooperative != 0);
+  // the SM-specialised variant's COMM and COMPUTE CTAs wait on each other: always cooperative
+  return launch_persistent(k, unsigned(a.grid), kThreads, args, smem, stream,
+                           a.cooperative != 0 || (variant >= 1 && a.m > 1));
 }
 
 int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi) {

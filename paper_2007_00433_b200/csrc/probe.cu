@@ -49,6 +49,12 @@ __global__ void pingpong_kernel(uint64_t *mine, uint64_t *peer, int iters, int i
 }
 
 }  // namespace
+
+cudaError_t launch_pingpong(uint64_t *mine, uint64_t *peer, int iters, int initiator, uint64_t base,
+                            uint64_t *out_ns, cudaStream_t stream) {
+  pingpong_kernel<<<1, 32, 0, stream>>>(mine, peer, iters, initiator, base, out_ns, 10ull * 1000000000ull);
+  return cudaGetLastError();
+}
 }  // namespace sesgd
 
 extern "C" {

@@ -30,6 +30,7 @@ constexpr int kRingThreads = 256;
 
 __device__ bool ring_wait(const RingArgs &a, const uint64_t *p, uint64_t target, int kind) {
   if (dev::ld_acquire_sys(p) >= target) return true;
+  count(a.counters, kCntFlagSpins);
   const uint64_t t0 = dev::globaltimer();
   for (;;) {
     const uint64_t v = dev::ld_acquire_sys(p);
@@ -112,6 +113,7 @@ struct Ring {
         }
       }
       dev::st_release_sys(flag(rank_at(a.pos + 1), step), uint64_t(a.call) + 1);
+      count(a.counters, kCntFlagStores);
     }
   }
   __device__ __forceinline__ void await(int step) const {
@@ -199,6 +201,7 @@ struct Ring {
 template <bool GRAD>
 __global__ void __launch_bounds__(kRingThreads) k5_ring(const __grid_constant__ RingArgs a) {
   const Ring<GRAD> r(a);
+  if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1)
     r.local_only();
   else

@@ -60,6 +60,15 @@ int check_latched(sesgd_ctx *ctx) {
   return fail(ctx, SESGD_ETIMEOUT, buf);
 }
 
+// CUDA events around every sync launch: sesgd_stats.last_launch_us is the device time of the most
+// recent one (an event record is not a kernel and costs ~1 us of host time)
+void mark_start(sesgd_ctx *ctx, cudaStream_t st) {
+  if (ctx->ev_l0) cudaEventRecord(ctx->ev_l0, st);
+}
+void mark_end(sesgd_ctx *ctx, cudaStream_t st) {
+  if (ctx->ev_l1 && cudaEventRecord(ctx->ev_l1, st) == cudaSuccess) ctx->ev_l_valid = true;
+}
+
 void free_bucket(sesgd_bucket &b) {
   if (b.d_x) cudaFree(b.d_x);
   if (b.d_v) cudaFree(b.d_v);
@@ -77,9 +86,16 @@ void free_bucket(sesgd_bucket &b) {
 //   [stage_off, ..)     f32 stage   [r slot][region]              (own x_hat, L2-resident)
 //   [recv_off, ..)      f32 recv    [2 parity][r slot][m position][region]
 // region = stage_slot_floats = sum over buckets of round_up(numel, 64).
+int resolve_path(const sesgd_ctx *ctx);
+
 void freeze_layout(sesgd_ctx *ctx) {
   if (ctx->path == SESGD_PATH_TWOSHOT || ctx->path == SESGD_PATH_NVLS)
     ctx->p2p_variant = 0;  // K4 runs on the DIRECT grid
+  // SESGD_OPT_PROTOCOL auto (-1): value-carried validity wherever the two-shot kernel supports it
+  // (fp32 LSU pushes; measured faster at every shape, profiles/r02_k4_experiments.json), else flags
+  if (ctx->protocol < 0)
+    ctx->protocol = (resolve_path(ctx) == SESGD_PATH_TWOSHOT && ctx->m >= 2 && !ctx->push_tma &&
+                     !ctx->payload_bf16) ? 1 : 0;
   const int var = ctx->p2p_variant;
   const int chunk = sesgd::p2p_chunk_elems(var);
   const int r = ctx->n_local;
@@ -226,8 +242,10 @@ int local_step(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_
   int gx = (target + a.k - 1) / a.k;
   const int64_t need = ((vec ? biggest / 4 : biggest) + threads - 1) / threads;
   if (need < gx) gx = int(need > 0 ? need : 1);
+  mark_start(ctx, st);
   cudaError_t e = sesgd::launch_resident(a, ctx->mode, vec, gx, 0, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "launch local step");
+  mark_end(ctx, st);
   for (size_t b = 0; b < ctx->buckets.size(); ++b) {
     if (bucket >= 0 && int(b) != bucket) continue;
     ctx->buckets[b].stats.hbm_algo_bytes += 20 * ctx->buckets[b].numel * ctx->n_local;
@@ -395,6 +413,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.experiment = ctx->experiment;
   a.protocol = ctx->protocol;
   a.cooperative = ctx->cooperative;
+  a.counters = ctx->d_counters;
   for (int s = 0; s < ctx->n_local; ++s) {
     const int me = ctx->local_workers[s];
     a.my_workers[s] = int8_t(me);
@@ -417,12 +436,14 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   bool vec = true;
   for (size_t b = 0; b < ctx->buckets.size(); ++b)
     if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
+  mark_start(ctx, st);
   cudaError_t e = (twoshot && ctx->protocol == 2 && !nvls)
                       ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
                   : twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
                             : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
                                                         ctx->guard_smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
+  mark_end(ctx, st);
   // bookkeeping
   int remote_peers = 0;
   for (int s = 0; s < ctx->n_local; ++s) {
@@ -500,6 +521,9 @@ void sesgd_destroy(sesgd_ctx *ctx) {
   if (ctx->d_bv) cudaFree(ctx->d_bv);
   if (ctx->d_bg) cudaFree(const_cast<float **>(ctx->d_bg));
   if (ctx->d_numels) cudaFree(ctx->d_numels);
+  if (ctx->d_counters) cudaFree(ctx->d_counters);
+  if (ctx->ev_l0) cudaEventDestroy(ctx->ev_l0);
+  if (ctx->ev_l1) cudaEventDestroy(ctx->ev_l1);
   for (auto *v : {&ctx->ev_in, &ctx->ev_k, &ctx->ev_out})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
@@ -616,7 +640,7 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->discard = int(value);
       return SESGD_OK;
     case SESGD_OPT_PROTOCOL:
-      if (value < 0 || value > 2) return fail(ctx, SESGD_EINVAL, "protocol must be 0, 1 or 2");
+      if (value < -1 || value > 2) return fail(ctx, SESGD_EINVAL, "protocol must be -1 (auto), 0, 1 or 2");
       if (ctx->layout_frozen) return fail(ctx, SESGD_ESTATE, "the protocol is fixed once the layout freezes");
       ctx->protocol = int(value);
       return SESGD_OK;
@@ -625,7 +649,7 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->cooperative = int(value);
       return SESGD_OK;
     case SESGD_OPT_EXPERIMENT:
-      if (value < 0 || value > 3) return fail(ctx, SESGD_EINVAL, "experiment bits must be in [0, 3]");
+      if (value < 0 || value > 63) return fail(ctx, SESGD_EINVAL, "experiment bits must be in [0, 63]");
       ctx->experiment = int(value);
       return SESGD_OK;
     case SESGD_OPT_HOP_DELAY_NS:
@@ -680,6 +704,18 @@ int sesgd_attach(sesgd_ctx *ctx, int32_t device, int32_t n_local, const int32_t 
     cudaFreeHost(h);
     return cuda_fail(ctx, e, "cudaMalloc(abort word)");
   }
+  unsigned long long *cnt = nullptr;
+  e = cudaMalloc(reinterpret_cast<void **>(&cnt), sesgd::kNumCounters * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(cnt, 0, sesgd::kNumCounters * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev_l0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev_l1);
+  if (e != cudaSuccess) {
+    cudaFreeHost(h);
+    cudaFree(ab);
+    if (cnt) cudaFree(cnt);
+    return cuda_fail(ctx, e, "device counters");
+  }
+  ctx->d_counters = cnt;
   ctx->h_err = h;
   ctx->d_err = d;
   ctx->d_abort = ab;
@@ -801,6 +837,20 @@ int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, void *cons
       return fail(ctx, SESGD_ESTATE, buf);
     }
     ctx->ws[r] = static_cast<char *>(rank_ws[r]);
+    // a peer workspace on another device of this process (e.g. mapped through CUDA IPC) needs
+    // peer access from this device; symmetric-memory mappings already have it
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, rank_ws[r]) == cudaSuccess && pa.type == cudaMemoryTypeDevice &&
+        pa.device != ctx->device) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(ctx->device);
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(pa.device, 0);
+      cudaSetDevice(cur);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+        return cuda_fail(ctx, pe, "enabling peer access to a peer workspace");
+      cudaGetLastError();  // clear a sticky "already enabled"
+    }
   }
   ctx->n_ranks = n_ranks;
   ctx->rank = rank;
@@ -871,8 +921,10 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     a.k = ctx->n / ctx->m;
     for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
     const int gx = resident_grid_x(ctx, b.vec, b.numel);
+    mark_start(ctx, st);
     cudaError_t e = sesgd::launch_resident(a, ctx->mode, b.vec, gx, ctx->resident_unroll, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel");
+    mark_end(ctx, st);
     b.stats.kernel_launches++;
     b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n;
     return SESGD_OK;
@@ -908,14 +960,17 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     ra.bucket = bucket;
     ra.nbuckets = int(ctx->buckets.size());
     ra.cooperative = ctx->cooperative;
+    ra.counters = ctx->d_counters;
     const int me = ctx->local_workers[0];
     const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
     for (int q = 0; q < ctx->m; ++q) {
       ra.ring_rank[q] = ctx->worker_rank[G[q]];
       if (G[q] == me) ra.pos = q;
     }
+    mark_start(ctx, st);
     cudaError_t e = sesgd::launch_ring(ra, ctx->mode, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch ring kernel");
+    mark_end(ctx, st);
     b.seq_hist[b.calls & 1] = ctx->seq;  // keep the one-shot guard history consistent
     b.calls++;
     ctx->seq++;
@@ -988,9 +1043,11 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     a.bg = ctx->d_bg;
     a.numels = ctx->d_numels;
     for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
+    mark_start(ctx, static_cast<cudaStream_t>(stream));
     cudaError_t e = sesgd::launch_resident(a, ctx->mode, vec, resident_grid_x(ctx, vec, biggest),
                                            ctx->resident_unroll, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel (all buckets)");
+    mark_end(ctx, static_cast<cudaStream_t>(stream));
     for (auto &b : ctx->buckets) {
       b.stats.sync_calls++;
       b.stats.hbm_algo_bytes += 20 * b.numel * ctx->n;
@@ -1173,6 +1230,41 @@ int sesgd_poll(sesgd_ctx *ctx) {
 int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats *out) {
   if (!ctx || !out || bucket < 0 || size_t(bucket) >= ctx->buckets.size()) return SESGD_EINVAL;
   *out = ctx->buckets[bucket].stats;
+  if (ctx->d_counters) {
+    unsigned long long c[sesgd::kNumCounters] = {};
+    if (cudaMemcpy(c, ctx->d_counters, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(const_cast<sesgd_ctx *>(ctx), SESGD_ECUDA, "reading the device counters");
+    out->dev_flag_stores = int64_t(c[sesgd::kCntFlagStores]);
+    out->dev_flag_spins = int64_t(c[sesgd::kCntFlagSpins]);
+    out->dev_value_spins = int64_t(c[sesgd::kCntValueSpins]);
+    out->dev_launches = int64_t(c[sesgd::kCntLaunches]);
+    out->hop_ns = ctx->hop_iters > 0 ? double(c[sesgd::kCntHopNs]) / ctx->hop_iters / 2.0 : 0.0;
+  }
+  out->last_launch_us = 0.0;
+  if (ctx->ev_l_valid && cudaEventQuery(ctx->ev_l1) == cudaSuccess) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev_l0, ctx->ev_l1) == cudaSuccess) out->last_launch_us = 1e3 * ms;
+  }
+  cudaGetLastError();  // a not-ready query is not an error of this call
+  return SESGD_OK;
+}
+
+int sesgd_measure_hop(sesgd_ctx *ctx, int32_t peer_rank, int32_t iters, int32_t initiator, void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  if (!ctx->peers) return fail(ctx, SESGD_ESTATE, "sesgd_attach_peers first");
+  if (peer_rank < 0 || peer_rank >= ctx->n_ranks || peer_rank == ctx->rank || iters < 1)
+    return fail(ctx, SESGD_EINVAL, "peer_rank must be another attached rank, iters >= 1");
+  // flag words in the workspace header, [128 + 8 * rank], one per peer rank, monotonic epochs
+  auto flag = [&](int owner, int other) {
+    return reinterpret_cast<uint64_t *>(ctx->ws[owner] + 128) + other;
+  };
+  const cudaError_t e = sesgd::launch_pingpong(
+      flag(ctx->rank, peer_rank), flag(peer_rank, ctx->rank), iters, initiator ? 1 : 0,
+      ctx->hop_base[peer_rank], reinterpret_cast<uint64_t *>(ctx->d_counters + sesgd::kCntHopNs),
+      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch ping-pong");
+  ctx->hop_base[peer_rank] += 2 * uint64_t(iters) + 2;
+  ctx->hop_iters = iters;
   return SESGD_OK;
 }
 

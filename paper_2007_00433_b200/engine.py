@@ -235,6 +235,14 @@ class SESGDEngine:
     def poll(self) -> None:
         C.sesgd_poll(self.ctx)
 
+    def measure_hop(self, peer_rank: int, iters: int = 5000, initiator: Optional[bool] = None,
+                    stream: Optional[torch.cuda.Stream] = None) -> None:
+        """K7 ping-pong with `peer_rank` through the workspaces (both ranks call it concurrently);
+        the one-way hop appears in stats()["hop_ns"] once the stream completes"""
+        s = stream if stream is not None else self.default_stream()
+        init = self.rank < peer_rank if initiator is None else initiator
+        C.sesgd_measure_hop(self.ctx, peer_rank, iters, init, s.cuda_stream)
+
     def close(self) -> None:
         if self.ctx is not None:
             C.sesgd_destroy(self.ctx)

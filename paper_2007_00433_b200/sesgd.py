@@ -34,7 +34,7 @@ EXPORTED = (
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
     "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus", "sesgd_set_weight_decay",
-    "sesgd_attach_multicast", "sesgd_pair_counts",
+    "sesgd_attach_multicast", "sesgd_pair_counts", "sesgd_measure_hop",
 )
 
 
@@ -46,7 +46,10 @@ class sesgd_cost(ctypes.Structure):
 class sesgd_stats(ctypes.Structure):
     _fields_ = [("sync_calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("handshake_rounds", ctypes.c_int64), ("flag_messages", ctypes.c_int64),
-                ("payload_bytes_in", ctypes.c_int64), ("hbm_algo_bytes", ctypes.c_int64)]
+                ("payload_bytes_in", ctypes.c_int64), ("hbm_algo_bytes", ctypes.c_int64),
+                ("dev_flag_stores", ctypes.c_int64), ("dev_flag_spins", ctypes.c_int64),
+                ("dev_value_spins", ctypes.c_int64), ("dev_launches", ctypes.c_int64),
+                ("last_launch_us", ctypes.c_double), ("hop_ns", ctypes.c_double)]
 
 
 class SesgdError(RuntimeError):
@@ -89,6 +92,7 @@ def lib():
             "sesgd_pair_counts": ([P, i64, i64, P, P], ctypes.c_int),
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
+            "sesgd_measure_hop": ([P, i32, i32, i32, P], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
             "sesgd_strerror": ([ctypes.c_int], ctypes.c_char_p),
             "sesgd_last_error": ([P], ctypes.c_char_p),
@@ -231,6 +235,10 @@ def sesgd_get_stats(ctx, bucket: int) -> dict:
     out = sesgd_stats()
     _check(lib().sesgd_get_stats(ctx, bucket, ctypes.byref(out)), ctx)
     return {f: getattr(out, f) for f, _ in sesgd_stats._fields_}
+
+
+def sesgd_measure_hop(ctx, peer_rank: int, iters: int, initiator: bool, stream: int = 0) -> None:
+    _check(lib().sesgd_measure_hop(ctx, peer_rank, iters, int(bool(initiator)), ctypes.c_void_p(int(stream))), ctx)
 
 
 def sesgd_probe_copy(dst: int, src: int, nbytes: int, ctas: int, stream: int = 0) -> None:

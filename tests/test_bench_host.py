@@ -95,6 +95,15 @@ def test_reference_arm_json_workload_equals_gpu_arm_config():
     d = json.loads(res.stdout.strip().splitlines()[-1])
     want = bench.common_config("resnet50", 8, 2, "param")
     assert {k: d["config"][k] for k in want} == want
-    src = inspect.getsource(bench.run_sesgd)
-    assert "**common_config(args.workload, n, m, args.mode)" in src
+    src = inspect.getsource(bench.measure) + inspect.getsource(bench.run_sesgd)
+    assert "**common_config(workload, n, m, args.mode)" in src
     assert "workload_desc(" not in src  # nothing appended to the shared string
+
+
+def test_all_core_oracle_leg_runs_the_plain_oracle_on_every_core():
+    """cpu_baseline.all_cores: one unchanged single-threaded oracle per usable core on disjoint
+    coordinate subsets; reports the core count and the CPU model beside the number"""
+    info = bench.cpu_info()
+    assert info["nproc"] >= 1 and info["cpu_count"] >= info["nproc"]
+    r = bench.cpu_oracle_all_cores(4, 2, "param", 1 << 20, "config1", rate_1core=2e6, budget_s=0.2)
+    assert r["cores"] == info["nproc"] and r["value"] > 0 and r["kind"] == "oracle"

@@ -43,7 +43,7 @@ def _free_port():
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
             lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
-            bf16=0, coords=None, protocol=0):
+            bf16=0, coords=None, protocol=0, release_every=0):
     """`gpus` ranks: processes on as many GPUs (nvlink) or virtual ranks on cuda:0 (loopback)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -66,7 +66,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
-               "--bf16", str(bf16), "--protocol", str(protocol), "--loopback", str(gpus if loop else 0), *extra,
+               "--bf16", str(bf16), "--protocol", str(protocol), "--release-every", str(release_every), "--loopback", str(gpus if loop else 0), *extra,
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -557,5 +557,36 @@ def test_two_gpus_value_protocols_weight_decay(tmp_path, protocol, mode):
     v = np.zeros_like(x)
     oracle.run_local(2, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=mode,
                      weight_decay=wd)
+    _compare(X, x)
+    _compare(V, v)
+
+
+# ---------------------------------------------------------------- stress: 1000 iterations, random shapes
+def _stress_cases(k=6, seed=2024):
+    """random (ranks, n, m, protocol, grid, lag, release_every, mode): every flag / slot / ring
+    reuse path over 1000 iterations (both call parities ~500 times)"""
+    rng = np.random.default_rng(seed)
+    cases = []
+    while len(cases) < k:
+        gpus = int(rng.choice([2, 4]))
+        n = gpus * int(rng.choice([1, 2]))
+        m = int(rng.choice([d for d in (2, 4, 8) if n % d == 0 and d <= n]))
+        r = n // gpus
+        protocol = int(rng.choice([0, 1, 2] if r == 1 else [0, 1]))
+        grid = int(rng.choice([0, 3, 8, 16]))
+        lag = int(rng.integers(1, 6))
+        rel = int(rng.integers(1, 5))
+        mode = int(rng.integers(0, 2))
+        cases.append((gpus, n, m, protocol, grid, lag, rel, mode))
+    return cases
+
+
+@pytest.mark.parametrize("gpus,n,m,protocol,grid,lag,rel,mode", _stress_cases())
+def test_stress_thousand_iterations_random_shapes(tmp_path, gpus, n, m, protocol, grid, lag, rel, mode):
+    buckets = [3001, 17, 4099]
+    T = 1000
+    X, V = _launch(tmp_path, gpus, n, m, T, buckets, mode, grid=grid, lag=lag, path=4, protocol=protocol,
+                   release_every=rel)
+    x, v = _oracle(n, m, sum(buckets), T, mode)
     _compare(X, x)
     _compare(V, v)

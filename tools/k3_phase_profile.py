@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--rel-delay", type=int, default=0)
     ap.add_argument("--rel-every", type=int, default=0)
+    ap.add_argument("--protocol", type=int, default=0)
+    ap.add_argument("--experiment", type=int, default=0)
     ap.add_argument("--out", default="gpurun_out/k3_phases.json")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -53,6 +55,10 @@ def main():
         opts[C.OPT_RELEASE_DELAY] = a.rel_delay
     if a.rel_every:
         opts[C.OPT_RELEASE_EVERY] = a.rel_every
+    if a.protocol:
+        opts[C.OPT_PROTOCOL] = a.protocol
+    if a.experiment:
+        opts[C.OPT_EXPERIMENT] = a.experiment
     eng = SESGDEngine(a.workers, a.gsize, buckets, rank=rank, world=world, p2p_variant=a.variant,
                       path=a.path, grid=a.grid, options=opts)
     C.sesgd_set_option(eng.ctx, C.OPT_PROFILE, 1)
@@ -90,6 +96,12 @@ def main():
                "compute_total": cp[:, 2].mean() / a.iters / 1e3,
                "compute_total_max": cp[:, 2].max() / a.iters / 1e3},
            "launches_seen": int(prof[:, 7].max()), "launches": launches}
+    if a.protocol == 2:  # K4W warp groups (p2p_ws.cu): leader-thread timers per CTA
+        us = lambda col: cp[:, col].mean() / a.iters / 1e3  # noqa: E731
+        res["per_iter_us"] = {"S_stream": us(0), "S_wait_ring_free": us(4), "R_fold": us(1),
+                              "R_wait_ring_full": us(5), "R_poll_spin": us(6), "F_gather": us(3),
+                              "F_poll_spin": us(2), "S_stream_max": cp[:, 0].max() / a.iters / 1e3,
+                              "F_gather_max": cp[:, 3].max() / a.iters / 1e3}
     allres = [None] * world
     dist.all_gather_object(allres, res)
     if rank == 0:

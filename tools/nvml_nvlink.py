@@ -1,4 +1,5 @@
-"""NVLink byte counters from NVML (no profiler): cumulative per-link TX / RX data throughput
+"""NVLink byte counters from NVML (probe only: on this pool's B200s the throughput fields answer
+NVML_ERROR_NOT_SUPPORTED and `nvidia-smi nvlink -gt d` prints N/A, profiles/r02_nvsmi_nvlink.txt) (no profiler): cumulative per-link TX / RX data throughput
 counters (field ids NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX = 138/139, RAW 140/141, KiB,
 nvml.h), summed over the device's links.  Read before and after a timed region they give the
 NVLink bytes the kernels actually moved (the "NVLink bus GB/s" of the north star) while the
