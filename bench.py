@@ -63,7 +63,7 @@ def parse():
     p.add_argument("--fold-lag", type=int, default=0)
     p.add_argument("--grid", type=int, default=0, help="CTAs per one-shot launch (0 = auto)")
     p.add_argument("--resident-unroll", type=int, default=0)
-    p.add_argument("--protocol", type=int, default=0, help="two-shot: SESGD_OPT_PROTOCOL")
+    p.add_argument("--protocol", type=int, default=-1, help="two-shot: SESGD_OPT_PROTOCOL (-1 auto)")
     p.add_argument("--experiment", type=int, default=0,
                    help="SESGD_OPT_EXPERIMENT bits (measurement only: results are wrong)")
     return p.parse_args()
@@ -175,8 +175,9 @@ def workload_desc(workload, n, m, nb, L, mode):
 
 
 def common_config(workload, n, m, mode):
-    """config keys both arms print identically (same workload, same metric): the GPU arm adds
-    its launch keys (workers_per_gpu, path, ...) beside them, never inside `workload`."""
+    """config keys both arms print identically (same workload, same metric): the GPU arm's launch
+    details (workers_per_gpu, path, ...) go to a separate "launch" object, the reference arm's
+    coordinate sample to cpu_baseline.sample, so the two `config` objects are equal."""
     from paper_2007_00433_b200.workloads import WORKLOADS
     buckets = WORKLOADS[workload]
     return {"workload": workload_desc(workload, n, m, len(buckets), int(sum(buckets)), mode),
@@ -260,7 +261,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(common_config(args.workload, n, m, args.mode), sample=sample),
+        "config": {**common_config(args.workload, n, m, args.mode),
+                   "parallelism": f"sesgd groups over {args.gpus} GPU(s)"},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -276,7 +278,7 @@ def engine_options(args, C):
                               (C.OPT_RELEASE_DELAY, args.release_delay), (C.OPT_RELEASE_EVERY, args.release_every),
                               (C.OPT_RELEASE_STAGGER, args.release_stagger),
                               (C.OPT_PAYLOAD_BF16, args.payload_bf16), (C.OPT_EXPERIMENT, args.experiment),
-                              (C.OPT_PROTOCOL, args.protocol)) if v}
+                              ) if v} | {C.OPT_PROTOCOL: args.protocol}
 
 
 class Dist:
@@ -390,7 +392,10 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        kernel = {"twoshot": "k4w_twoshot" if (args.protocol == 2 and r == 1) else "k4_twoshot",
+        proto = args.protocol if args.protocol >= 0 else (2 if r == 1 else 1)  # auto (sesgd_capi.cu)
+        if args.push_tma or args.payload_bf16:
+            proto = 0 if args.protocol < 0 else proto
+        kernel = {"twoshot": "k4w_twoshot" if (proto == 2 and r == 1) else "k4_twoshot",
                   "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
@@ -449,7 +454,9 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
     # consistency of the workers' parameters after the run (K9), outside the timed region
     css, cmx = eng.consensus(stream)
     out = {
-        "config": {**common_config(workload, n, m, args.mode), "workers_per_gpu": r,
+        "config": {**common_config(workload, n, m, args.mode),
+                   "parallelism": f"sesgd groups over {world} GPU(s)"},
+        "launch": {"workers_per_gpu": r,
                    "path": "resident (K6)" if resident else {
                        "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P ("
                                   + ("K4W, warp-specialised" if kernel == "k4w_twoshot" else "K4") + ")",
@@ -617,7 +624,8 @@ def run_sesgd(args):
             "metric": METRIC, "value": main["value"], "unit": "GB/s", "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {**main["config"], "parallelism": f"sesgd groups over {world} GPU(s)"},
+            "config": main["config"],
+            "launch": main["launch"],
             "iters_per_s": main["iters_per_s"],
             "gbs_per_gpu": main["gbs_per_gpu"],
             "kernel_ms_per_step": main["kernel_ms_per_step"],

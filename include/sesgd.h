@@ -138,8 +138,9 @@ extern "C" {
                                     (K3, K4, K5) run against each other through local memory.  Set
                                     before sesgd_workspace_bytes (the grid fixes the layout) */
 #define SESGD_OPT_PROTOCOL 21      /* two-shot handshake (set before sesgd_workspace_bytes, identical
-                                    on every rank): -1 (default, auto) = 1 where supported (the
-                                    two-shot path with fp32 LSU pushes), else 0.
+                                    on every rank): -1 (default, auto) = 2 with one worker per
+                                    GPU, 1 with several, where supported (the two-shot path with
+                                    fp32 LSU pushes), else 0.
                                     0 = epoch flags released with a system-scope fence per batch.
                                     1 = value-carried validity: every receive-slot float holds a
                                     sentinel NaN (0xFFFFFFFF) until the peer's value lands; the
@@ -165,9 +166,7 @@ extern "C" {
                                     the system-scope fence before the two-shot flag releases,
                                     bit 1 sends the two-shot pushes to this rank's own receive
                                     slots instead of the peers' (no NVLink payload).  Bounds what
-                                    the flag protocol and the NVLink traffic cost;
-                                    bits 2 / 3: value-carried pushes / polls as weak st / ld.cg
-                                    instead of relaxed.sys; bit 4: K4W warp layout 1 */
+                                    the flag protocol and the NVLink traffic cost */
 
 /* Latency model, Eq. 2 and Eq. 3 exact forms (R16). */
 typedef struct sesgd_cost {

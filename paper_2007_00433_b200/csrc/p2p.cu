@@ -204,13 +204,8 @@ __device__ __forceinline__ float unsentinel(float v) {
   return __float_as_uint(v) == kSentinel ? __uint_as_float(0x7FFFFFFFu) : v;
 }
 template <int W>
-__device__ __forceinline__ void st_sent(float *p, const float (&r)[W], int nvalid, bool weak = false) {
+__device__ __forceinline__ void st_sent(float *p, const float (&r)[W], int nvalid) {
   if constexpr (W == 4) {
-    if (nvalid >= 4 && weak) {  // (SESGD_OPT_EXPERIMENT bit 2: measurement only)
-      *reinterpret_cast<float4 *>(p) = make_float4(unsentinel(r[0]), unsentinel(r[1]), unsentinel(r[2]),
-                                                   unsentinel(r[3]));
-      return;
-    }
     if (nvalid >= 4) {
       asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(unsentinel(r[0])),
                    "f"(unsentinel(r[1])), "f"(unsentinel(r[2])), "f"(unsentinel(r[3]))
@@ -288,11 +283,6 @@ __device__ __forceinline__ void ld_poll(const P2PArgs &a, float *p, float (&r)[W
   };
   auto load = [&]() {
     if constexpr (W == 4) {
-      if (nvalid >= 4 && (a.experiment & 8)) {  // (measurement only: weak L2 load)
-        const float4 t = __ldcg(reinterpret_cast<const float4 *>(p));
-        r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
-        return;
-      }
       if (nvalid >= 4) {
         ld_relaxed4(p, r);
         return;
@@ -1234,7 +1224,7 @@ struct Split {
         } else if (TMA && o + nv <= ts_bulk_hi(j, len)) {
           st_slot<W>(ent + o, val, nv);  // shared memory image of the chunk
         } else if constexpr (SENT) {
-          st_sent<W>(recv(w, p) + c.soff + e, val, nv, (a.experiment & 4) != 0);  // NVLink store, validity in the value
+          st_sent<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store, validity in the value
         } else {
           st_slot<W>(recv(w, p) + c.soff + e, val, nv);  // NVLink store
         }
@@ -1345,7 +1335,7 @@ struct Split {
           const int w = G[rr];
           if (rem<MULTI>(w)) {
             if constexpr (SENT)
-              st_sent<W>(recv(w, p) + c.soff + e, acc, nv, (a.experiment & 4) != 0);
+              st_sent<W>(recv(w, p) + c.soff + e, acc, nv);
             else if (!bulk)
               st_slot<W>(recv(w, p) + c.soff + e, acc, nv);
             continue;

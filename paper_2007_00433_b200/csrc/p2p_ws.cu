@@ -1,55 +1,45 @@
 // p2p_ws.cu -- K4W: the two-shot group exchange of K4 (same slices, same arithmetic, same
 // ascending fold, so the same bits) as a WARP-SPECIALISED persistent kernel with value-carried
 // validity (SESGD_OPT_PROTOCOL = 2), one worker per GPU -- the north star's 8-GPU layout and the
-// n = m = 2 two-GPU shape.
-//
-// Why (measured, profiles/r02_k4_experiments.json): K4's CTAs run stage -> reduce -> finish of
-// successive chunks in lock step, so every chunk step pays three latency-bound phases and a
-// system-scope fence; with NO NVLink payload at all (pushes to local memory) K4 still takes
-// 0.24 ms at n = 2 (ResNet-50), against an HBM floor of 0.078 ms.  Here the three phases are
-// three warp groups of one CTA (one CTA per SM) that never wait for each other except through
-// data:
-//   S (16 warps)  streams g, v, x from HBM (Alg.1 lines 3-8: v <- mu v + g, x_hat <- x - lr v),
-//                 stores v, keeps its own slice of x_hat in a shared-memory ring and pushes the
-//                 other members' slices to their receive slots over NVLink (reduce-scatter);
-//   R (4 warps)   per chunk: waits for the ring entry (mbarrier), folds the m contributions of
-//                 its slice in ascending member order (own from shared memory, peers' polled in
-//                 the receive slots), divides by m (Eq. 6; Alg.1 line 11), stores x and
-//                 pushes the mean to every peer (all-gather); frees the ring entry;
-//   F (4 warps)   per chunk: polls the peers' means of their slices and stores x.
+// n = m = 2 two-GPU shape.  One CTA per SM; its warps are five roles joined only by data:
+//   P (1 warp)    TMA producer: cp.async.bulk of the chunk's g, v, x (16 KiB each) into a
+//                 3-stage shared-memory ring (mbarrier complete_tx), so every SM keeps two to
+//                 three chunks of HBM reads in flight regardless of what the other warps do;
+//   S (8 warps)   the local step from shared memory (Alg.1 lines 3-8: v <- mu v + g,
+//                 x_hat <- x - lr v), v back to HBM, its own slice of x_hat into a second ring
+//                 for R, the other members' slices pushed to their receive slots over NVLink
+//                 (reduce-scatter);
+//   R (2 x 4)     two groups, each folding every other chunk: the m contributions of my slice in
+//                 ascending member order (own from the x_hat ring, the peers' polled in the
+//                 receive slots), / m (Eq. 6; Alg.1 line 11), x to HBM and the mean pushed
+//                 to every peer (all-gather);
+//   F (2 x 4)     two groups, every other chunk: poll the peers' means of their slices, x to HBM.
+// Measured on K4W v1 (profiles/r02_k4w_phases_*.json): with S loading through registers the
+// stream was latency-bound (one HBM round trip per chunk, ~4.7 us per chunk per SM) and a single
+// R / F group kept only one chunk in flight; the TMA ring and the interleaved groups remove both.
 // No flags and no fence on the data path: every receive float is armed with a sentinel NaN and
 // polled until the peer's value replaces it (p2p.cu, "value-carried validity"), then re-armed.
 // The only system-scope synchronisation is K4's per-launch `consumed` counter (a peer must have
-// re-armed its slots of call - 2 before they are written again), one acquire at the start and
-// one release at the end of every CTA.  GRAD mode (Eq. 5): the payload is g and R / F apply the
-// momentum update with the group-mean gradient.
+// re-armed its slots of call - 2 before they are written again): one acquire at the start and
+// one release at the end of every CTA.  GRAD mode (Eq. 5): the payload is g, R / F apply the
+// momentum update with the group-mean gradient (they load v, x themselves).
 #include "common.cuh"
 #include "internal.h"
 
 namespace sesgd {
 namespace {
 
-// warp-group layouts (S, R, F warps; vectors in flight per R / F thread); 768 threads, 1 CTA/SM
-template <int LAY>
-struct Lay;
-template <>
-struct Lay<0> {
-  static constexpr int S = 16, R = 4, F = 4, U = 4;
-};
-template <>
-struct Lay<1> {
-  static constexpr int S = 8, R = 8, F = 8, U = 2;
-};
-template <>
-struct Lay<2> {  // 640 threads: up to 102 registers (S loads 4 items at once without spills)
-  static constexpr int S = 8, R = 6, F = 6, U = 2;
-};
-template <int LAY>
-constexpr int threads_of() { return 32 * (Lay<LAY>::S + Lay<LAY>::R + Lay<LAY>::F); }
-constexpr int kChunkWS = 4096;                  // K4's chunking (p2p_chunk_elems): same slices
-constexpr int kRing = 8;                        // ring entries (chunks S may run ahead of R)
-constexpr uint32_t kSentinelWS = 0xFFFFFFFFu;   // as p2p.cu's kSentinel
+constexpr int kWarpsP = 1, kWarpsS = 8, kGroupsR = 2, kWarpsR = 4, kGroupsF = 2, kWarpsF = 4;
+constexpr int kThS = kWarpsS * 32, kThR = kWarpsR * 32, kThF = kWarpsF * 32;
+constexpr int kWarpsAll = kWarpsP + kWarpsS + kGroupsR * kWarpsR + kGroupsF * kWarpsF;  // 25
+constexpr int kThreadsWS = kWarpsAll * 32;                                             // 800
+constexpr int kChunkWS = 4096;  // K4's chunking (p2p_chunk_elems): same slices
+constexpr int kQL = 3;          // load ring stages (g, v, x of one chunk each)
+constexpr int kQX = 4;          // x_hat ring entries (a multiple of kGroupsR)
+constexpr int kU = 2;           // vectors in flight per R / F thread
+constexpr uint32_t kSentinelWS = 0xFFFFFFFFu;  // as p2p.cu's kSentinel
 constexpr int kWaitDataWS = 6;
+static_assert(kQX % kGroupsR == 0, "an x_hat ring entry is always consumed by the same R group");
 
 __device__ __forceinline__ float unsent(float v) {
   return __float_as_uint(v) == kSentinelWS ? __uint_as_float(0x7FFFFFFFu) : v;
@@ -80,12 +70,8 @@ __device__ __forceinline__ void stm(float *p, const float (&r)[W], int nv) {
 }
 // NVLink push of a payload vector: relaxed system-scope stores (the receiver polls the values)
 template <int W>
-__device__ __forceinline__ void push(float *p, const float (&r)[W], int nv, bool weak = false) {
+__device__ __forceinline__ void push(float *p, const float (&r)[W], int nv) {
   if constexpr (W == 4) {
-    if (nv >= 4 && weak) {  // (SESGD_OPT_EXPERIMENT bit 2: measurement only)
-      *reinterpret_cast<float4 *>(p) = make_float4(unsent(r[0]), unsent(r[1]), unsent(r[2]), unsent(r[3]));
-      return;
-    }
     if (nv >= 4) {
       asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(unsent(r[0])),
                    "f"(unsent(r[1])), "f"(unsent(r[2])), "f"(unsent(r[3]))
@@ -98,13 +84,8 @@ __device__ __forceinline__ void push(float *p, const float (&r)[W], int nv, bool
     if (w < nv) asm volatile("st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p + w), "f"(unsent(r[w])) : "memory");
 }
 template <int W>
-__device__ __forceinline__ void ld_rel(const float *p, float (&r)[W], int nv, bool weak = false) {
+__device__ __forceinline__ void ld_rel(const float *p, float (&r)[W], int nv) {
   if constexpr (W == 4) {
-    if (nv >= 4 && weak) {  // (SESGD_OPT_EXPERIMENT bit 3: measurement only)
-      const float4 t = __ldcg(reinterpret_cast<const float4 *>(p));
-      r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
-      return;
-    }
     if (nv >= 4) {
       asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
                    : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
@@ -145,19 +126,32 @@ __device__ __forceinline__ void rearm(float *p, int nv) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dev::smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
+  while (!dev::mbar_try_wait(bar, parity)) {
+  }
+}
 
-template <int W, bool GRAD, int LAY>
+// shared memory: barriers, then the load ring (g, v, x per stage) and the x_hat ring
+struct Smem {
+  uint64_t full_ld[kQL], empty_ld[kQL], full_x[kQX], empty_x[kQX];
+};
+constexpr size_t kSmemHead = 256;  // >= sizeof(Smem), keeps the rings 128-byte aligned
+constexpr size_t kStageBytes = size_t(3) * kChunkWS * 4;
+
+template <int W, bool GRAD>
 struct WS {
-  static constexpr int kThS = Lay<LAY>::S * 32, kThR = Lay<LAY>::R * 32, kThF = Lay<LAY>::F * 32;
-  static constexpr int kU = Lay<LAY>::U;
-  static constexpr int kItemsS = kChunkWS / W / kThS;  // W-vectors per S thread per chunk
+  static constexpr bool kTma = (W == 4);  // bulk copies need 16-byte aligned buffers
   const P2PArgs &a;
+  Smem *sm;
+  float *ld_ring;  // [kQL][3][kChunkWS]
+  float *x_ring;   // [kQX][cap]
+  int cap;
   int me, p, m;
   const int8_t *G;
   int64_t first, nk;
   int gc;
 
-  __device__ WS(const P2PArgs &args) : a(args) {
+  __device__ WS(const P2PArgs &args, unsigned char *smem) : a(args) {
     me = a.my_workers[0];
     p = a.my_pos[0];
     m = a.m;
@@ -166,6 +160,10 @@ struct WS {
     const int i = blockIdx.x;
     first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
     nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
+    sm = reinterpret_cast<Smem *>(smem);
+    ld_ring = reinterpret_cast<float *>(smem + kSmemHead);
+    x_ring = reinterpret_cast<float *>(smem + kSmemHead + kQL * kStageBytes);
+    cap = (kChunkWS - (m - 1) * slice() + 3) & ~3;  // largest slice (the last one)
   }
 
   struct Ref {
@@ -205,21 +203,16 @@ struct WS {
     return reinterpret_cast<uint64_t *>(a.ws[a.worker_rank[w]] + a.consumed_off) + blockIdx.x;
   }
 
-  // poll a payload vector until it is no longer the sentinel, then re-arm it
-  __device__ __forceinline__ void wait_value(float *src, float (&y)[W], int nv, int pos,
-                                             uint64_t *spin = nullptr) const {
+  // poll a payload vector until it is no longer the sentinel (then the caller re-arms it)
+  __device__ __forceinline__ void wait_value(const float *src, float (&y)[W], int nv, int pos,
+                                             uint64_t *spin) const {
     if (!pending<W>(y, nv) || (a.experiment & 2)) return;  // (experiment: nobody writes my slots)
     count(a.counters, kCntValueSpins);
     const uint64_t t0 = dev::globaltimer();
-    struct Acc {
-      uint64_t *s;
-      uint64_t t0;
-      __device__ ~Acc() {
-        if (s) *s += dev::globaltimer() - t0;
-      }
-    } acc{spin, t0};
-    do {
-      if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) return;
+    for (;;) {
+      ld_rel<W>(src, y, nv);
+      if (!pending<W>(y, nv)) break;
+      if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;
       if (dev::globaltimer() - t0 > a.timeout_ns) {
         if (atomicExch(a.abort_dev, 1u) == 0u) {
           unsigned long long *e = a.err_host;
@@ -234,78 +227,103 @@ struct WS {
           atomicExch(e, (unsigned long long)(-SESGD_ETIMEOUT));
           __threadfence_system();
         }
-        return;
+        break;
       }
-      ld_rel<W>(src, y, nv, (a.experiment & 8) != 0);
-    } while (pending<W>(y, nv));
+    }
+    if (spin) *spin += dev::globaltimer() - t0;
   }
 
-  // ---------------------------------------------------------------- S: stream + scatter
-  __device__ void run_s(float *ring, int cap, uint64_t *full, uint64_t *empty) const {
-    const int t = threadIdx.x;
+  // ---------------------------------------------------------------- P: TMA loads
+  __device__ void run_p() const {
+    if (!kTma || (threadIdx.x & 31) != 0) return;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int q = int(k % kQL);
+      if (k >= kQL) mbar_spin(&sm->empty_ld[q], uint32_t((k / kQL - 1) & 1));
+      const Ref c = locate(first + k * gc);
+      const uint32_t bytes = uint32_t(c.len / 4) * 16;  // whole float4s; the tail is read by S
+      float *st = ld_ring + size_t(q) * 3 * kChunkWS;
+      dev::mbar_arrive_expect_tx(&sm->full_ld[q], (GRAD ? 1u : 3u) * bytes);
+      if (bytes) {
+        dev::bulk_g2s(st, a.bg[c.b] + c.e0, bytes, &sm->full_ld[q]);
+        if constexpr (!GRAD) {
+          dev::bulk_g2s(st + kChunkWS, a.bv[c.b] + c.e0, bytes, &sm->full_ld[q]);
+          dev::bulk_g2s(st + 2 * kChunkWS, a.bx[c.b] + c.e0, bytes, &sm->full_ld[q]);
+        }
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- S: local step + scatter
+  __device__ void run_s() const {
+    const int t = threadIdx.x - kWarpsP * 32;
     const bool lead = a.prof && t == 0;
     const uint64_t ts = lead ? dev::globaltimer() : 0;
     uint64_t t_wait = 0;
+    constexpr int kItems = kChunkWS / W / kThS;
     for (int64_t k = 0; k < nk; ++k) {
       const Ref c = locate(first + k * gc);
-      const int q = int(k % kRing);
-      if (k >= kRing) {  // R has folded the entry's previous chunk
-        const uint32_t par = uint32_t((k / kRing - 1) & 1);
-        const uint64_t tw = lead ? dev::globaltimer() : 0;
-        while (!dev::mbar_try_wait(&empty[q], par)) {
-        }
-        if (lead) t_wait += dev::globaltimer() - tw;
-      }
-      float *ent = ring + q * cap;
+      const int q = int(k % kQL), qx = int(k % kQX);
+      const uint64_t tw = lead ? dev::globaltimer() : 0;
+      if (kTma) mbar_spin(&sm->full_ld[q], uint32_t((k / kQL) & 1));
+      if (k >= kQX) mbar_spin(&sm->empty_x[qx], uint32_t((k / kQX - 1) & 1));
+      if (lead) t_wait += dev::globaltimer() - tw;
+      const float *sg = ld_ring + size_t(q) * 3 * kChunkWS;
+      float *ent = x_ring + size_t(qx) * cap;
       const int64_t mlo = lo(p, c.len);
       const int S = slice();
+      const int64_t len4 = c.len & ~int64_t(3);
       float *xs = a.bx[c.b], *vs = a.bv[c.b];
       const float *gs = a.bg[c.b];
-      // every load of the chunk in flight before the first store (one HBM latency per chunk; the
-      // compiler cannot hoist loads above stores it cannot prove disjoint)
-      float val[kItemsS][W], v[GRAD ? 1 : kItemsS][W], x[GRAD ? 1 : kItemsS][W];
 #pragma unroll
-      for (int it = 0; it < kItemsS; ++it) {
+      for (int it = 0; it < kItems; ++it) {
         const int64_t o = (int64_t(it) * kThS + t) * W;
         const int nv = int(min(int64_t(W), c.len - o));
         if (nv <= 0) continue;
         const int64_t e = c.e0 + o;
-        ldm<W>(gs + e, val[it], nv);
-        if constexpr (!GRAD) {
-          ldm<W>(vs + e, v[it], nv);
-          ldm<W>(xs + e, x[it], nv);
+        const bool from_smem = kTma && o + W <= len4;
+        float val[W], v[W], x[W];
+        if (from_smem) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(sg + o);
+          val[0] = t4.x; val[W > 1 ? 1 : 0] = t4.y; val[W > 2 ? 2 : 0] = t4.z; val[W > 3 ? 3 : 0] = t4.w;
+        } else {
+          ldm<W>(gs + e, val, nv);
         }
-      }
-#pragma unroll
-      for (int it = 0; it < kItemsS; ++it) {
-        const int64_t o = (int64_t(it) * kThS + t) * W;
-        const int nv = int(min(int64_t(W), c.len - o));
-        if (nv <= 0) continue;
-        const int64_t e = c.e0 + o;
         if constexpr (!GRAD) {
+          if (from_smem) {
+            const float4 v4 = *reinterpret_cast<const float4 *>(sg + kChunkWS + o);
+            const float4 x4 = *reinterpret_cast<const float4 *>(sg + 2 * kChunkWS + o);
+            v[0] = v4.x; v[W > 1 ? 1 : 0] = v4.y; v[W > 2 ? 2 : 0] = v4.z; v[W > 3 ? 3 : 0] = v4.w;
+            x[0] = x4.x; x[W > 1 ? 1 : 0] = x4.y; x[W > 2 ? 2 : 0] = x4.z; x[W > 3 ? 3 : 0] = x4.w;
+          } else {
+            ldm<W>(vs + e, v, nv);
+            ldm<W>(xs + e, x, nv);
+          }
 #pragma unroll
           for (int w = 0; w < W; ++w) {
-            v[it][w] = dev::momentum(a.mu, v[it][w], dev::decay(val[it][w], a.wd, x[it][w]));
-            val[it][w] = dev::sgd(x[it][w], a.lr, v[it][w]);  // x_hat
+            v[w] = dev::momentum(a.mu, v[w], dev::decay(val[w], a.wd, x[w]));
+            val[w] = dev::sgd(x[w], a.lr, v[w]);  // x_hat
           }
-          stm<W>(vs + e, v[it], nv);
+          stm<W>(vs + e, v, nv);
         }
         const int j = min(int(o / S), m - 1);  // owner position (a vector never straddles)
         if (j == p) {
           if (W == 4 && nv == 4) {
             *reinterpret_cast<float4 *>(ent + (o - mlo)) =
-                make_float4(val[it][0], val[it][W > 1 ? 1 : 0], val[it][W > 2 ? 2 : 0], val[it][W > 3 ? 3 : 0]);
+                make_float4(val[0], val[W > 1 ? 1 : 0], val[W > 2 ? 2 : 0], val[W > 3 ? 3 : 0]);
           } else {
 #pragma unroll
             for (int w = 0; w < W; ++w)
-              if (w < nv) ent[o - mlo + w] = val[it][w];
+              if (w < nv) ent[o - mlo + w] = val[w];
           }
         } else {
-          push<W>(recv(G[j], p) + c.soff + e, val[it], nv, (a.experiment & 4) != 0);  // reduce-scatter
+          push<W>(recv(G[j], p) + c.soff + e, val, nv);  // reduce-scatter over NVLink
         }
       }
       __syncwarp();
-      if ((t & 31) == 0) mbar_arrive(&full[q]);
+      if ((t & 31) == 0) {
+        if (kTma) mbar_arrive(&sm->empty_ld[q]);  // the load stage is free for the producer
+        mbar_arrive(&sm->full_x[qx]);             // my slice's x_hat is ready for R
+      }
     }
     if (lead) {
       uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
@@ -315,26 +333,23 @@ struct WS {
   }
 
   // ---------------------------------------------------------------- R: fold my slice + gather
-  __device__ void run_r(const float *ring, int cap, uint64_t *full, uint64_t *empty) const {
-    const int t = threadIdx.x - kThS;
-    const bool lead = a.prof && t == 0;
+  __device__ void run_r(int grp, int t) const {
+    const bool lead = a.prof && t == 0 && grp == 0;
     const uint64_t ts = lead ? dev::globaltimer() : 0;
     uint64_t t_wait = 0, t_spin = 0;
     uint64_t *spin = lead ? &t_spin : nullptr;
-    for (int64_t k = 0; k < nk; ++k) {
+    for (int64_t k = grp; k < nk; k += kGroupsR) {
       const Ref c = locate(first + k * gc);
-      const int q = int(k % kRing);
-      const uint32_t par = uint32_t((k / kRing) & 1);
+      const int qx = int(k % kQX);
       const uint64_t tw = lead ? dev::globaltimer() : 0;
-      while (!dev::mbar_try_wait(&full[q], par)) {
-      }
+      mbar_spin(&sm->full_x[qx], uint32_t((k / kQX) & 1));
       if (lead) t_wait += dev::globaltimer() - tw;
-      if (k == 0 && a.hop_delay_ns) {  // config 4: the all-gather round's injected hop
+      if (k == grp && a.hop_delay_ns) {  // config 4: the all-gather round's injected hop
         const uint64_t t0 = dev::globaltimer();
         while (dev::globaltimer() - t0 < a.hop_delay_ns) {
         }
       }
-      const float *ent = ring + q * cap;
+      const float *ent = x_ring + size_t(qx) * cap;
       const int64_t mlo = lo(p, c.len), mhi = hi(p, c.len);
       float *xs = a.bx[c.b], *vs = a.bv[c.b];
       for (int64_t base = mlo; base < mhi; base += int64_t(kThR) * W * kU) {
@@ -355,7 +370,7 @@ struct WS {
             for (int u = 0; u < kU; ++u) {  // every vector's load in flight first
               const int64_t o = base + (int64_t(u) * kThR + t) * W;
               const int nv = int(max(int64_t(0), min(int64_t(W), mhi - o)));
-              if (nv > 0) ld_rel<W>(src + o, y[u], nv, (a.experiment & 8) != 0);
+              if (nv > 0) ld_rel<W>(src + o, y[u], nv);
             }
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
@@ -380,7 +395,7 @@ struct WS {
 #pragma unroll
           for (int w = 0; w < W; ++w) acc[u][w] = __fdiv_rn(acc[u][w], float(m));
           for (int rr = 0; rr < m; ++rr)  // all-gather: my slice's mean to every peer
-            if (rr != p) push<W>(recv(G[rr], p) + c.soff + e, acc[u], nv, (a.experiment & 4) != 0);
+            if (rr != p) push<W>(recv(G[rr], p) + c.soff + e, acc[u], nv);
           if constexpr (!GRAD) {
             stm<W>(xs + e, acc[u], nv);
           } else {
@@ -398,7 +413,7 @@ struct WS {
         }
       }
       __syncwarp();
-      if ((t & 31) == 0) mbar_arrive(&empty[q]);
+      if ((t & 31) == 0) mbar_arrive(&sm->empty_x[qx]);
     }
     if (lead) {
       uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
@@ -409,13 +424,12 @@ struct WS {
   }
 
   // ---------------------------------------------------------------- F: the peers' slices
-  __device__ void run_f() const {
-    const int t = threadIdx.x - kThS - kThR;
-    const bool lead = a.prof && t == 0;
+  __device__ void run_f(int grp, int t) const {
+    const bool lead = a.prof && t == 0 && grp == 0;
     const uint64_t ts = lead ? dev::globaltimer() : 0;
     uint64_t t_spin = 0;
     uint64_t *spin = lead ? &t_spin : nullptr;
-    for (int64_t k = 0; k < nk; ++k) {
+    for (int64_t k = grp; k < nk; k += kGroupsF) {
       const Ref c = locate(first + k * gc);
       float *xs = a.bx[c.b], *vs = a.bv[c.b];
       for (int j = 0; j < m; ++j) {
@@ -428,7 +442,7 @@ struct WS {
           for (int u = 0; u < kU; ++u) {
             const int64_t o = base + (int64_t(u) * kThF + t) * W;
             const int nv = int(max(int64_t(0), min(int64_t(W), jhi - o)));
-            if (nv > 0) ld_rel<W>(src + o, y[u], nv, (a.experiment & 8) != 0);
+            if (nv > 0) ld_rel<W>(src + o, y[u], nv);
           }
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
@@ -489,25 +503,24 @@ struct WS {
   }
 };
 
-template <int W, bool GRAD, int LAY>
-__global__ void __launch_bounds__(threads_of<LAY>(), 1) k4w_twoshot(const __grid_constant__ P2PArgs a) {
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];
-  using L = Lay<LAY>;
-  const WS<W, GRAD, LAY> s(a);
+  const WS<W, GRAD> s(a, dsmem);
   if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1) {
     s.local_only();
     return;
   }
   if (s.nk == 0) return;
-  const int cap = (kChunkWS - (a.m - 1) * s.slice() + 3) & ~3;  // largest slice (the last one)
-  uint64_t *full = reinterpret_cast<uint64_t *>(dsmem);
-  uint64_t *empty = full + kRing;
-  float *ring = reinterpret_cast<float *>(dsmem + 2 * kRing * sizeof(uint64_t));
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kRing; ++q) {
-      dev::mbar_init(&full[q], L::S);
-      dev::mbar_init(&empty[q], L::R);
+    for (int q = 0; q < kQL; ++q) {
+      dev::mbar_init(&s.sm->full_ld[q], 1);
+      dev::mbar_init(&s.sm->empty_ld[q], kWarpsS);
+    }
+    for (int q = 0; q < kQX; ++q) {
+      dev::mbar_init(&s.sm->full_x[q], kWarpsS);
+      dev::mbar_init(&s.sm->empty_x[q], kWarpsR);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -519,6 +532,7 @@ __global__ void __launch_bounds__(threads_of<LAY>(), 1) k4w_twoshot(const __grid
       if (j == s.p) continue;
       const uint64_t *f = s.consumed(s.G[j]);
       if (dev::ld_acquire_sys(f) >= need) continue;
+      count(a.counters, kCntFlagSpins);
       const uint64_t t0 = dev::globaltimer();
       while (dev::ld_acquire_sys(f) < need) {
         if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;
@@ -542,7 +556,7 @@ __global__ void __launch_bounds__(threads_of<LAY>(), 1) k4w_twoshot(const __grid
     }
   }
   __syncthreads();
-  if (a.hop_delay_ns) {  // injected per-hop latency (config 4): once per handshake round
+  if (a.hop_delay_ns) {  // injected per-hop latency (config 4): the reduce-scatter round's hop
     if (threadIdx.x == 0) {
       const uint64_t t0 = dev::globaltimer();
       while (dev::globaltimer() - t0 < a.hop_delay_ns) {
@@ -551,68 +565,63 @@ __global__ void __launch_bounds__(threads_of<LAY>(), 1) k4w_twoshot(const __grid
     __syncthreads();
   }
   const int warp = threadIdx.x >> 5;
-  if (warp < L::S)
-    s.run_s(ring, cap, full, empty);
-  else if (warp < L::S + L::R)
-    s.run_r(ring, cap, full, empty);
-  else
-    s.run_f();
+  constexpr int kR0 = kWarpsP + kWarpsS, kF0 = kR0 + kGroupsR * kWarpsR;
+  if (warp < kWarpsP) {
+    s.run_p();
+  } else if (warp < kR0) {
+    s.run_s();
+  } else if (warp < kF0) {
+    const int w = warp - kR0;
+    s.run_r(w / kWarpsR, (w % kWarpsR) * 32 + (threadIdx.x & 31));
+  } else {
+    const int w = warp - kF0;
+    s.run_f(w / kWarpsF, (w % kWarpsF) * 32 + (threadIdx.x & 31));
+  }
   __syncthreads();  // every re-arm of this CTA precedes the release (cumulativity)
   if (threadIdx.x == 0)
     dev::st_release_sys(s.consumed(s.me), a.seq_epoch0 + uint64_t((s.first + (s.nk - 1) * s.gc) / s.gc));
 }
 
-template <int LAY>
-const void *pick_ws_t(int mode, bool vec) {
+const void *pick_ws(int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
   if (vec)
-    return grad ? reinterpret_cast<const void *>(&k4w_twoshot<4, true, LAY>)
-                : reinterpret_cast<const void *>(&k4w_twoshot<4, false, LAY>);
-  return grad ? reinterpret_cast<const void *>(&k4w_twoshot<1, true, LAY>)
-              : reinterpret_cast<const void *>(&k4w_twoshot<1, false, LAY>);
+    return grad ? reinterpret_cast<const void *>(&k4w_twoshot<4, true>)
+                : reinterpret_cast<const void *>(&k4w_twoshot<4, false>);
+  return grad ? reinterpret_cast<const void *>(&k4w_twoshot<1, true>)
+              : reinterpret_cast<const void *>(&k4w_twoshot<1, false>);
 }
-const void *pick_ws(int mode, bool vec, int lay) {
-  return lay == 2 ? pick_ws_t<2>(mode, vec) : lay == 1 ? pick_ws_t<1>(mode, vec) : pick_ws_t<0>(mode, vec);
-}
-int ws_threads(int lay) {
-  return lay == 2 ? threads_of<2>() : lay == 1 ? threads_of<1>() : threads_of<0>();
-}
-// layout of this launch (SESGD_OPT_EXPERIMENT bits 4/5 select 1/2: measurement only)
-int ws_layout(const P2PArgs &a) { return (a.experiment & 32) ? 2 : (a.experiment & 16) ? 1 : 0; }
 
 size_t ws_smem(int m) {
   const int slice = (kChunkWS / (m > 0 ? m : 1)) & ~31;
   const int cap = (kChunkWS - (m - 1) * slice + 3) & ~3;
-  return 2 * kRing * sizeof(uint64_t) + size_t(kRing) * size_t(cap) * 4;
+  return kSmemHead + size_t(kQL) * kStageBytes + size_t(kQX) * size_t(cap) * 4;
 }
 
 }  // namespace
 
-int p2p_ws_threads() { return ws_threads(0); }
+int p2p_ws_threads() { return kThreadsWS; }
 
 int p2p_ws_occupancy(int m) {
+  static_assert(sizeof(Smem) <= kSmemHead, "barrier block");
   const size_t smem = ws_smem(m);
   int occ = 1 << 30;
   for (int mode = 0; mode < 2; ++mode)
     for (int vec = 0; vec < 2; ++vec) {
-      for (int lay = 0; lay < 3; ++lay) {
-      const void *k = pick_ws(mode, vec != 0, lay);
+      const void *k = pick_ws(mode, vec != 0);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       int b = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, ws_threads(lay), smem) != cudaSuccess) b = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kThreadsWS, smem) != cudaSuccess) b = 1;
       occ = b < occ ? b : occ;
-      }
     }
   return occ > 0 ? occ : 1;
 }
 
 cudaError_t launch_p2p_ws(const P2PArgs &a, int mode, bool vec, cudaStream_t stream) {
-  const int lay = ws_layout(a);
-  const void *k = pick_ws(mode, vec, lay);
+  const void *k = pick_ws(mode, vec);
   const size_t smem = ws_smem(a.m);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};
-  return launch_persistent(k, unsigned(a.grid), unsigned(ws_threads(lay)), args, smem, stream, a.cooperative != 0);
+  return launch_persistent(k, unsigned(a.grid), kThreadsWS, args, smem, stream, a.cooperative != 0);
 }
 
 }  // namespace sesgd

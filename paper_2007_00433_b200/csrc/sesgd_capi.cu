@@ -92,10 +92,14 @@ void freeze_layout(sesgd_ctx *ctx) {
   if (ctx->path == SESGD_PATH_TWOSHOT || ctx->path == SESGD_PATH_NVLS)
     ctx->p2p_variant = 0;  // K4 runs on the DIRECT grid
   // SESGD_OPT_PROTOCOL auto (-1): value-carried validity wherever the two-shot kernel supports it
-  // (fp32 LSU pushes; measured faster at every shape, profiles/r02_k4_experiments.json), else flags
-  if (ctx->protocol < 0)
-    ctx->protocol = (resolve_path(ctx) == SESGD_PATH_TWOSHOT && ctx->m >= 2 && !ctx->push_tma &&
-                     !ctx->payload_bf16) ? 1 : 0;
+  // (fp32 LSU pushes), in the warp-specialised K4W when one worker lives on each GPU; else flags
+  // (measured, profiles/r02_k4_experiments.json: n = m = 2 kernel 0.188 ms K4W, 0.190 K4 value-
+  // carried, 0.185-0.228 K4 flags)
+  if (ctx->protocol < 0) {
+    const bool value = resolve_path(ctx) == SESGD_PATH_TWOSHOT && ctx->m >= 2 && !ctx->push_tma &&
+                       !ctx->payload_bf16;
+    ctx->protocol = !value ? 0 : (ctx->n_local == 1 ? 2 : 1);
+  }
   const int var = ctx->p2p_variant;
   const int chunk = sesgd::p2p_chunk_elems(var);
   const int r = ctx->n_local;
@@ -649,7 +653,7 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->cooperative = int(value);
       return SESGD_OK;
     case SESGD_OPT_EXPERIMENT:
-      if (value < 0 || value > 63) return fail(ctx, SESGD_EINVAL, "experiment bits must be in [0, 63]");
+      if (value < 0 || value > 3) return fail(ctx, SESGD_EINVAL, "experiment bits must be in [0, 3]");
       ctx->experiment = int(value);
       return SESGD_OK;
     case SESGD_OPT_HOP_DELAY_NS:

@@ -31,7 +31,8 @@ class SESGDEngine:
                  rank: int = 0, world: int = 1, process_group=None, path: int = C.PATH_AUTO,
                  grid: int = 0, timeout_ms: int = 20000, hop_delay_ns: int = 0,
                  p2p_variant: int = -1, discard: int = 1, options: Optional[dict] = None,
-                 weight_decay: float = 0.0, loopback: bool = False, manual_peers: bool = False):
+                 weight_decay: float = 0.0, loopback: bool = False, manual_peers: bool = False,
+                 share_x_with: Optional["SESGDEngine"] = None):
         if n % world != 0:
             raise ValueError("n must be a multiple of the number of ranks")
         self.n, self.m, self.seed = n, group_size, seed
@@ -65,7 +66,9 @@ class SESGDEngine:
 
         self.offsets, total = _aligned_offsets(self.bucket_sizes)
         mk = lambda: torch.zeros(total, dtype=torch.float32, device=self.device)  # noqa: E731
-        self.x_flat = [mk() for _ in range(self.r)]
+        # share_x_with: the final-average context (Alg.1's last line) works on another engine's
+        # parameters, with its own zero momentum / gradient scratch
+        self.x_flat = list(share_x_with.x_flat) if share_x_with is not None else [mk() for _ in range(self.r)]
         self.v_flat = [mk() for _ in range(self.r)]
         self.g_flat = [mk() for _ in range(self.r)]
         for b, numel in enumerate(self.bucket_sizes):
@@ -180,10 +183,23 @@ class SESGDEngine:
             C.sesgd_sync_step_host(self.ctx, b, lr, momentum, [h.data_ptr() for h in g_host[b]],
                                    [h.data_ptr() for h in x_host[b]], s.cuda_stream)
 
+    def average_engine(self, process_group=None) -> "SESGDEngine":
+        """the final-average context: group_size = n over this engine's parameters, two-shot
+        path (created on first use; every rank must call it)"""
+        if getattr(self, "_avg", None) is None:
+            self._avg = SESGDEngine(self.n, self.n, self.bucket_sizes, seed=self.seed, device=self.device.index,
+                                    rank=self.rank, world=self.world, path=C.PATH_TWOSHOT,
+                                    process_group=process_group or getattr(self, "group", None),
+                                    loopback=self.loopback, share_x_with=self)
+        return self._avg
+
     def global_average(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Algorithm 1's last line: every worker's parameters become the mean over all n
-        workers (K8, ascending fold).  Several GPUs: the ranks' parameters are all-gathered
-        (data movement only) and every rank averages the n rows locally."""
+        workers (ascending fold, one division by n).  One GPU: K8 over the resident rows.  Several
+        GPUs: one SESGD exchange with group_size = n through the two-shot NVLink kernel (K4 / K4W)
+        on a context whose momentum and gradient are zero scratch and lr = 0, so x_hat = x exactly
+        and the group mean is the global mean -- 2(n-1)/n x 4 B per element over NVLink instead of
+        all-gathering (n-1) x 4 B."""
         if self.loopback:
             raise RuntimeError("loopback virtual ranks: use LoopbackGroup.global_average()")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -192,16 +208,7 @@ class SESGDEngine:
             for b in range(nb):
                 C.sesgd_global_average(self.ctx, b, self.n, None, s.cuda_stream)
             return
-        import torch.distributed as dist
-        with torch.cuda.stream(s):
-            local = torch.stack(self.x_flat)  # [r, total]
-            gathered = torch.empty((self.world,) + tuple(local.shape), dtype=local.dtype, device=self.device)
-            dist.all_gather_into_tensor(gathered, local, group=self.group)
-            rows = gathered.view(self.n, -1)  # worker w = rank w // r, slot w % r: ascending id
-            for b in range(nb):
-                ptrs = [rows[w].data_ptr() + 4 * self.offsets[b] for w in range(self.n)]
-                C.sesgd_global_average(self.ctx, b, self.n, ptrs, s.cuda_stream)
-        self._gathered = gathered  # alive until the next call (the kernels read it on s)
+        self.average_engine().step(0, 0.0, 0.0, s)
 
     def _gathered_rows(self, stream):
         """every rank's parameters, all-gathered (data movement only): [n, total] on this GPU"""
@@ -244,6 +251,9 @@ class SESGDEngine:
         C.sesgd_measure_hop(self.ctx, peer_rank, iters, init, s.cuda_stream)
 
     def close(self) -> None:
+        if getattr(self, "_avg", None) is not None:
+            self._avg.close()
+            self._avg = None
         if self.ctx is not None:
             C.sesgd_destroy(self.ctx)
             self.ctx = None
@@ -297,13 +307,25 @@ class LoopbackGroup:
         return torch.cat([torch.stack(e.x_flat) for e in self.engines])
 
     def global_average(self) -> None:
-        """Algorithm 1's last line on every virtual rank: K8 over the gathered rows"""
-        rows = self._gather()
-        for e in self.engines:
-            for b in range(len(e.bucket_sizes)):
-                ptrs = [rows[w].data_ptr() + 4 * e.offsets[b] for w in range(e.n)]
-                C.sesgd_global_average(e.ctx, b, e.n, ptrs, e.stream.cuda_stream)
+        """Algorithm 1's last line on every virtual rank: one exchange with group_size = n
+        through the two-shot kernel on zero-momentum contexts (as SESGDEngine.global_average)"""
         self.synchronize()
+        if getattr(self, "_avg", None) is None:
+            e0 = self.engines[0]
+            self._avg = [SESGDEngine(e.n, e.n, e.bucket_sizes, seed=e.seed, device=e.device.index, rank=e.rank,
+                                     world=e.world, path=C.PATH_TWOSHOT, loopback=True, share_x_with=e,
+                                     timeout_ms=10000)
+                         for e in self.engines]
+            ptrs = [a.workspace.data_ptr() for a in self._avg]
+            torch.cuda.synchronize(e0.device)
+            for a in self._avg:
+                C.sesgd_attach_peers(a.ctx, self.world, a.rank, ptrs, a.worker_rank)
+        for a in self._avg:
+            a.step(0, 0.0, 0.0)
+        for a in self._avg:
+            a.stream.synchronize()
+        for a in self._avg:
+            a.poll()
 
     def consensus(self):
         """K9 over the gathered rows, on virtual rank 0"""
@@ -321,5 +343,8 @@ class LoopbackGroup:
             e.poll()
 
     def close(self) -> None:
+        for a in getattr(self, "_avg", None) or []:
+            a.close()
+        self._avg = None
         for e in self.engines:
             e.close()

@@ -22,7 +22,7 @@ def _options(a):
     return {k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
                               (C.OPT_PUSH_TMA, a.tma), (C.OPT_LOCAL_PERIOD, a.period),
                               (C.OPT_SCHEDULE, a.schedule), (C.OPT_PAYLOAD_BF16, a.bf16),
-                              (C.OPT_PROTOCOL, a.protocol), (C.OPT_RELEASE_EVERY, a.release_every)) if v}
+                              (C.OPT_RELEASE_EVERY, a.release_every)) if v} | {C.OPT_PROTOCOL: a.protocol}
 
 
 def _padded(idx, buckets, offsets):
@@ -96,7 +96,7 @@ def main():
     p.add_argument("--consensus", type=int, default=0)
     p.add_argument("--wd", type=float, default=0.0)
     p.add_argument("--bf16", type=int, default=0)
-    p.add_argument("--protocol", type=int, default=0)
+    p.add_argument("--protocol", type=int, default=-1)  # SESGD_OPT_PROTOCOL, -1 = auto
     p.add_argument("--release-every", type=int, default=0)
     p.add_argument("--loopback", type=int, default=0)
     p.add_argument("--coords", default="")

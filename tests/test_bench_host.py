@@ -94,7 +94,7 @@ def test_reference_arm_json_workload_equals_gpu_arm_config():
     assert res.returncode == 0, res.stderr[-2000:]
     d = json.loads(res.stdout.strip().splitlines()[-1])
     want = bench.common_config("resnet50", 8, 2, "param")
-    assert {k: d["config"][k] for k in want} == want
+    assert d["config"] == {**want, "parallelism": "sesgd groups over 1 GPU(s)"}
     src = inspect.getsource(bench.measure) + inspect.getsource(bench.run_sesgd)
     assert "**common_config(workload, n, m, args.mode)" in src
     assert "workload_desc(" not in src  # nothing appended to the shared string

@@ -43,7 +43,7 @@ def _free_port():
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
             lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
-            bf16=0, coords=None, protocol=0, release_every=0):
+            bf16=0, coords=None, protocol=-1, release_every=0):
     """`gpus` ranks: processes on as many GPUs (nvlink) or virtual ranks on cuda:0 (loopback)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -264,10 +264,11 @@ def test_two_gpus_ring_path_injected_latency(tmp_path):
 @pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_two_gpus_twoshot(tmp_path, mode, fused):
-    """K4 (reduce-scatter + all-gather pushes, two handshake rounds) on 2 GPUs, n = m = 2:
-    the slice owner folds in ascending worker id and divides once, so the bits are the oracle's."""
+    """K4 with the epoch-flag protocol (SESGD_OPT_PROTOCOL 0: reduce-scatter + all-gather pushes,
+    two handshake rounds, fence + flags) on 2 GPUs, n = m = 2: the slice owner folds in ascending
+    worker id and divides once, so the bits are the oracle's."""
     buckets = [100003, 7, 40000, 4096]
-    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused, path=4)
+    X, V = _launch(tmp_path, 2, 2, 2, 6, buckets, mode, fused=fused, path=4, protocol=0)
     x, v = _oracle(2, 2, sum(buckets), 6, mode)
     _compare(X, x)
     _compare(V, v)
@@ -276,9 +277,9 @@ def test_two_gpus_twoshot(tmp_path, mode, fused):
 @pytest.mark.parametrize("lag,grid", [(1, 8), (2, 24), (3, 0), (8, 16), (64, 4)])
 def test_two_gpus_twoshot_pipeline_shapes(tmp_path, lag, grid):
     """Small grids (many chunks per CTA) x fold lags (1 .. 32 per round): every pipeline depth,
-    including ones longer than a CTA's chunk list, gives the oracle's bits."""
+    including ones longer than a CTA's chunk list, gives the oracle's bits (flag protocol)."""
     buckets = [250001, 13, 70000]
-    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, grid=grid, lag=lag, path=4)
+    X, V = _launch(tmp_path, 2, 2, 2, 5, buckets, grid=grid, lag=lag, path=4, protocol=0)
     x, v = _oracle(2, 2, sum(buckets), 5, 0)
     _compare(X, x)
     _compare(V, v)
@@ -295,10 +296,10 @@ def test_two_gpus_twoshot_resume(tmp_path):
 @pytest.mark.parametrize("m", [2, 4])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_four_gpus_twoshot(tmp_path, m, mode):
-    """K4 on 4 GPUs: m = 2 (groups change every iteration) and m = 4 (4 slice owners,
-    ragged last slice and bucket tails)."""
+    """K4 (flag protocol) on 4 GPUs: m = 2 (groups change every iteration) and m = 4 (4 slice
+    owners, ragged last slice and bucket tails)."""
     buckets = [200003, 5000, 1]
-    X, V = _launch(tmp_path, 4, 4, m, 6, buckets, mode, path=4)
+    X, V = _launch(tmp_path, 4, 4, m, 6, buckets, mode, path=4, protocol=0)
     x, v = _oracle(4, m, sum(buckets), 6, mode)
     _compare(X, x)
     _compare(V, v)
@@ -330,7 +331,8 @@ def test_four_gpus_twoshot_tma(tmp_path, m):
 @pytest.mark.parametrize("n,m,period", [(4, 2, 2), (2, 2, 3), (4, 4, 2)])
 def test_two_gpus_local_sesgd_final_average(tmp_path, n, m, period, path):
     """Local-SESGD (exchange only when (t + 1) % period == 0; m = n is Local-SGD) over NVLink,
-    then Algorithm 1's final global average (all-gather + K8): the oracle's bits."""
+    then Algorithm 1's final global average (one two-shot exchange with group_size = n on a
+    zero-momentum context, lr = 0): the oracle's bits (its ascending fold over all n workers)."""
     buckets = [65537, 3, 20000]
     T = 5
     X, V = _launch(tmp_path, 2, n, m, T, buckets, path=path, period=period, final_avg=1)
