@@ -9,6 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsesgd.so")
+LIB_CHECKED = os.path.join(PKG, "libsesgd_checked.so")  # -DSESGD_CHECKED: device bounds checks
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -26,23 +27,25 @@ def deps():
         + [os.path.join(ROOT, "include", "sesgd.h")]
 
 
-def up_to_date() -> bool:
-    return os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps())
+def up_to_date(lib: str = LIB) -> bool:
+    return os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(d) for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *sources()]
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    if not force and up_to_date(lib):
+        return lib
+    extra = ["-DSESGD_CHECKED"] if checked else []
+    cmd = ["nvcc", *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", lib, *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(PKG, "build.log")
+    log = os.path.join(PKG, "build_checked.log" if checked else "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed (see {log}):\n{res.stderr[-4000:]}")
     if verbose:
         print(res.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

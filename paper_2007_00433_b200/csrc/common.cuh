@@ -3,6 +3,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Bounds / protocol checks of the checked build (_build.build(checked=True) compiles with
+// -DSESGD_CHECKED: libsesgd_checked.so, selected with SESGD_LIB=checked).  compute-sanitizer is
+// refused on this GPU pool, so the parity suite runs against this build instead: a failed check
+// traps the kernel (the launch fails with an error the tests see).
+#ifdef SESGD_CHECKED
+#define SESGD_CHECK(cond)                                                                        \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("SESGD_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,  \
+             int(blockIdx.x), int(threadIdx.x));                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define SESGD_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace sesgd {
 namespace dev {
 

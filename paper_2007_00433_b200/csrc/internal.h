@@ -85,6 +85,8 @@ struct P2PArgs {
   int64_t ready_off, sent_off, staged_off, consumed_off, stage_off, recv_off;  // byte offsets
   uint64_t seq_epoch0;              // S(seq, g) = seq_epoch0 + g / Gc for this launch
   uint64_t prev2_epoch0;            // the same for the launch that made call - 2 (guard)
+  int64_t seq, prev2_seq;           // launch sequence numbers of this launch / of call - 2's (K4W)
+  uint64_t claim_base;              // K4W: value of the chunk-claim counter when this launch starts
   int64_t call;                     // call index of the bucket(s) (identical on every rank)
   uint64_t timeout_ns;
   uint64_t hop_delay_ns;
@@ -265,6 +267,7 @@ struct sesgd_ctx {
   cudaEvent_t ev_l0 = nullptr, ev_l1 = nullptr;  // around the most recent sync launch
   bool ev_l_valid = false;
   uint64_t hop_base[SESGD_MAX_RANKS] = {};
+  uint64_t claim_base = 0;        // K4W dynamic chunk claims so far (chunks + one failed claim per CTA)
   int hop_iters = 0;
   int profile = 0;
   std::string last_error;

@@ -351,6 +351,7 @@ struct Split {
       }
       b = lo;
     }
+    SESGD_CHECK(b >= 0 && b < a.nbuckets && g >= a.g0 && g < a.g1);
     const BucketMeta &mb = a.meta[b];
     ChunkRef c;
     c.b = b;
@@ -366,9 +367,12 @@ struct Split {
   }
   __device__ __forceinline__ bool remote(int w) const { return a.worker_rank[w] != a.my_rank; }
   __device__ __forceinline__ float *stage(int slot) const {  // my rank's stage of a local slot
+    SESGD_CHECK(slot >= 0 && slot < a.r);
     return reinterpret_cast<float *>(a.ws[a.my_rank] + a.stage_off) + int64_t(slot) * a.region_floats;
   }
   __device__ __forceinline__ float *recv(int worker, int pos) const {  // worker's receive slot
+    SESGD_CHECK(worker >= 0 && worker < a.n && pos >= 0 && pos < a.m);
+    SESGD_CHECK(a.worker_slot[worker] >= 0 && a.worker_slot[worker] < a.r);
     char *base = a.ws[(a.experiment & 2) ? a.my_rank : a.worker_rank[worker]] + a.recv_off;
     const int64_t region = (int64_t(a.parity) * a.r + a.worker_slot[worker]) * a.m + pos;
     return reinterpret_cast<float *>(base) + region * a.region_floats;

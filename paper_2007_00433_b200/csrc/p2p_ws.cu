@@ -2,9 +2,10 @@
 // ascending fold, so the same bits) as a WARP-SPECIALISED persistent kernel with value-carried
 // validity (SESGD_OPT_PROTOCOL = 2), one worker per GPU -- the north star's 8-GPU layout and the
 // n = m = 2 two-GPU shape.  One CTA per SM; its warps are five roles joined only by data:
-//   P (1 warp)    TMA producer: cp.async.bulk of the chunk's g, v, x (16 KiB each) into a
-//                 3-stage shared-memory ring (mbarrier complete_tx), so every SM keeps two to
-//                 three chunks of HBM reads in flight regardless of what the other warps do;
+//   P (1 warp)    claims chunks dynamically (one global atomic per chunk: a fast SM takes more
+//                 chunks, so no CTA waits for a slow one at the end) and loads the chunk's g, v, x
+//                 (16 KiB each) with cp.async.bulk into a 3-stage shared-memory ring (mbarrier
+//                 complete_tx): every SM keeps two to three chunks of HBM reads in flight;
 //   S (8 warps)   the local step from shared memory (Alg.1 lines 3-8: v <- mu v + g,
 //                 x_hat <- x - lr v), v back to HBM, its own slice of x_hat into a second ring
 //                 for R, the other members' slices pushed to their receive slots over NVLink
@@ -19,9 +20,10 @@
 // R / F group kept only one chunk in flight; the TMA ring and the interleaved groups remove both.
 // No flags and no fence on the data path: every receive float is armed with a sentinel NaN and
 // polled until the peer's value replaces it (p2p.cu, "value-carried validity"), then re-armed.
-// The only system-scope synchronisation is K4's per-launch `consumed` counter (a peer must have
-// re-armed its slots of call - 2 before they are written again): one acquire at the start and
-// one release at the end of every CTA.  GRAD mode (Eq. 5): the payload is g, R / F apply the
+// The only system-scope synchronisation is one per-launch counter per rank, bumped (release) by
+// every CTA when it is done: a peer must have finished -- re-armed every receive slot of -- its
+// launch of call - 2 before this launch writes those slots again (one acquire per peer at start).
+// Chunk ids travel from P to S and F through a shared-memory id ring; an id < 0 ends a role.  GRAD mode (Eq. 5): the payload is g, R / F apply the
 // momentum update with the group-mean gradient (they load v, x themselves).
 #include "common.cuh"
 #include "internal.h"
@@ -37,9 +39,12 @@ constexpr int kChunkWS = 4096;  // K4's chunking (p2p_chunk_elems): same slices
 constexpr int kQL = 3;          // load ring stages (g, v, x of one chunk each)
 constexpr int kQX = 4;          // x_hat ring entries (a multiple of kGroupsR)
 constexpr int kU = 2;           // vectors in flight per R / F thread
+constexpr int kQI = 8;          // chunk-id ring entries (P -> S, F; a multiple of kGroupsF)
+constexpr int64_t kClaimOff = 64, kDoneOff = 72;  // workspace header words: claim / done counters
 constexpr uint32_t kSentinelWS = 0xFFFFFFFFu;  // as p2p.cu's kSentinel
 constexpr int kWaitDataWS = 6;
 static_assert(kQX % kGroupsR == 0, "an x_hat ring entry is always consumed by the same R group");
+static_assert(kQI % kGroupsF == 0 && kQI > kQL, "id ring: same F group per entry, deeper than the load ring");
 
 __device__ __forceinline__ float unsent(float v) {
   return __float_as_uint(v) == kSentinelWS ? __uint_as_float(0x7FFFFFFFu) : v;
@@ -133,9 +138,11 @@ __device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
 
 // shared memory: barriers, then the load ring (g, v, x per stage) and the x_hat ring
 struct Smem {
-  uint64_t full_ld[kQL], empty_ld[kQL], full_x[kQX], empty_x[kQX];
+  uint64_t full_ld[kQL], empty_ld[kQL], full_x[kQX], empty_x[kQX], full_id[kQI], empty_id[kQI];
+  int64_t id[kQI];   // chunk of step k at [k % kQI] (written by P)
+  int64_t xid[kQX];  // chunk of the x_hat ring entry (written by S)
 };
-constexpr size_t kSmemHead = 256;  // >= sizeof(Smem), keeps the rings 128-byte aligned
+constexpr size_t kSmemHead = 512;  // >= sizeof(Smem), keeps the rings 128-byte aligned
 constexpr size_t kStageBytes = size_t(3) * kChunkWS * 4;
 
 template <int W, bool GRAD>
@@ -148,7 +155,7 @@ struct WS {
   int cap;
   int me, p, m;
   const int8_t *G;
-  int64_t first, nk;
+  int64_t nk;  // chunks of this launch (claimed dynamically)
   int gc;
 
   __device__ WS(const P2PArgs &args, unsigned char *smem) : a(args) {
@@ -157,9 +164,7 @@ struct WS {
     m = a.m;
     G = a.canon + a.group_of[me] * a.m;
     gc = a.grid;
-    const int i = blockIdx.x;
-    first = a.g0 + ((int64_t(i) - a.g0 % gc) % gc + gc) % gc;
-    nk = (a.g1 > first) ? (a.g1 - first + gc - 1) / gc : 0;
+    nk = a.g1 - a.g0;
     sm = reinterpret_cast<Smem *>(smem);
     ld_ring = reinterpret_cast<float *>(smem + kSmemHead);
     x_ring = reinterpret_cast<float *>(smem + kSmemHead + kQL * kStageBytes);
@@ -180,6 +185,7 @@ struct WS {
       }
       b = lo;
     }
+    SESGD_CHECK(b >= 0 && b < a.nbuckets && g >= a.g0 && g < a.g1);
     const BucketMeta &mb = a.meta[b];
     Ref c;
     c.b = b;
@@ -196,11 +202,12 @@ struct WS {
   }
   // receive slot [pos] of worker w (one worker per rank: slot 0), parity of this call
   __device__ __forceinline__ float *recv(int w, int pos) const {
+    SESGD_CHECK(w >= 0 && w < a.n && pos >= 0 && pos < m && a.worker_rank[w] >= 0);
     char *base = a.ws[(a.experiment & 2) ? a.my_rank : a.worker_rank[w]] + a.recv_off;
     return reinterpret_cast<float *>(base) + (int64_t(a.parity) * m + pos) * a.region_floats;
   }
-  __device__ __forceinline__ uint64_t *consumed(int w) const {
-    return reinterpret_cast<uint64_t *>(a.ws[a.worker_rank[w]] + a.consumed_off) + blockIdx.x;
+  __device__ __forceinline__ unsigned long long *counter(int rank, int64_t off) const {
+    return reinterpret_cast<unsigned long long *>(a.ws[rank] + off);
   }
 
   // poll a payload vector until it is no longer the sentinel (then the caller re-arms it)
@@ -234,12 +241,32 @@ struct WS {
   }
 
   // ---------------------------------------------------------------- P: TMA loads
+  // publish chunk id g for step k to F (and, through the load ring, to S)
+  __device__ __forceinline__ void post_id(int64_t k, int64_t g) const {
+    const int qi = int(k % kQI);
+    if (k >= kQI) mbar_spin(&sm->empty_id[qi], uint32_t((k / kQI - 1) & 1));
+    sm->id[qi] = g;
+    mbar_arrive(&sm->full_id[qi]);
+  }
   __device__ void run_p() const {
-    if (!kTma || (threadIdx.x & 31) != 0) return;
-    for (int64_t k = 0; k < nk; ++k) {
+    if ((threadIdx.x & 31) != 0) return;
+    unsigned long long *claim = counter(a.my_rank, kClaimOff);
+    for (int64_t k = 0;; ++k) {
+      const uint64_t idx = atomicAdd(claim, 1ull) - a.claim_base;
+      const int64_t g = idx < uint64_t(nk) ? a.g0 + int64_t(idx) : -1;
       const int q = int(k % kQL);
       if (k >= kQL) mbar_spin(&sm->empty_ld[q], uint32_t((k / kQL - 1) & 1));
-      const Ref c = locate(first + k * gc);
+      post_id(k, g);
+      if (g < 0) {  // end: S sees it through the load ring, each F group through its own id entry
+        dev::mbar_arrive_expect_tx(&sm->full_ld[q], 0);
+        post_id(k + 1, -1);
+        return;
+      }
+      if (!kTma) {
+        mbar_arrive(&sm->full_ld[q]);
+        continue;
+      }
+      const Ref c = locate(g);
       const uint32_t bytes = uint32_t(c.len / 4) * 16;  // whole float4s; the tail is read by S
       float *st = ld_ring + size_t(q) * 3 * kChunkWS;
       dev::mbar_arrive_expect_tx(&sm->full_ld[q], (GRAD ? 1u : 3u) * bytes);
@@ -260,13 +287,25 @@ struct WS {
     const uint64_t ts = lead ? dev::globaltimer() : 0;
     uint64_t t_wait = 0;
     constexpr int kItems = kChunkWS / W / kThS;
-    for (int64_t k = 0; k < nk; ++k) {
-      const Ref c = locate(first + k * gc);
+    for (int64_t k = 0;; ++k) {
       const int q = int(k % kQL), qx = int(k % kQX);
       const uint64_t tw = lead ? dev::globaltimer() : 0;
-      if (kTma) mbar_spin(&sm->full_ld[q], uint32_t((k / kQL) & 1));
+      mbar_spin(&sm->full_ld[q], uint32_t((k / kQL) & 1));
+      const int64_t g = sm->id[k % kQI];
+      if (g < 0) {  // end: one marker per R group
+        for (int64_t kk = k; kk < k + kGroupsR; ++kk) {
+          const int qq = int(kk % kQX);
+          if (kk >= kQX) mbar_spin(&sm->empty_x[qq], uint32_t((kk / kQX - 1) & 1));
+          if ((t & 31) == 0) {
+            sm->xid[qq] = -1;
+            mbar_arrive(&sm->full_x[qq]);
+          }
+        }
+        break;
+      }
       if (k >= kQX) mbar_spin(&sm->empty_x[qx], uint32_t((k / kQX - 1) & 1));
       if (lead) t_wait += dev::globaltimer() - tw;
+      const Ref c = locate(g);
       const float *sg = ld_ring + size_t(q) * 3 * kChunkWS;
       float *ent = x_ring + size_t(qx) * cap;
       const int64_t mlo = lo(p, c.len);
@@ -306,7 +345,9 @@ struct WS {
           stm<W>(vs + e, v, nv);
         }
         const int j = min(int(o / S), m - 1);  // owner position (a vector never straddles)
+        SESGD_CHECK(o + nv <= hi(j, c.len) && o >= lo(j, c.len));
         if (j == p) {
+          SESGD_CHECK(o - mlo >= 0 && o - mlo + nv <= cap);
           if (W == 4 && nv == 4) {
             *reinterpret_cast<float4 *>(ent + (o - mlo)) =
                 make_float4(val[0], val[W > 1 ? 1 : 0], val[W > 2 ? 2 : 0], val[W > 3 ? 3 : 0]);
@@ -321,8 +362,9 @@ struct WS {
       }
       __syncwarp();
       if ((t & 31) == 0) {
-        if (kTma) mbar_arrive(&sm->empty_ld[q]);  // the load stage is free for the producer
-        mbar_arrive(&sm->full_x[qx]);             // my slice's x_hat is ready for R
+        mbar_arrive(&sm->empty_ld[q]);  // the load stage is free for the producer
+        sm->xid[qx] = g;
+        mbar_arrive(&sm->full_x[qx]);   // my slice's x_hat is ready for R
       }
     }
     if (lead) {
@@ -338,12 +380,14 @@ struct WS {
     const uint64_t ts = lead ? dev::globaltimer() : 0;
     uint64_t t_wait = 0, t_spin = 0;
     uint64_t *spin = lead ? &t_spin : nullptr;
-    for (int64_t k = grp; k < nk; k += kGroupsR) {
-      const Ref c = locate(first + k * gc);
+    for (int64_t k = grp;; k += kGroupsR) {
       const int qx = int(k % kQX);
       const uint64_t tw = lead ? dev::globaltimer() : 0;
       mbar_spin(&sm->full_x[qx], uint32_t((k / kQX) & 1));
       if (lead) t_wait += dev::globaltimer() - tw;
+      const int64_t g = sm->xid[qx];
+      if (g < 0) break;
+      const Ref c = locate(g);
       if (k == grp && a.hop_delay_ns) {  // config 4: the all-gather round's injected hop
         const uint64_t t0 = dev::globaltimer();
         while (dev::globaltimer() - t0 < a.hop_delay_ns) {
@@ -351,6 +395,7 @@ struct WS {
       }
       const float *ent = x_ring + size_t(qx) * cap;
       const int64_t mlo = lo(p, c.len), mhi = hi(p, c.len);
+      SESGD_CHECK(mhi - mlo <= cap && c.soff + c.e0 + mhi <= a.region_floats);
       float *xs = a.bx[c.b], *vs = a.bv[c.b];
       for (int64_t base = mlo; base < mhi; base += int64_t(kThR) * W * kU) {
         float acc[kU][W];
@@ -429,8 +474,14 @@ struct WS {
     const uint64_t ts = lead ? dev::globaltimer() : 0;
     uint64_t t_spin = 0;
     uint64_t *spin = lead ? &t_spin : nullptr;
-    for (int64_t k = grp; k < nk; k += kGroupsF) {
-      const Ref c = locate(first + k * gc);
+    for (int64_t k = grp;; k += kGroupsF) {
+      const int qi = int(k % kQI);
+      mbar_spin(&sm->full_id[qi], uint32_t((k / kQI) & 1));
+      const int64_t g = sm->id[qi];
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&sm->empty_id[qi]);  // the id is read: P may reuse the entry
+      if (g < 0) break;
+      const Ref c = locate(g);
       float *xs = a.bx[c.b], *vs = a.bv[c.b];
       for (int j = 0; j < m; ++j) {
         if (j == p) continue;
@@ -512,7 +563,6 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
     s.local_only();
     return;
   }
-  if (s.nk == 0) return;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kQL; ++q) {
       dev::mbar_init(&s.sm->full_ld[q], 1);
@@ -522,15 +572,19 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
       dev::mbar_init(&s.sm->full_x[q], kWarpsS);
       dev::mbar_init(&s.sm->empty_x[q], kWarpsR);
     }
+    for (int q = 0; q < kQI; ++q) {
+      dev::mbar_init(&s.sm->full_id[q], 1);
+      dev::mbar_init(&s.sm->empty_id[q], kWarpsF);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // guard: every peer re-armed its receive slots of call - 2 for my chunks (its CTA i polls
-  // exactly my CTA i's chunks); one acquire per peer and launch
-  if (a.call >= 2 && threadIdx.x < 32) {
-    const uint64_t need = a.prev2_epoch0 + uint64_t((s.first + (s.nk - 1) * s.gc) / s.gc);
+  // guard: every peer has finished (and so re-armed every receive slot of) its launch of call - 2:
+  // each CTA of each launch bumps the rank's done counter once, launches run in stream order
+  if (a.prev2_seq >= 0 && threadIdx.x < 32) {
+    const uint64_t need = uint64_t(a.grid) * uint64_t(a.prev2_seq + 1);
     for (int j = threadIdx.x; j < a.m; j += 32) {
       if (j == s.p) continue;
-      const uint64_t *f = s.consumed(s.G[j]);
+      const uint64_t *f = reinterpret_cast<const uint64_t *>(s.counter(a.worker_rank[s.G[j]], kDoneOff));
       if (dev::ld_acquire_sys(f) >= need) continue;
       count(a.counters, kCntFlagSpins);
       const uint64_t t0 = dev::globaltimer();
@@ -539,7 +593,7 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
         if (dev::globaltimer() - t0 > a.timeout_ns) {
           if (atomicExch(a.abort_dev, 1u) == 0u) {
             unsigned long long *e = a.err_host;
-            e[1] = 1;  // consumed
+            e[1] = 1;  // consumed (the peer's launch of call - 2 is not done)
             e[2] = blockIdx.x;
             e[3] = dev::ld_acquire_sys(f);
             e[4] = need;
@@ -578,8 +632,10 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
     s.run_f(w / kWarpsF, (w % kWarpsF) * 32 + (threadIdx.x & 31));
   }
   __syncthreads();  // every re-arm of this CTA precedes the release (cumulativity)
-  if (threadIdx.x == 0)
-    dev::st_release_sys(s.consumed(s.me), a.seq_epoch0 + uint64_t((s.first + (s.nk - 1) * s.gc) / s.gc));
+  if (threadIdx.x == 0) {
+    dev::fence_acq_rel_sys();
+    atomicAdd(s.counter(a.my_rank, kDoneOff), 1ull);
+  }
 }
 
 const void *pick_ws(int mode, bool vec) {

@@ -386,6 +386,9 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.call = call;
   a.seq_epoch0 = uint64_t(ctx->seq) * uint64_t(ctx->kmax) + 1;
   a.prev2_epoch0 = call >= 2 ? uint64_t(ref.seq_hist[call & 1]) * uint64_t(ctx->kmax) + 1 : 0;
+  a.seq = ctx->seq;
+  a.prev2_seq = call >= 2 ? ref.seq_hist[call & 1] : -1;
+  a.claim_base = ctx->claim_base;
   a.timeout_ns = uint64_t(ctx->timeout_ms) * 1000000ULL;
   a.hop_delay_ns = uint64_t(ctx->hop_delay_ns);
   a.err_host = ctx->d_err;
@@ -448,6 +451,8 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
                                                         ctx->guard_smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
   mark_end(ctx, st);
+  if (twoshot && ctx->protocol == 2 && !nvls)  // every claimed chunk plus one failed claim per CTA
+    ctx->claim_base += uint64_t(a.g1 - a.g0) + uint64_t(ctx->grid);
   // bookkeeping
   int remote_peers = 0;
   for (int s = 0; s < ctx->n_local; ++s) {

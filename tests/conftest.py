@@ -26,7 +26,7 @@ def _build_all():
     from paper_2007_00433_b200 import _build
     oracle.build()
     synth.build()
-    _build.build()
+    _build.build(checked=os.environ.get("SESGD_LIB") == "checked")
 
 
 _build_all()
