@@ -347,6 +347,15 @@ SESGD_API int sesgd_poll(sesgd_ctx *ctx);
 /* Counters of bucket `bucket`.  Errors: SESGD_EINVAL. */
 SESGD_API int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats *out);
 
+/* Measurement harness, not part of an iteration's normal API: sesgd_sync_all for BOTH ranks of a
+ * two-rank loopback layout (contexts c0 = rank 0 and c1 = rank 1 on the same GPU, attached to
+ * each other, protocol 2 = K4W, one worker each) as ONE kernel launch whose first half of CTAs
+ * runs rank 0 and second half rank 1 -- same kernel body, same bits as two sesgd_sync_all calls
+ * -- so a profiler that serialises launches (ncu, which would deadlock two concurrent grids that
+ * wait on each other) can capture the whole exchange.  Both contexts' call histories advance.
+ * Errors: SESGD_EINVAL, SESGD_ESTATE, SESGD_ENOTSUP (not that layout), SESGD_ECUDA. */
+SESGD_API int sesgd_sync_all_pair(sesgd_ctx *c0, sesgd_ctx *c1, float lr, float momentum, void *stream);
+
 /* Per-hop handshake latency t_tau (Eq. 2) between this rank and `peer_rank` through the
  * two ranks' workspaces (K7 flag ping-pong, one thread, system-scope release / acquire): both ranks
  * call it concurrently with the same `iters`, exactly one with initiator = 1.  Enqueued on

@@ -172,6 +172,7 @@ cudaError_t launch_p2p_twoshot(const P2PArgs &a, int mode, bool vec, bool tma, c
 int p2p_twoshot_occupancy(int mode, bool vec, bool tma, bool multi);
 // K4W (SESGD_OPT_PROTOCOL = 2): warp-specialised two-shot, one worker per GPU, one CTA per SM
 cudaError_t launch_p2p_ws(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
+cudaError_t launch_p2p_ws_pair(const P2PArgs &a0, const P2PArgs &a1, int mode, bool vec, cudaStream_t stream);
 int p2p_ws_occupancy(int m);
 int p2p_ws_threads();
 

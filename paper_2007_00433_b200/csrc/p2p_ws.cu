@@ -157,6 +157,7 @@ struct WS {
   const int8_t *G;
   int64_t nk;  // chunks of this launch (claimed dynamically)
   int gc;
+  int cta;     // CTA index within this rank's grid (the pair harness runs two ranks in one grid)
 
   __device__ WS(const P2PArgs &args, unsigned char *smem) : a(args) {
     me = a.my_workers[0];
@@ -164,6 +165,7 @@ struct WS {
     m = a.m;
     G = a.canon + a.group_of[me] * a.m;
     gc = a.grid;
+    cta = int(blockIdx.x) % a.grid;
     nk = a.g1 - a.g0;
     sm = reinterpret_cast<Smem *>(smem);
     ld_ring = reinterpret_cast<float *>(smem + kSmemHead);
@@ -224,7 +226,7 @@ struct WS {
         if (atomicExch(a.abort_dev, 1u) == 0u) {
           unsigned long long *e = a.err_host;
           e[1] = (unsigned long long)kWaitDataWS;
-          e[2] = blockIdx.x;
+          e[2] = cta;
           e[3] = 0;
           e[4] = uint64_t(a.call) + 1;
           e[5] = (unsigned long long)me;
@@ -368,7 +370,7 @@ struct WS {
       }
     }
     if (lead) {
-      uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
+      uint64_t *pr = a.prof + int64_t(cta) * 8;
       pr[0] += dev::globaltimer() - ts;
       pr[4] += t_wait;
     }
@@ -461,7 +463,7 @@ struct WS {
       if ((t & 31) == 0) mbar_arrive(&sm->empty_x[qx]);
     }
     if (lead) {
-      uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
+      uint64_t *pr = a.prof + int64_t(cta) * 8;
       pr[1] += dev::globaltimer() - ts;
       pr[5] += t_wait;
       pr[6] += t_spin;
@@ -522,7 +524,7 @@ struct WS {
       }
     }
     if (lead) {
-      uint64_t *pr = a.prof + int64_t(blockIdx.x) * 8;
+      uint64_t *pr = a.prof + int64_t(cta) * 8;
       pr[3] += dev::globaltimer() - ts;
       pr[2] += t_spin;
       pr[7] += 1;
@@ -531,7 +533,7 @@ struct WS {
 
   // m == 1: no exchange, the local step is the whole update
   __device__ void local_only() const {
-    for (int64_t g = a.g0 + blockIdx.x; g < a.g1; g += a.grid) {
+    for (int64_t g = a.g0 + cta; g < a.g1; g += a.grid) {
       const Ref c = locate(g);
       float *xs = a.bx[c.b], *vs = a.bv[c.b];
       const float *gs = a.bg[c.b];
@@ -555,10 +557,9 @@ struct WS {
 };
 
 template <int W, bool GRAD>
-__global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_constant__ P2PArgs a) {
-  extern __shared__ __align__(128) unsigned char dsmem[];
+__device__ __forceinline__ void k4w_body(const P2PArgs &a, unsigned char *dsmem) {
   const WS<W, GRAD> s(a, dsmem);
-  if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
+  if (s.cta == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1) {
     s.local_only();
     return;
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
           if (atomicExch(a.abort_dev, 1u) == 0u) {
             unsigned long long *e = a.err_host;
             e[1] = 1;  // consumed (the peer's launch of call - 2 is not done)
-            e[2] = blockIdx.x;
+            e[2] = s.cta;
             e[3] = dev::ld_acquire_sys(f);
             e[4] = need;
             e[5] = (unsigned long long)s.G[j];
@@ -638,6 +639,25 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
   }
 }
 
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_constant__ P2PArgs a) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  k4w_body<W, GRAD>(a, dsmem);
+}
+
+// measurement harness (sesgd_sync_all_pair): two loopback virtual ranks of one GPU in ONE grid --
+// CTAs [0, a0.grid) are rank a0's, the rest rank a1's -- so a profiler that serialises kernel
+// launches (ncu) sees the whole exchange in one kernel.  Same body, same bits.
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWS, 1) k4w_pair(const __grid_constant__ P2PArgs a0,
+                                                          const __grid_constant__ P2PArgs a1) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  if (int(blockIdx.x) < a0.grid)
+    k4w_body<W, GRAD>(a0, dsmem);
+  else
+    k4w_body<W, GRAD>(a1, dsmem);
+}
+
 const void *pick_ws(int mode, bool vec) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
   if (vec)
@@ -670,6 +690,18 @@ int p2p_ws_occupancy(int m) {
       occ = b < occ ? b : occ;
     }
   return occ > 0 ? occ : 1;
+}
+
+cudaError_t launch_p2p_ws_pair(const P2PArgs &a0, const P2PArgs &a1, int mode, bool vec, cudaStream_t stream) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  const void *k = vec ? (grad ? reinterpret_cast<const void *>(&k4w_pair<4, true>)
+                              : reinterpret_cast<const void *>(&k4w_pair<4, false>))
+                      : (grad ? reinterpret_cast<const void *>(&k4w_pair<1, true>)
+                              : reinterpret_cast<const void *>(&k4w_pair<1, false>));
+  const size_t smem = ws_smem(a0.m);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  void *args[] = {const_cast<P2PArgs *>(&a0), const_cast<P2PArgs *>(&a1)};
+  return launch_persistent(k, unsigned(a0.grid + a1.grid), kThreadsWS, args, smem, stream, false);
 }
 
 cudaError_t launch_p2p_ws(const P2PArgs &a, int mode, bool vec, cudaStream_t stream) {

@@ -356,8 +356,10 @@ int upload_tables(sesgd_ctx *ctx) {
 
 // One one-shot launch over bucket `bucket` (>= 0) or over every bucket (-1, all buckets
 // share the same call history).  Host bookkeeping of calls / launch sequence follows.
+// dry != nullptr: build the arguments into *dry and do the bookkeeping without launching (the
+// two-rank pair harness launches both ranks' arguments as one grid)
 int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st,
-                   bool twoshot = false, bool nvls = false) {
+                   bool twoshot = false, bool nvls = false, P2PArgs *dry = nullptr) {
   const sesgd_bucket &ref = ctx->buckets[bucket >= 0 ? bucket : 0];
   P2PArgs a{};
   a.meta = ctx->d_meta;
@@ -443,14 +445,18 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   bool vec = true;
   for (size_t b = 0; b < ctx->buckets.size(); ++b)
     if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
-  mark_start(ctx, st);
-  cudaError_t e = (twoshot && ctx->protocol == 2 && !nvls)
-                      ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
-                  : twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
-                            : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
-                                                        ctx->guard_smem, st);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
-  mark_end(ctx, st);
+  if (dry) {
+    *dry = a;
+  } else {
+    mark_start(ctx, st);
+    cudaError_t e = (twoshot && ctx->protocol == 2 && !nvls)
+                        ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
+                    : twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
+                              : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
+                                                          ctx->guard_smem, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
+    mark_end(ctx, st);
+  }
   if (twoshot && ctx->protocol == 2 && !nvls)  // every claimed chunk plus one failed claim per CTA
     ctx->claim_base += uint64_t(a.g1 - a.g0) + uint64_t(ctx->grid);
   // bookkeeping
@@ -470,7 +476,8 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
     bk.stats.hbm_algo_bytes += 20 * bk.numel * ctx->n_local;
     if (ctx->m > 1 && twoshot) {  // RS + AG flag per (chunk, peer); 2 (m-1)/m of the bucket in
       bk.stats.handshake_rounds = 2;
-      bk.stats.flag_messages += 2 * int64_t(remote_peers) * bk.nchunks;
+      if (ctx->protocol == 0 || nvls)  // the value-carried protocols store no flag
+        bk.stats.flag_messages += 2 * int64_t(remote_peers) * bk.nchunks;
       bk.stats.payload_bytes_in += 2 * int64_t(remote_peers) * bk.numel * 4 / ctx->m;
     } else if (ctx->m > 1) {
       bk.stats.handshake_rounds = 1;
@@ -1088,6 +1095,36 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     return fail(ctx, SESGD_ENOTSUP, "protocol 2 (warp-specialised K4W) needs one worker per GPU");
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
   return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot, nvls);
+}
+
+int sesgd_sync_all_pair(sesgd_ctx *c0, sesgd_ctx *c1, float lr, float momentum, void *stream) {
+  if (!c0 || !c1 || c0 == c1) return SESGD_EINVAL;
+  for (sesgd_ctx *c : {c0, c1}) {
+    int rc = check_latched(c);
+    if (rc != SESGD_OK) return rc;
+    if (!c->peers || !c->iter_set) return fail(c, SESGD_ESTATE, "attach peers and begin_iter first");
+    if (c->n_ranks != 2 || c->protocol != 2 || resolve_path(c) != SESGD_PATH_TWOSHOT || c->n_local != 1 ||
+        local_only_iteration(c))
+      return fail(c, SESGD_ENOTSUP, "the pair harness runs K4W (protocol 2) on a two-rank loopback layout");
+    for (auto &b : c->buckets)
+      if (b.calls != c->buckets[0].calls) return fail(c, SESGD_ESTATE, "buckets must share one call history");
+  }
+  if (c0->rank != 0 || c1->rank != 1 || c0->ws[0] != c1->ws[0] || c0->ws[1] != c1->ws[1] ||
+      c0->grid != c1->grid || c0->mode != c1->mode)
+    return fail(c0, SESGD_EINVAL, "c0, c1 must be ranks 0 and 1 of the same two-rank layout");
+  bool vec = true;
+  for (sesgd_ctx *c : {c0, c1})
+    for (auto &b : c->buckets) vec = vec && b.vec;
+  P2PArgs a0{}, a1{};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (auto &b : c0->buckets) b.stats.sync_calls++;
+  for (auto &b : c1->buckets) b.stats.sync_calls++;
+  int rc = launch_oneshot(c0, -1, lr, momentum, st, true, false, &a0);
+  if (rc == SESGD_OK) rc = launch_oneshot(c1, -1, lr, momentum, st, true, false, &a1);
+  if (rc != SESGD_OK) return rc;
+  const cudaError_t e = sesgd::launch_p2p_ws_pair(a0, a1, c0->mode, vec, st);
+  if (e != cudaSuccess) return cuda_fail(c0, e, "launch the K4W pair");
+  return SESGD_OK;
 }
 
 int sesgd_global_average(sesgd_ctx *ctx, int32_t bucket, const float *const *rows, int32_t nrows,

@@ -297,6 +297,18 @@ class LoopbackGroup:
         for e in self.engines:
             e.step(t, lr, momentum, fused=fused)
 
+    def step_pair(self, t: int, lr: float, momentum: float) -> None:
+        """measurement harness (two virtual ranks, K4W): both ranks' iteration as ONE kernel launch
+        (sesgd_sync_all_pair) on rank 0's stream, so ncu can capture the exchange"""
+        if self.world != 2:
+            raise ValueError("the pair harness needs exactly two virtual ranks")
+        e0, e1 = self.engines
+        e0.begin_iter(t)
+        e1.begin_iter(t)
+        e0.stream.wait_stream(e1.stream)
+        C.sesgd_sync_all_pair(e0.ctx, e1.ctx, lr, momentum, e0.stream.cuda_stream)
+        e1.stream.wait_stream(e0.stream)
+
     def synchronize(self) -> None:
         for e in self.engines:
             e.stream.synchronize()

@@ -35,7 +35,7 @@ EXPORTED = (
     "sesgd_poll", "sesgd_get_stats", "sesgd_launch_grid", "sesgd_strerror", "sesgd_last_error",
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
     "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus", "sesgd_set_weight_decay",
-    "sesgd_attach_multicast", "sesgd_pair_counts", "sesgd_measure_hop",
+    "sesgd_attach_multicast", "sesgd_pair_counts", "sesgd_measure_hop", "sesgd_sync_all_pair",
 )
 
 
@@ -94,6 +94,7 @@ def lib():
             "sesgd_poll": ([P], ctypes.c_int),
             "sesgd_get_stats": ([P, i32, ctypes.POINTER(sesgd_stats)], ctypes.c_int),
             "sesgd_measure_hop": ([P, i32, i32, i32, P], ctypes.c_int),
+            "sesgd_sync_all_pair": ([P, P, f32, f32, P], ctypes.c_int),
             "sesgd_launch_grid": ([P, ctypes.POINTER(i32)], ctypes.c_int),
             "sesgd_strerror": ([ctypes.c_int], ctypes.c_char_p),
             "sesgd_last_error": ([P], ctypes.c_char_p),
@@ -236,6 +237,10 @@ def sesgd_get_stats(ctx, bucket: int) -> dict:
     out = sesgd_stats()
     _check(lib().sesgd_get_stats(ctx, bucket, ctypes.byref(out)), ctx)
     return {f: getattr(out, f) for f, _ in sesgd_stats._fields_}
+
+
+def sesgd_sync_all_pair(c0, c1, lr: float, momentum: float, stream: int = 0) -> None:
+    _check(lib().sesgd_sync_all_pair(c0, c1, lr, momentum, ctypes.c_void_p(int(stream))), c0)
 
 
 def sesgd_measure_hop(ctx, peer_rank: int, iters: int, initiator: bool, stream: int = 0) -> None:
