@@ -392,10 +392,11 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        proto = args.protocol if args.protocol >= 0 else (2 if r == 1 else 1)  # auto (sesgd_capi.cu)
+        proto = args.protocol if args.protocol >= 0 else (2 if r <= 8 else 1)  # auto (sesgd_capi.cu)
         if args.push_tma or args.payload_bf16:
             proto = 0 if args.protocol < 0 else proto
-        kernel = {"twoshot": "k4w_twoshot" if (proto == 2 and r == 1) else "k4_twoshot",
+        k4w = "k4w_twoshot" if r == 1 else "k4w_multi"
+        kernel = {"twoshot": k4w if proto == 2 else "k4_twoshot",
                   "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
         # actual schedule of the timed iterations: a group spanning s GPUs costs every one
@@ -459,7 +460,8 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
         "launch": {"workers_per_gpu": r,
                    "path": "resident (K6)" if resident else {
                        "twoshot": "two-shot reduce-scatter/all-gather push over NVLink P2P ("
-                                  + ("K4W, warp-specialised" if kernel == "k4w_twoshot" else "K4") + ")",
+                                  + {"k4w_twoshot": "K4W, warp-specialised", "k4w_multi": "K4W-M, warp-specialised,"
+                                     " several workers per GPU"}.get(kernel, "K4") + ")",
                        "ring": "ring inside each group over NVLink P2P (K5)"}.get(
                            eff_path, "one-shot push over NVLink P2P (K3)"),
                    "l2": f"inputs larger than L2: {3 * 4 * L * r / 1e9:.2f} GB working set per GPU vs 126 MB L2; no flush"},

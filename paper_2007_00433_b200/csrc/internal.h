@@ -175,6 +175,11 @@ cudaError_t launch_p2p_ws(const P2PArgs &a, int mode, bool vec, cudaStream_t str
 cudaError_t launch_p2p_ws_pair(const P2PArgs &a0, const P2PArgs &a1, int mode, bool vec, cudaStream_t stream);
 int p2p_ws_occupancy(int m);
 int p2p_ws_threads();
+// K4W-M (SESGD_OPT_PROTOCOL = 2 with several workers per GPU), p2p_wsm.cu
+cudaError_t launch_p2p_wsm(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
+bool p2p_wsm_supported(int r, int m);
+int p2p_wsm_occupancy(int r);
+int64_t p2p_wsm_units(int r, int m, int64_t chunks);  // claimable units of `chunks` chunks
 
 }  // namespace sesgd
 

@@ -27,9 +27,11 @@
 // momentum update with the group-mean gradient (they load v, x themselves).
 #include "common.cuh"
 #include "internal.h"
+#include "ws_common.cuh"
 
 namespace sesgd {
 namespace {
+using namespace wsx;
 
 constexpr int kWarpsP = 1, kWarpsS = 8, kGroupsR = 2, kWarpsR = 4, kGroupsF = 2, kWarpsF = 4;
 constexpr int kThS = kWarpsS * 32, kThR = kWarpsR * 32, kThF = kWarpsF * 32;
@@ -40,101 +42,8 @@ constexpr int kQL = 3;          // load ring stages (g, v, x of one chunk each)
 constexpr int kQX = 4;          // x_hat ring entries (a multiple of kGroupsR)
 constexpr int kU = 2;           // vectors in flight per R / F thread
 constexpr int kQI = 8;          // chunk-id ring entries (P -> S, F; a multiple of kGroupsF)
-constexpr int64_t kClaimOff = 64, kDoneOff = 72;  // workspace header words: claim / done counters
-constexpr uint32_t kSentinelWS = 0xFFFFFFFFu;  // as p2p.cu's kSentinel
-constexpr int kWaitDataWS = 6;
 static_assert(kQX % kGroupsR == 0, "an x_hat ring entry is always consumed by the same R group");
 static_assert(kQI % kGroupsF == 0 && kQI > kQL, "id ring: same F group per entry, deeper than the load ring");
-
-__device__ __forceinline__ float unsent(float v) {
-  return __float_as_uint(v) == kSentinelWS ? __uint_as_float(0x7FFFFFFFu) : v;
-}
-template <int W>
-__device__ __forceinline__ void ldm(const float *p, float (&r)[W], int nv) {
-  if constexpr (W == 4) {
-    if (nv >= 4) {
-      const float4 t = dev::ld4(p);
-      r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
-      return;
-    }
-  }
-#pragma unroll
-  for (int w = 0; w < W; ++w) r[w] = (w < nv) ? __ldcs(p + w) : 0.f;
-}
-template <int W>
-__device__ __forceinline__ void stm(float *p, const float (&r)[W], int nv) {
-  if constexpr (W == 4) {
-    if (nv >= 4) {
-      dev::st4(p, make_float4(r[0], r[1], r[2], r[3]));
-      return;
-    }
-  }
-#pragma unroll
-  for (int w = 0; w < W; ++w)
-    if (w < nv) __stcs(p + w, r[w]);
-}
-// NVLink push of a payload vector: relaxed system-scope stores (the receiver polls the values)
-template <int W>
-__device__ __forceinline__ void push(float *p, const float (&r)[W], int nv) {
-  if constexpr (W == 4) {
-    if (nv >= 4) {
-      asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(unsent(r[0])),
-                   "f"(unsent(r[1])), "f"(unsent(r[2])), "f"(unsent(r[3]))
-                   : "memory");
-      return;
-    }
-  }
-#pragma unroll
-  for (int w = 0; w < W; ++w)
-    if (w < nv) asm volatile("st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p + w), "f"(unsent(r[w])) : "memory");
-}
-template <int W>
-__device__ __forceinline__ void ld_rel(const float *p, float (&r)[W], int nv) {
-  if constexpr (W == 4) {
-    if (nv >= 4) {
-      asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
-                   : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
-                   : "l"(p)
-                   : "memory");
-      return;
-    }
-  }
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-    if (w < nv)
-      asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(r[w]) : "l"(p + w) : "memory");
-    else
-      r[w] = 0.f;
-  }
-}
-template <int W>
-__device__ __forceinline__ bool pending(const float (&r)[W], int nv) {
-  bool any = false;
-#pragma unroll
-  for (int w = 0; w < W; ++w) any |= (w < nv) && __float_as_uint(r[w]) == kSentinelWS;
-  return any;
-}
-template <int W>
-__device__ __forceinline__ void rearm(float *p, int nv) {
-  const float s = __uint_as_float(kSentinelWS);
-  if constexpr (W == 4) {
-    if (nv >= 4) {
-      *reinterpret_cast<float4 *>(p) = make_float4(s, s, s, s);
-      return;
-    }
-  }
-#pragma unroll
-  for (int w = 0; w < W; ++w)
-    if (w < nv) p[w] = s;
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dev::smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
-  while (!dev::mbar_try_wait(bar, parity)) {
-  }
-}
 
 // shared memory: barriers, then the load ring (g, v, x per stage) and the x_hat ring
 struct Smem {
@@ -209,37 +118,11 @@ struct WS {
     return reinterpret_cast<float *>(base) + (int64_t(a.parity) * m + pos) * a.region_floats;
   }
   __device__ __forceinline__ unsigned long long *counter(int rank, int64_t off) const {
-    return reinterpret_cast<unsigned long long *>(a.ws[rank] + off);
+    return ws_counter(a, rank, off);
   }
-
-  // poll a payload vector until it is no longer the sentinel (then the caller re-arms it)
   __device__ __forceinline__ void wait_value(const float *src, float (&y)[W], int nv, int pos,
                                              uint64_t *spin) const {
-    if (!pending<W>(y, nv) || (a.experiment & 2)) return;  // (experiment: nobody writes my slots)
-    count(a.counters, kCntValueSpins);
-    const uint64_t t0 = dev::globaltimer();
-    for (;;) {
-      ld_rel<W>(src, y, nv);
-      if (!pending<W>(y, nv)) break;
-      if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;
-      if (dev::globaltimer() - t0 > a.timeout_ns) {
-        if (atomicExch(a.abort_dev, 1u) == 0u) {
-          unsigned long long *e = a.err_host;
-          e[1] = (unsigned long long)kWaitDataWS;
-          e[2] = cta;
-          e[3] = 0;
-          e[4] = uint64_t(a.call) + 1;
-          e[5] = (unsigned long long)me;
-          e[6] = (unsigned long long)pos;
-          e[7] = (unsigned long long)a.my_rank;
-          __threadfence_system();
-          atomicExch(e, (unsigned long long)(-SESGD_ETIMEOUT));
-          __threadfence_system();
-        }
-        break;
-      }
-    }
-    if (spin) *spin += dev::globaltimer() - t0;
+    wsx::wait_value<W>(a, cta, me, src, y, nv, pos, spin);
   }
 
   // ---------------------------------------------------------------- P: TMA loads
@@ -579,37 +462,10 @@ __device__ __forceinline__ void k4w_body(const P2PArgs &a, unsigned char *dsmem)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // guard: every peer has finished (and so re-armed every receive slot of) its launch of call - 2:
-  // each CTA of each launch bumps the rank's done counter once, launches run in stream order
-  if (a.prev2_seq >= 0 && threadIdx.x < 32) {
-    const uint64_t need = uint64_t(a.grid) * uint64_t(a.prev2_seq + 1);
-    for (int j = threadIdx.x; j < a.m; j += 32) {
-      if (j == s.p) continue;
-      const uint64_t *f = reinterpret_cast<const uint64_t *>(s.counter(a.worker_rank[s.G[j]], kDoneOff));
-      if (dev::ld_acquire_sys(f) >= need) continue;
-      count(a.counters, kCntFlagSpins);
-      const uint64_t t0 = dev::globaltimer();
-      while (dev::ld_acquire_sys(f) < need) {
-        if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;
-        if (dev::globaltimer() - t0 > a.timeout_ns) {
-          if (atomicExch(a.abort_dev, 1u) == 0u) {
-            unsigned long long *e = a.err_host;
-            e[1] = 1;  // consumed (the peer's launch of call - 2 is not done)
-            e[2] = s.cta;
-            e[3] = dev::ld_acquire_sys(f);
-            e[4] = need;
-            e[5] = (unsigned long long)s.G[j];
-            e[6] = (unsigned long long)j;
-            e[7] = (unsigned long long)a.my_rank;
-            __threadfence_system();
-            atomicExch(e, (unsigned long long)(-SESGD_ETIMEOUT));
-            __threadfence_system();
-          }
-          break;
-        }
-      }
-    }
-  }
+  // guard: every peer has finished (and so re-armed every receive slot of) its launch of call - 2
+  if (a.prev2_seq >= 0 && threadIdx.x < 32)
+    for (int j = threadIdx.x; j < a.m; j += 32)
+      if (j != s.p) wait_done(a, s.cta, a.worker_rank[s.G[j]], s.G[j], j);
   __syncthreads();
   if (a.hop_delay_ns) {  // injected per-hop latency (config 4): the reduce-scatter round's hop
     if (threadIdx.x == 0) {
@@ -633,10 +489,7 @@ __device__ __forceinline__ void k4w_body(const P2PArgs &a, unsigned char *dsmem)
     s.run_f(w / kWarpsF, (w % kWarpsF) * 32 + (threadIdx.x & 31));
   }
   __syncthreads();  // every re-arm of this CTA precedes the release (cumulativity)
-  if (threadIdx.x == 0) {
-    dev::fence_acq_rel_sys();
-    atomicAdd(s.counter(a.my_rank, kDoneOff), 1ull);
-  }
+  if (threadIdx.x == 0) signal_done(a);
 }
 
 template <int W, bool GRAD>

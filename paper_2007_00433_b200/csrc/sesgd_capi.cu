@@ -98,7 +98,7 @@ void freeze_layout(sesgd_ctx *ctx) {
   if (ctx->protocol < 0) {
     const bool value = resolve_path(ctx) == SESGD_PATH_TWOSHOT && ctx->m >= 2 && !ctx->push_tma &&
                        !ctx->payload_bf16;
-    ctx->protocol = !value ? 0 : (ctx->n_local == 1 ? 2 : 1);
+    ctx->protocol = !value ? 0 : (ctx->n_local == 1 || sesgd::p2p_wsm_supported(ctx->n_local, ctx->m)) ? 2 : 1;
   }
   const int var = ctx->p2p_variant;
   const int chunk = sesgd::p2p_chunk_elems(var);
@@ -119,7 +119,8 @@ void freeze_layout(sesgd_ctx *ctx) {
   // every CTA must be co-resident (COMM and COMPUTE wait on each other): grid = SMs x
   // occupancy, with the COMM guard cache (pairs x Gc u64) in dynamic shared memory
   int grid = ctx->sm_count * occupancy(sesgd::p2p_smem_bytes(var, 0, 0));
-  if (ctx->protocol == 2) grid = ctx->sm_count * sesgd::p2p_ws_occupancy(ctx->m);  // K4W: CTA per SM
+  if (ctx->protocol == 2)  // K4W / K4W-M: one CTA per SM
+    grid = ctx->sm_count * (r == 1 ? sesgd::p2p_ws_occupancy(ctx->m) : sesgd::p2p_wsm_occupancy(r));
   if (ctx->grid_opt > 0 && ctx->grid_opt < grid) grid = int(ctx->grid_opt);
   size_t smem = sesgd::p2p_smem_bytes(var, pairs, grid);
   const int grid2 = ctx->sm_count * occupancy(smem);
@@ -450,15 +451,18 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   } else {
     mark_start(ctx, st);
     cudaError_t e = (twoshot && ctx->protocol == 2 && !nvls)
-                        ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
+                        ? (ctx->n_local == 1 ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
+                                             : sesgd::launch_p2p_wsm(a, ctx->mode, vec, st))
                     : twoshot ? sesgd::launch_p2p_twoshot(a, ctx->mode, vec, ctx->push_tma != 0, st)
                               : sesgd::launch_p2p_oneshot(a, ctx->p2p_variant, ctx->mode, vec,
                                                           ctx->guard_smem, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
     mark_end(ctx, st);
   }
-  if (twoshot && ctx->protocol == 2 && !nvls)  // every claimed chunk plus one failed claim per CTA
-    ctx->claim_base += uint64_t(a.g1 - a.g0) + uint64_t(ctx->grid);
+  if (twoshot && ctx->protocol == 2 && !nvls && ctx->m >= 2)  // every claimed unit + one failed claim per CTA
+    ctx->claim_base += uint64_t(ctx->n_local == 1 ? a.g1 - a.g0
+                                                  : sesgd::p2p_wsm_units(ctx->n_local, ctx->m, a.g1 - a.g0)) +
+                       uint64_t(ctx->grid);
   // bookkeeping
   int remote_peers = 0;
   for (int s = 0; s < ctx->n_local; ++s) {
@@ -1008,8 +1012,8 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path with LSU pushes");
   if (ctx->protocol >= 1 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma || ctx->payload_bf16))
     return fail(ctx, SESGD_ENOTSUP, "the value-carried protocol needs the fp32 two-shot path with LSU pushes");
-  if (ctx->protocol == 2 && ctx->n_local != 1)
-    return fail(ctx, SESGD_ENOTSUP, "protocol 2 (warp-specialised K4W) needs one worker per GPU");
+  if (ctx->protocol == 2 && ctx->n_local != 1 && !sesgd::p2p_wsm_supported(ctx->n_local, ctx->m))
+    return fail(ctx, SESGD_ENOTSUP, "protocol 2 (K4W-M) supports 2..8 workers per GPU");
   if (path == SESGD_PATH_NVLS && (ctx->p2p_variant != 0 || ctx->n_local != 1 || ctx->m != ctx->n || !ctx->mc_ws))
     return fail(ctx, SESGD_ENOTSUP,
                 "the NVLS path needs one worker per GPU, group_size = n and sesgd_attach_multicast");
@@ -1091,8 +1095,8 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     return fail(ctx, SESGD_ENOTSUP, "the bf16 payload needs the two-shot path with LSU pushes");
   if (ctx->protocol >= 1 && (path != SESGD_PATH_TWOSHOT || ctx->push_tma || ctx->payload_bf16))
     return fail(ctx, SESGD_ENOTSUP, "the value-carried protocol needs the fp32 two-shot path with LSU pushes");
-  if (ctx->protocol == 2 && ctx->n_local != 1)
-    return fail(ctx, SESGD_ENOTSUP, "protocol 2 (warp-specialised K4W) needs one worker per GPU");
+  if (ctx->protocol == 2 && ctx->n_local != 1 && !sesgd::p2p_wsm_supported(ctx->n_local, ctx->m))
+    return fail(ctx, SESGD_ENOTSUP, "protocol 2 (K4W-M) supports 2..8 workers per GPU");
   for (auto &b : ctx->buckets) b.stats.sync_calls++;
   return launch_oneshot(ctx, -1, lr, momentum, static_cast<cudaStream_t>(stream), twoshot, nvls);
 }

@@ -141,27 +141,28 @@ def test_two_gpus_one_worker_each(tmp_path, mode, fused):
     _compare(V, v)
 
 
-@pytest.mark.parametrize("path", [2, 4])
+@pytest.mark.parametrize("path,protocol", [(2, -1), (4, 0), (4, 1)])
 @pytest.mark.parametrize("n,m", [(4, 2), (8, 2), (8, 4), (4, 1), (8, 8)])
-def test_two_gpus_resident_pairs(tmp_path, n, m, path):
+def test_two_gpus_resident_pairs(tmp_path, n, m, path, protocol):
     """n/2 workers per GPU through K3 (one-shot) and K4 (two-shot): groups mix co-resident
     members (read in place from the local stage, updated in place) and remote members (NVLink
     push); all-local groups are updated in registers; the schedule changes every iteration,
     exercising the call-2 receive-slot guard."""
     buckets = [65537, 3, 20000]
     T = 7
-    X, V = _launch(tmp_path, 2, n, m, T, buckets, path=path)
+    X, V = _launch(tmp_path, 2, n, m, T, buckets, path=path, protocol=protocol)
     x, v = _oracle(n, m, sum(buckets), T, 0)
     _compare(X, x)
     _compare(V, v)
 
 
+@pytest.mark.parametrize("protocol", [0, 1])
 @pytest.mark.parametrize("n,m", [(8, 4), (4, 2)])
-def test_two_gpus_resident_pairs_twoshot_grad(tmp_path, n, m):
+def test_two_gpus_resident_pairs_twoshot_grad(tmp_path, n, m, protocol):
     """K4 with co-resident members in GRAD mode: the slice owner applies the mean gradient to
     its co-resident members' v and x."""
     buckets = [65537, 3, 20000]
-    X, V = _launch(tmp_path, 2, n, m, 6, buckets, mode=1, path=4)
+    X, V = _launch(tmp_path, 2, n, m, 6, buckets, mode=1, path=4, protocol=protocol)
     x, v = _oracle(n, m, sum(buckets), 6, 1)
     _compare(X, x)
     _compare(V, v)
@@ -590,5 +591,58 @@ def test_stress_thousand_iterations_random_shapes(tmp_path, gpus, n, m, protocol
     X, V = _launch(tmp_path, gpus, n, m, T, buckets, mode, grid=grid, lag=lag, path=4, protocol=protocol,
                    release_every=rel)
     x, v = _oracle(n, m, sum(buckets), T, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+# ---------------------------------------------------------------- K4W-M: several workers per GPU
+# SESGD_OPT_PROTOCOL 2 with r > 1 (p2p_wsm.cu): units = pieces of one slice of one chunk for every
+# local worker; all-local groups folded in S, spanning groups through the x_hat ring / NVLink.
+@pytest.mark.parametrize("n,m,mode", [(4, 2, 0), (8, 2, 0), (8, 2, 1), (8, 4, 0), (8, 4, 1), (16, 8, 0)])
+def test_two_ranks_k4w_multi(tmp_path, n, m, mode):
+    buckets = [60001, 4097, 3]
+    X, V = _launch(tmp_path, 2, n, m, 6, buckets, mode, path=4, protocol=2)
+    x, v = _oracle(n, m, sum(buckets), 6, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("grid,fused", [(1, 1), (3, 0), (8, 1)])
+def test_two_ranks_k4w_multi_small_grids(tmp_path, grid, fused):
+    buckets = [250001, 13, 70000]
+    X, V = _launch(tmp_path, 2, 8, 2, 5, buckets, grid=grid, fused=fused, path=4, protocol=2)
+    x, v = _oracle(8, 2, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_four_ranks_k4w_multi(tmp_path, m):
+    buckets = [200003, 5000, 1]
+    X, V = _launch(tmp_path, 4, 8, m, 5, buckets, path=4, protocol=2)
+    x, v = _oracle(8, m, sum(buckets), 5, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("gpus", [4, 2])
+def test_k4w_multi_resnet50_bench_shape(tmp_path, gpus):
+    """cfg 2 at full size through K4W-M: n = 8, m = 2, 2 / 4 workers per rank, T = 100"""
+    from paper_2007_00433_b200.workloads import RESNET50_BUCKETS
+    buckets = list(RESNET50_BUCKETS)
+    coords = _sample(buckets)
+    X, V = _launch(tmp_path, gpus, 8, 2, 100, buckets, coords=coords, path=4, protocol=2)
+    x, v = _oracle(8, 2, sum(buckets), 100, 0, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_k4w_multi_weight_decay(tmp_path):
+    buckets = [65537, 3]
+    T, wd = 5, 1e-2
+    X, V = _launch(tmp_path, 2, 4, 2, T, buckets, 1, path=4, wd=wd, protocol=2)
+    x = np.tile(synth.x0_host(sum(buckets)), (4, 1))
+    v = np.zeros_like(x)
+    oracle.run_local(4, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=1, weight_decay=wd)
     _compare(X, x)
     _compare(V, v)
