@@ -162,6 +162,19 @@ extern "C" {
                                     launched cooperatively.  (A cooperative launch cannot start
                                     while the previous kernel drains: measured +10..30 us per
                                     step, profiles/r02_proto_*.json) */
+#define SESGD_OPT_DEVICE_ITER 23   /* 1: the iteration state lives in DEVICE memory -- the iteration t,
+                                    its groups (evaluated on the GPU from the shared seed)
+                                    and the call history of the exchange kernels -- so that
+                                    sesgd_begin_iter_device + the sync calls of one iteration can be
+                                    captured ONCE into a CUDA graph and the graph replayed for every
+                                    iteration.  Setting it uploads the host's state (synchronous);
+                                    setting 0 synchronises the device and copies the state back.
+                                    Needs sesgd_attach and every bucket registered (none after);
+                                    supported paths: resident (K6), two-shot with protocol 2
+                                    (K4W, K4W-M) and ring (K5); others return SESGD_ENOTSUP from
+                                    the sync call.  Not with SESGD_OPT_LOCAL_PERIOD > 1.  The
+                                    host-side counters of sesgd_get_stats count enqueued calls,
+                                    not graph replays (the dev_* counters count launches) */
 #define SESGD_OPT_EXPERIMENT 20    /* MEASUREMENT ONLY -- results are wrong when set: bit 0 drops
                                     the system-scope fence before the two-shot flag releases,
                                     bit 1 sends the two-shot pushes to this rank's own receive
@@ -262,7 +275,8 @@ SESGD_API int sesgd_attach_peers(sesgd_ctx *ctx, int32_t n_ranks, int32_t rank, 
 
 /* Set the current iteration t (any t >= 0: random access / resume).  Computes the
  * schedule of t (and of t-2, for the stage-reuse guard) on the host.
- * Errors: SESGD_EINVAL (iter < 0), SESGD_ESTATE (not attached). */
+ * Errors: SESGD_EINVAL (iter < 0), SESGD_ESTATE (not attached, or SESGD_OPT_DEVICE_ITER on:
+ * the iteration then lives on the device, sesgd_begin_iter_device). */
 SESGD_API int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter);
 
 /* The hot path: one SESGD sync+update of bucket `bucket` at the current iteration for all
@@ -349,8 +363,8 @@ SESGD_API int sesgd_get_stats(const sesgd_ctx *ctx, int32_t bucket, sesgd_stats 
 
 /* Measurement harness, not part of an iteration's normal API: sesgd_sync_all for BOTH ranks of a
  * two-rank loopback layout (contexts c0 = rank 0 and c1 = rank 1 on the same GPU, attached to
- * each other, protocol 2 = K4W, one worker each) as ONE kernel launch whose first half of CTAs
- * runs rank 0 and second half rank 1 -- same kernel body, same bits as two sesgd_sync_all calls
+ * each other, protocol 2: one worker each = K4W, or 2..8 workers each = K4W-M) as ONE kernel
+ * launch whose first half of CTAs runs rank 0 and second half rank 1 -- same kernel body, same bits as two sesgd_sync_all calls
  * -- so a profiler that serialises launches (ncu, which would deadlock two concurrent grids that
  * wait on each other) can capture the whole exchange.  Both contexts' call histories advance.
  * Errors: SESGD_EINVAL, SESGD_ESTATE, SESGD_ENOTSUP (not that layout), SESGD_ECUDA. */
@@ -364,6 +378,36 @@ SESGD_API int sesgd_sync_all_pair(sesgd_ctx *c0, sesgd_ctx *c1, float lr, float 
  * attached), SESGD_ECUDA. */
 SESGD_API int sesgd_measure_hop(sesgd_ctx *ctx, int32_t peer_rank, int32_t iters, int32_t initiator,
                                 void *stream);
+
+/* Device-side begin_iter (SESGD_OPT_DEVICE_ITER = 1): enqueues on `stream` one single-thread
+ * kernel that sets the device iteration to `iter` (>= 0) or, with iter = SESGD_ITER_NEXT (-1), to
+ * the device's current iteration + 1 (0 if none was set), and evaluates that iteration's canonical
+ * groups on the GPU -- the same partition sesgd_groups returns (A1; Alg.1 line 9,
+ * P:236).  Graph-capturable: captured once with SESGD_ITER_NEXT, every replay moves to the next
+ * iteration.  The host's iteration (shadow) advances the same way per ENQUEUE.
+ * Errors: SESGD_EINVAL (iter < -1), SESGD_ESTATE (device iteration off), SESGD_ECUDA. */
+#define SESGD_ITER_NEXT (-1)
+SESGD_API int sesgd_begin_iter_device(sesgd_ctx *ctx, int64_t iter, void *stream);
+
+/* Device address of the device iteration counter (int64, SESGD_OPT_DEVICE_ITER = 1): kernels of
+ * the caller's own that depend on t (a data loader, an LR schedule, the synthetic gradients of
+ * the tests) read it inside the same graph.  Owned by the context, valid until the option is
+ * cleared or the context destroyed.  Errors: SESGD_EINVAL, SESGD_ESTATE (device iteration off). */
+SESGD_API int sesgd_device_iter_ptr(const sesgd_ctx *ctx, const int64_t **t_dev_out);
+
+/* Snapshot of the device iteration state (SESGD_OPT_DEVICE_ITER = 1), for tests and debugging:
+ * synchronises the device, then copies t, the launch sequence number, the chunk-claim base, the
+ * canonical groups of t (canon[n], -1 beyond n) and K5's ring of local worker 0, and the call
+ * count of the first nbuckets buckets into bucket_calls (may be NULL when nbuckets = 0).
+ * Errors: SESGD_EINVAL, SESGD_ESTATE (device iteration off), SESGD_ECUDA. */
+typedef struct sesgd_device_iter_state {
+  int64_t t, seq, claim_base;
+  int32_t ring_pos;
+  int8_t canon[SESGD_MAX_WORKERS];
+  int8_t ring_rank[SESGD_MAX_WORKERS];
+} sesgd_device_iter_state;
+SESGD_API int sesgd_device_iter_read(const sesgd_ctx *ctx, sesgd_device_iter_state *out, int64_t *bucket_calls,
+                                     int32_t nbuckets);
 
 /* Number of SMs and CTAs per launch the library uses on the attached device (0 before attach). */
 SESGD_API int sesgd_launch_grid(const sesgd_ctx *ctx, int32_t *ctas_out);

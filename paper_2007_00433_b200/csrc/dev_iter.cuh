@@ -1,0 +1,70 @@
+// dev_iter.cuh -- the kernels' side of the device-resident iteration state (SESGD_OPT_DEVICE_ITER,
+// iter.cu).  A launch in that mode carries only its static arguments; thread 0 of every CTA copies
+// them to shared memory and patches the per-launch fields (call history, parity, sequence number,
+// chunk-claim base) and the iteration's schedule from the device state, so a captured CUDA graph
+// replays correctly for every iteration.  The LAST CTA of the launch to finish advances the state
+// (every CTA read it before finishing), and stream order hands it to the next launch.
+#pragma once
+#include "internal.h"
+
+namespace sesgd {
+namespace devit {
+
+// the launch's per-call fields from the state (thread 0; `s` is a shared-memory copy of the args)
+__device__ __forceinline__ void patch(P2PArgs &s) {
+  const DevIter *d = s.dev;
+  const DevBucket B = s.dev_buckets[s.bucket >= 0 ? s.bucket : 0];  // an all-bucket launch: one history
+  s.call = B.calls;
+  s.parity = int(B.calls & 1);
+  s.seq = d->seq;
+  s.prev2_seq = B.calls >= 2 ? B.hist[B.calls & 1] : -1;
+  s.seq_epoch0 = uint64_t(s.seq) * uint64_t(s.kmax) + 1;
+  s.prev2_epoch0 = B.calls >= 2 ? uint64_t(s.prev2_seq) * uint64_t(s.kmax) + 1 : 0;
+  s.claim_base = d->claim_base;
+  for (int i = 0; i < s.n; ++i) {
+    s.canon[i] = d->canon[i];
+    s.group_of[i] = d->group_of[i];
+  }
+  for (int q = 0; q < s.r; ++q) {
+    s.my_pos[q] = d->my_pos[q];
+    s.slot_kind[q] = d->slot_kind[q];
+  }
+}
+
+__device__ __forceinline__ void patch(RingArgs &s) {
+  const DevIter *d = s.dev;
+  const DevBucket B = s.dev_buckets[s.bucket];
+  s.call = B.calls;
+  s.parity = int(B.calls & 1);
+  s.seq = d->seq;
+  s.pos = d->ring_pos;
+  for (int q = 0; q < s.m; ++q) s.ring_rank[q] = d->ring_rank[q];
+}
+
+// thread 0 of every CTA, after the CTA's last access to its arguments: the last CTA advances the
+// call history of the launch's buckets, the launch sequence and the chunk-claim base
+__device__ __forceinline__ bool last_cta(DevIter *d) {
+  __threadfence();
+  return atomicAdd(&d->fin, 1u) + 1u == gridDim.x;
+}
+__device__ __forceinline__ void advance(DevIter *d, DevBucket *bk, int bucket, int nbuckets, int64_t seq,
+                                        uint64_t claim_next) {
+  for (int b = (bucket >= 0 ? bucket : 0); b < (bucket >= 0 ? bucket + 1 : nbuckets); ++b) {
+    DevBucket &B = bk[b];
+    B.hist[B.calls & 1] = seq;
+    B.calls += 1;
+  }
+  d->seq = seq + 1;
+  d->claim_base = claim_next;
+  d->fin = 0u;
+  __threadfence();
+}
+__device__ __forceinline__ void finish(const P2PArgs &s) {
+  if (last_cta(s.dev)) advance(s.dev, s.dev_buckets, s.bucket, s.nbuckets, s.seq, s.claim_base + s.dev_claim_inc);
+}
+__device__ __forceinline__ void finish(const RingArgs &s) {
+  if (last_cta(s.dev)) advance(s.dev, s.dev_buckets, s.bucket, s.nbuckets, s.seq, s.dev->claim_base);
+}
+
+}  // namespace devit
+}  // namespace sesgd

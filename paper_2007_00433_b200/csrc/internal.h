@@ -25,6 +25,37 @@ void latency_model(int n, int m, double bytes, double nu, double tau, sesgd_cost
 // ---------------------------------------------------------------- kernels
 constexpr int kMaxLocal = SESGD_MAX_WORKERS;
 
+// Device-resident iteration state (SESGD_OPT_DEVICE_ITER; iter.cu): the iteration t, its
+// schedule and the call history of the multi-GPU kernels live in device memory, so one captured
+// CUDA graph of [sesgd_begin_iter_device, sync launches] replays every iteration.  Every worker
+// derives its groups on the device from the shared seed, with no message.
+struct DevIter {
+  int64_t t;              // current iteration (its schedule is below)
+  int64_t seq;            // multi-GPU sync launches of this context so far
+  uint64_t claim_base;    // K4W / K4W-M chunk-claim counter before the next launch
+  unsigned int fin;       // CTAs of the running launch that finished (the last one advances)
+  int32_t ring_pos;       // K5: position of local slot 0 in its group
+  int8_t canon[SESGD_MAX_WORKERS], group_of[SESGD_MAX_WORKERS];
+  int8_t member_slot[SESGD_MAX_WORKERS];  // K6: canon mapped to local slots (every worker local)
+  int8_t my_pos[SESGD_MAX_WORKERS];       // per local slot: position in its group
+  int8_t slot_kind[SESGD_MAX_WORKERS];    // per local slot: as P2PArgs::slot_kind
+  int8_t ring_rank[SESGD_MAX_WORKERS];    // K5: rank of ring position q (local slot 0's group)
+};
+struct DevBucket {
+  int64_t calls;    // sync launches that covered the bucket
+  int64_t hist[2];  // launch sequence numbers of the last two calls, by call parity
+};
+// static inputs of the begin kernel (host-side attach / layout data)
+struct IterBeginArgs {
+  uint64_t seed;
+  int64_t t;        // >= 0: set the iteration; < 0: advance the device's t by one
+  int n, m, schedule, n_local, rank, direct;
+  int8_t local_workers[SESGD_MAX_WORKERS];
+  int8_t slot_of[SESGD_MAX_WORKERS];      // worker -> local slot (every worker local: K6)
+  int8_t worker_rank[SESGD_MAX_WORKERS];  // -1 before the layout is frozen
+};
+cudaError_t launch_iter_begin(const IterBeginArgs &a, DevIter *d, cudaStream_t stream);
+
 // K6: all n workers resident on this GPU (1-GPU "k simulated workers").
 struct ResidentArgs {
   float *const *x;        // [n_local] device table, indexed by local slot
@@ -42,6 +73,7 @@ struct ResidentArgs {
   const float *const *bg;
   const int64_t *numels;  // [nb]
   int8_t member_slot[SESGD_MAX_WORKERS];  // canonical order, mapped to local slots
+  const DevIter *dev;     // non-null: member_slot comes from the device iteration state
 };
 // mode: SESGD_MODE_*; vec: all pointers 16-byte aligned; grid_x: CTAs per group;
 // unroll: 0 = default (SESGD_OPT_RESIDENT_UNROLL)
@@ -116,6 +148,13 @@ struct P2PArgs {
   int8_t worker_slot[SESGD_MAX_WORKERS];
   int8_t canon[SESGD_MAX_WORKERS];           // canonical groups of the iteration
   int8_t group_of[SESGD_MAX_WORKERS];
+  // device iteration state (null: the fields above are this launch's): the kernel patches call,
+  // parity, seq, prev2_seq, epochs, claim_base and the schedule fields from it, and its last CTA
+  // to finish advances it (dev_claim_inc: claims this launch makes)
+  DevIter *dev;
+  DevBucket *dev_buckets;
+  uint64_t dev_claim_inc;
+  int64_t kmax;             // epochs per launch (seq_epoch0 = seq * kmax + 1)
 };
 // device-side handshake counters (one block per context, cumulative; fire-and-forget atomics)
 enum DevCounter : int {
@@ -150,6 +189,9 @@ struct RingArgs {
   int cooperative;
   unsigned long long *counters;
   int8_t ring_rank[SESGD_MAX_WORKERS];  // rank of ring position 0..m-1 (ascending worker id)
+  DevIter *dev;                         // device iteration state (as P2PArgs::dev)
+  DevBucket *dev_buckets;
+  int64_t seq;                          // launch sequence number (patched in device mode)
 };
 cudaError_t launch_ring(const RingArgs &a, int mode, cudaStream_t stream);
 cudaError_t launch_pingpong(uint64_t *mine, uint64_t *peer, int iters, int initiator, uint64_t base,
@@ -177,6 +219,7 @@ int p2p_ws_occupancy(int m);
 int p2p_ws_threads();
 // K4W-M (SESGD_OPT_PROTOCOL = 2 with several workers per GPU), p2p_wsm.cu
 cudaError_t launch_p2p_wsm(const P2PArgs &a, int mode, bool vec, cudaStream_t stream);
+cudaError_t launch_p2p_wsm_pair(const P2PArgs &a0, const P2PArgs &a1, int mode, bool vec, cudaStream_t stream);
 bool p2p_wsm_supported(int r, int m);
 int p2p_wsm_occupancy(int r);
 int64_t p2p_wsm_units(int r, int m, int64_t chunks);  // claimable units of `chunks` chunks
@@ -276,5 +319,10 @@ struct sesgd_ctx {
   uint64_t claim_base = 0;        // K4W dynamic chunk claims so far (chunks + one failed claim per CTA)
   int hop_iters = 0;
   int profile = 0;
+  // SESGD_OPT_DEVICE_ITER: iteration state in device memory (iter.cu, dev_iter.cuh); the host
+  // fields (t, seq, claim_base, bucket calls / seq_hist) keep shadowing what was ENQUEUED
+  int device_iter = 0;
+  sesgd::DevIter *d_iter = nullptr;
+  sesgd::DevBucket *d_bstate = nullptr;
   std::string last_error;
 };

@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ws_common.cuh"
+#include "dev_iter.cuh"
 
 namespace sesgd {
 namespace {
@@ -63,6 +64,7 @@ struct WS {
   float *x_ring;   // [kQX][cap]
   int cap;
   int me, p, m;
+  float inv_m;  // dev::pow2_inverse(m)
   const int8_t *G;
   int64_t nk;  // chunks of this launch (claimed dynamically)
   int gc;
@@ -72,6 +74,7 @@ struct WS {
     me = a.my_workers[0];
     p = a.my_pos[0];
     m = a.m;
+    inv_m = dev::pow2_inverse(m);
     G = a.canon + a.group_of[me] * a.m;
     gc = a.grid;
     cta = int(blockIdx.x) % a.grid;
@@ -323,7 +326,7 @@ struct WS {
           if (nv <= 0) continue;
           const int64_t e = c.e0 + o;
 #pragma unroll
-          for (int w = 0; w < W; ++w) acc[u][w] = __fdiv_rn(acc[u][w], float(m));
+          for (int w = 0; w < W; ++w) acc[u][w] = dev::mean_rt(acc[u][w], m, inv_m);
           for (int rr = 0; rr < m; ++rr)  // all-gather: my slice's mean to every peer
             if (rr != p) push<W>(recv(G[rr], p) + c.soff + e, acc[u], nv);
           if constexpr (!GRAD) {
@@ -498,6 +501,21 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot(const __grid_consta
   k4w_body<W, GRAD>(a, dsmem);
 }
 
+// device-resident iteration state (SESGD_OPT_DEVICE_ITER): the per-call fields and the schedule
+// come from device memory (dev_iter.cuh), so one captured graph replays every iteration
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWS, 1) k4w_twoshot_dev(const __grid_constant__ P2PArgs a) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  __shared__ P2PArgs sa;
+  if (threadIdx.x == 0) {
+    sa = a;
+    devit::patch(sa);
+  }
+  __syncthreads();
+  k4w_body<W, GRAD>(sa, dsmem);
+  if (threadIdx.x == 0) devit::finish(sa);
+}
+
 // measurement harness (sesgd_sync_all_pair): two loopback virtual ranks of one GPU in ONE grid --
 // CTAs [0, a0.grid) are rank a0's, the rest rank a1's -- so a profiler that serialises kernel
 // launches (ncu) sees the whole exchange in one kernel.  Same body, same bits.
@@ -511,8 +529,15 @@ __global__ void __launch_bounds__(kThreadsWS, 1) k4w_pair(const __grid_constant_
     k4w_body<W, GRAD>(a1, dsmem);
 }
 
-const void *pick_ws(int mode, bool vec) {
+const void *pick_ws(int mode, bool vec, bool devi = false) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (devi) {
+    if (vec)
+      return grad ? reinterpret_cast<const void *>(&k4w_twoshot_dev<4, true>)
+                  : reinterpret_cast<const void *>(&k4w_twoshot_dev<4, false>);
+    return grad ? reinterpret_cast<const void *>(&k4w_twoshot_dev<1, true>)
+                : reinterpret_cast<const void *>(&k4w_twoshot_dev<1, false>);
+  }
   if (vec)
     return grad ? reinterpret_cast<const void *>(&k4w_twoshot<4, true>)
                 : reinterpret_cast<const void *>(&k4w_twoshot<4, false>);
@@ -535,8 +560,8 @@ int p2p_ws_occupancy(int m) {
   const size_t smem = ws_smem(m);
   int occ = 1 << 30;
   for (int mode = 0; mode < 2; ++mode)
-    for (int vec = 0; vec < 2; ++vec) {
-      const void *k = pick_ws(mode, vec != 0);
+    for (int vec = 0; vec < 4; ++vec) {  // bit 1: the device-iteration variant
+      const void *k = pick_ws(mode, (vec & 1) != 0, (vec & 2) != 0);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       int b = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kThreadsWS, smem) != cudaSuccess) b = 1;
@@ -558,7 +583,7 @@ cudaError_t launch_p2p_ws_pair(const P2PArgs &a0, const P2PArgs &a1, int mode, b
 }
 
 cudaError_t launch_p2p_ws(const P2PArgs &a, int mode, bool vec, cudaStream_t stream) {
-  const void *k = pick_ws(mode, vec);
+  const void *k = pick_ws(mode, vec, a.dev != nullptr);
   const size_t smem = ws_smem(a.m);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};

@@ -18,12 +18,16 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ws_common.cuh"
+#include "dev_iter.cuh"
 
 namespace sesgd {
 namespace {
 using namespace wsx;
 
-constexpr int kWarpsP = 1, kWarpsS = 8, kGroupsR = 2, kWarpsR = 4, kGroupsF = 2, kWarpsF = 4;
+// S streams every local worker's data (r items per vector); R and F only touch the groups that
+// span GPUs (a fraction of the workers), so S gets most of the warps (measured: with S = 8,
+// R = F = 2 x 4, S was busy for the whole launch and R / F waited on it)
+constexpr int kWarpsP = 1, kWarpsS = 16, kGroupsR = 2, kWarpsR = 2, kGroupsF = 2, kWarpsF = 2;
 constexpr int kThS = kWarpsS * 32, kThR = kWarpsR * 32, kThF = kWarpsF * 32;
 constexpr int kThreadsWSM = (kWarpsP + kWarpsS + kGroupsR * kWarpsR + kGroupsF * kWarpsF) * 32;  // 800
 constexpr int kChunkWSM = 4096;  // K4's chunking: same slices
@@ -32,12 +36,21 @@ constexpr int kU = 2;            // vectors in flight per R / F thread
 constexpr int kMaxR = 8;         // local workers supported (else K4)
 static_assert(kQX % kGroupsR == 0 && kQI % kGroupsF == 0 && kQI > kQL, "ring depths");
 
+// a decoded unit: bucket b, slice j, chunk start e0 (bucket element), stage offset of the bucket,
+// piece [plo, phi) of the chunk.  P decodes each claimed unit ONCE and publishes it with the id
+// (a 64-bit division and a bucket search per unit; every S / R / F thread used to redo them)
+struct UnitM {
+  int b, j;
+  int64_t e0, soff, plo, phi;
+};
 struct SmemM {
   uint64_t full_ld[kQL], empty_ld[kQL], full_x[kQX], empty_x[kQX], full_id[kQI], empty_id[kQI];
-  int64_t uid[kQI];  // unit of step k (P -> S, F)
-  int64_t xuid[kQX]; // unit of the x_hat ring entry (S -> R)
+  int64_t uid[kQI];   // unit of step k (P -> S, F); < 0 ends the role
+  int64_t xuid[kQX];  // unit of the x_hat ring entry (S -> R)
+  UnitM unit[kQI];    // decoded uid[]
+  UnitM xunit[kQX];   // decoded xuid[]
 };
-constexpr size_t kHeadM = 512;
+constexpr size_t kHeadM = 1024;
 
 __host__ __device__ inline int sub_of(int r) { return r <= 4 ? 1024 : 512; }
 
@@ -49,11 +62,13 @@ struct WSM {
   float *ld_ring;  // [kQL][r][3][sub]
   float *x_ring;   // [kQX][r][sub]
   int r, m, sub, upc, cta;
+  float inv_m;  // dev::pow2_inverse(m)
   int64_t nunits;
 
   __device__ WSM(const P2PArgs &args, unsigned char *smem) : a(args) {
     r = a.r;
     m = a.m;
+    inv_m = dev::pow2_inverse(m);
     sub = sub_of(r);
     cta = int(blockIdx.x) % a.grid;
     sm = reinterpret_cast<SmemM *>(smem);
@@ -69,10 +84,7 @@ struct WSM {
   __device__ __forceinline__ int64_t hi(int j, int64_t len) const {
     return j == m - 1 ? len : min(int64_t(j + 1) * slice(), len);
   }
-  struct Unit {
-    int b, j;
-    int64_t e0, soff, plo, phi;  // the piece is [plo, phi) of the chunk (may be empty)
-  };
+  using Unit = UnitM;  // the piece is [plo, phi) of the chunk (may be empty)
   __device__ __forceinline__ Unit decode(int64_t u) const {
     const int64_t g = a.g0 + u / upc;
     int p = int(u % upc);
@@ -122,10 +134,11 @@ struct WSM {
   }
   __device__ __forceinline__ float *xent(int q, int s) const { return x_ring + (size_t(q) * r + s) * sub; }
 
-  __device__ __forceinline__ void post_id(int64_t k, int64_t u) const {
+  __device__ __forceinline__ void post_id(int64_t k, int64_t u, const Unit *x = nullptr) const {
     const int qi = int(k % kQI);
     if (k >= kQI) mbar_spin(&sm->empty_id[qi], uint32_t((k / kQI - 1) & 1));
     sm->uid[qi] = u;
+    if (x) sm->unit[qi] = *x;
     mbar_arrive(&sm->full_id[qi]);
   }
 
@@ -138,7 +151,9 @@ struct WSM {
       const int64_t u = idx < uint64_t(nunits) ? int64_t(idx) : -1;
       const int q = int(k % kQL);
       if (k >= kQL) mbar_spin(&sm->empty_ld[q], uint32_t((k / kQL - 1) & 1));
-      post_id(k, u);
+      Unit x{};
+      if (u >= 0) x = decode(u);
+      post_id(k, u, &x);
       if (u < 0) {
         dev::mbar_arrive_expect_tx(&sm->full_ld[q], 0);
         post_id(k + 1, -1);
@@ -148,7 +163,6 @@ struct WSM {
         mbar_arrive(&sm->full_ld[q]);
         continue;
       }
-      const Unit x = decode(u);
       const uint32_t bytes = uint32_t((x.phi - x.plo) / 4) * 16;  // whole float4s; tails via S
       uint32_t tx = 0;
       for (int s = 0; s < r; ++s) tx += bytes * ((GRAD && a.slot_kind[s] == 0) ? 1u : 3u);
@@ -202,15 +216,19 @@ struct WSM {
       }
       if (k >= kQX) mbar_spin(&sm->empty_x[qx], uint32_t((k / kQX - 1) & 1));
       if (lead) t_wait += dev::globaltimer() - tw;
-      const Unit x = decode(u);
+      const Unit x = sm->unit[k % kQI];
       const int64_t len4 = x.plo + ((x.phi - x.plo) & ~int64_t(3));
       const int64_t nvec = (x.phi - x.plo + W - 1) / W;
-      for (int s = 0; s < r; ++s) {
+      // (local slot, vector) items of the unit, flattened so that every S thread has the same
+      // share whatever r is (r * nvec items; nvec = 256 for a full piece at r <= 4)
+      const int nvi = int(nvec);
+      for (int it = t; it < r * nvi; it += kThS) {
+        const int s = it / nvi, vi = it - s * nvi;
         const int kind = a.slot_kind[s];
         if (kind == 2) continue;  // updated with its group's first member
         const int8_t *G = group(a.my_workers[s]);
-        for (int64_t vi = t; vi < nvec; vi += kThS) {
-          const int64_t o = x.plo + vi * W;
+        {
+          const int64_t o = x.plo + int64_t(vi) * W;
           const int nv = int(min(int64_t(W), x.phi - o));
           const int64_t e = x.e0 + o;
           if (kind == 1) {  // every member here: the 1-GPU kernel's arithmetic in registers
@@ -236,7 +254,7 @@ struct WSM {
               }
             }
 #pragma unroll
-            for (int w = 0; w < W; ++w) acc[w] = __fdiv_rn(acc[w], float(m));
+            for (int w = 0; w < W; ++w) acc[w] = dev::mean_rt(acc[w], m, inv_m);
             for (int rr = 0; rr < m; ++rr) {
               const int sl = a.worker_slot[G[rr]];
               if constexpr (!GRAD) {
@@ -285,6 +303,7 @@ struct WSM {
       if ((t & 31) == 0) {
         mbar_arrive(&sm->empty_ld[q]);
         sm->xuid[qx] = u;
+        sm->xunit[qx] = x;
         mbar_arrive(&sm->full_x[qx]);
       }
     }
@@ -315,7 +334,7 @@ struct WSM {
         }
         delayed = true;
       }
-      const Unit x = decode(u);
+      const Unit x = sm->xunit[qx];
       for (int o_s = 0; o_s < r; ++o_s) {  // every local owner of slice j in a group with remote members
         if (a.slot_kind[o_s] != 0 || a.my_pos[o_s] != x.j) continue;
         const int me = a.my_workers[o_s];
@@ -363,7 +382,7 @@ struct WSM {
             if (nv <= 0) continue;
             const int64_t e = x.e0 + o;
 #pragma unroll
-            for (int q2 = 0; q2 < W; ++q2) acc[uu][q2] = __fdiv_rn(acc[uu][q2], float(m));
+            for (int q2 = 0; q2 < W; ++q2) acc[uu][q2] = dev::mean_rt(acc[uu][q2], m, inv_m);
             for (int rr = 0; rr < m; ++rr) {
               const int w = G[rr];
               if (!local(w)) {
@@ -410,10 +429,10 @@ struct WSM {
       const int qi = int(k % kQI);
       mbar_spin(&sm->full_id[qi], uint32_t((k / kQI) & 1));
       const int64_t u = sm->uid[qi];
+      const Unit x = sm->unit[qi];
       __syncwarp();
       if ((t & 31) == 0) mbar_arrive(&sm->empty_id[qi]);
       if (u < 0) break;
-      const Unit x = decode(u);
       for (int s = 0; s < r; ++s) {  // every local worker whose slice-j owner is remote
         if (a.slot_kind[s] != 0) continue;
         const int me = a.my_workers[s];
@@ -463,8 +482,7 @@ struct WSM {
 };
 
 template <int W, bool GRAD>
-__global__ void __launch_bounds__(kThreadsWSM, 1) k4w_multi(const __grid_constant__ P2PArgs a) {
-  extern __shared__ __align__(128) unsigned char dsmem[];
+__device__ __forceinline__ void k4w_multi_body(const P2PArgs &a, unsigned char *dsmem) {
   const WSM<W, GRAD> s(a, dsmem);
   if (s.cta == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (threadIdx.x == 0) {
@@ -516,8 +534,46 @@ __global__ void __launch_bounds__(kThreadsWSM, 1) k4w_multi(const __grid_constan
   if (threadIdx.x == 0) signal_done(a);
 }
 
-const void *pick_wsm(int mode, bool vec) {
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWSM, 1) k4w_multi(const __grid_constant__ P2PArgs a) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  k4w_multi_body<W, GRAD>(a, dsmem);
+}
+
+// measurement harness (sesgd_sync_all_pair): two loopback virtual ranks in ONE grid (as k4w_pair)
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWSM, 1) k4w_multi_pair(const __grid_constant__ P2PArgs a0,
+                                                                const __grid_constant__ P2PArgs a1) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  if (int(blockIdx.x) < a0.grid)
+    k4w_multi_body<W, GRAD>(a0, dsmem);
+  else
+    k4w_multi_body<W, GRAD>(a1, dsmem);
+}
+
+// device-resident iteration state (SESGD_OPT_DEVICE_ITER, dev_iter.cuh)
+template <int W, bool GRAD>
+__global__ void __launch_bounds__(kThreadsWSM, 1) k4w_multi_dev(const __grid_constant__ P2PArgs a) {
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  __shared__ P2PArgs sa;
+  if (threadIdx.x == 0) {
+    sa = a;
+    devit::patch(sa);
+  }
+  __syncthreads();
+  k4w_multi_body<W, GRAD>(sa, dsmem);
+  if (threadIdx.x == 0) devit::finish(sa);
+}
+
+const void *pick_wsm(int mode, bool vec, bool devi = false) {
   const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  if (devi) {
+    if (vec)
+      return grad ? reinterpret_cast<const void *>(&k4w_multi_dev<4, true>)
+                  : reinterpret_cast<const void *>(&k4w_multi_dev<4, false>);
+    return grad ? reinterpret_cast<const void *>(&k4w_multi_dev<1, true>)
+                : reinterpret_cast<const void *>(&k4w_multi_dev<1, false>);
+  }
   if (vec)
     return grad ? reinterpret_cast<const void *>(&k4w_multi<4, true>)
                 : reinterpret_cast<const void *>(&k4w_multi<4, false>);
@@ -532,15 +588,17 @@ size_t wsm_smem(int r) {
 
 }  // namespace
 
-bool p2p_wsm_supported(int r, int m) { return r >= 2 && r <= kMaxR && m >= 2 && wsm_smem(r) <= 227 * 1024; }
+bool p2p_wsm_supported(int r, int m) {  // (+ the device-iteration variant's argument copy)
+  return r >= 2 && r <= kMaxR && m >= 2 && wsm_smem(r) + sizeof(P2PArgs) <= 227 * 1024;
+}
 
 int p2p_wsm_occupancy(int r) {
   static_assert(sizeof(SmemM) <= kHeadM, "barrier block");
   const size_t smem = wsm_smem(r);
   int occ = 1 << 30;
   for (int mode = 0; mode < 2; ++mode)
-    for (int vec = 0; vec < 2; ++vec) {
-      const void *k = pick_wsm(mode, vec != 0);
+    for (int vec = 0; vec < 4; ++vec) {  // bit 1: the device-iteration variant
+      const void *k = pick_wsm(mode, (vec & 1) != 0, (vec & 2) != 0);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       int b = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kThreadsWSM, smem) != cudaSuccess) b = 1;
@@ -560,8 +618,20 @@ int64_t p2p_wsm_units(int r, int m, int64_t chunks) {
   return chunks * upc;
 }
 
+cudaError_t launch_p2p_wsm_pair(const P2PArgs &a0, const P2PArgs &a1, int mode, bool vec, cudaStream_t stream) {
+  const bool grad = (mode == SESGD_MODE_GRAD_AVG);
+  const void *k = vec ? (grad ? reinterpret_cast<const void *>(&k4w_multi_pair<4, true>)
+                              : reinterpret_cast<const void *>(&k4w_multi_pair<4, false>))
+                      : (grad ? reinterpret_cast<const void *>(&k4w_multi_pair<1, true>)
+                              : reinterpret_cast<const void *>(&k4w_multi_pair<1, false>));
+  const size_t smem = wsm_smem(a0.r);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  void *args[] = {const_cast<P2PArgs *>(&a0), const_cast<P2PArgs *>(&a1)};
+  return launch_persistent(k, unsigned(a0.grid + a1.grid), kThreadsWSM, args, smem, stream, false);
+}
+
 cudaError_t launch_p2p_wsm(const P2PArgs &a, int mode, bool vec, cudaStream_t stream) {
-  const void *k = pick_wsm(mode, vec);
+  const void *k = pick_wsm(mode, vec, a.dev != nullptr);
   const size_t smem = wsm_smem(a.r);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   void *args[] = {const_cast<P2PArgs *>(&a)};

@@ -214,7 +214,8 @@ __device__ __forceinline__ void resident_bucket(const ResidentArgs &a, const int
 template <int M, int W, bool GRAD, int U, bool WD>
 __global__ void __launch_bounds__(kThreads) k6_resident(const __grid_constant__ ResidentArgs a) {
   const int m = M > 0 ? M : a.m;
-  const int8_t *mem = a.member_slot + blockIdx.y * m;
+  // device iteration state (SESGD_OPT_DEVICE_ITER): the iteration's groups from device memory
+  const int8_t *mem = (a.dev ? a.dev->member_slot : a.member_slot) + blockIdx.y * m;
   if (a.nb == 0) {
     resident_bucket<M, W, GRAD, U, WD>(a, mem, m, a.x, a.v, a.g, a.numel);
   } else {

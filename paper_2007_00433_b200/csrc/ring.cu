@@ -22,6 +22,7 @@
 // later is guarded by the receiver's consumed counter.  Every spin has a timeout.
 #include "common.cuh"
 #include "internal.h"
+#include "dev_iter.cuh"
 
 namespace sesgd {
 namespace {
@@ -208,7 +209,29 @@ __global__ void __launch_bounds__(kRingThreads) k5_ring(const __grid_constant__ 
     r.run();
 }
 
-const void *pick(int mode) {
+// device-resident iteration state (SESGD_OPT_DEVICE_ITER, dev_iter.cuh)
+template <bool GRAD>
+__global__ void __launch_bounds__(kRingThreads) k5_ring_dev(const __grid_constant__ RingArgs a) {
+  __shared__ RingArgs sa;
+  if (threadIdx.x == 0) {
+    sa = a;
+    devit::patch(sa);
+  }
+  __syncthreads();
+  const Ring<GRAD> r(sa);
+  if (blockIdx.x == 0 && threadIdx.x == 0) count(sa.counters, kCntLaunches);
+  if (sa.m == 1)
+    r.local_only();
+  else
+    r.run();
+  __syncthreads();
+  if (threadIdx.x == 0) devit::finish(sa);
+}
+
+const void *pick(int mode, bool devi = false) {
+  if (devi)
+    return mode == SESGD_MODE_GRAD_AVG ? reinterpret_cast<const void *>(&k5_ring_dev<true>)
+                                       : reinterpret_cast<const void *>(&k5_ring_dev<false>);
   return mode == SESGD_MODE_GRAD_AVG ? reinterpret_cast<const void *>(&k5_ring<true>)
                                      : reinterpret_cast<const void *>(&k5_ring<false>);
 }
@@ -218,15 +241,17 @@ const void *pick(int mode) {
 int ring_block_threads() { return kRingThreads; }
 
 int ring_occupancy(int mode) {
-  int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode), kRingThreads, 0) != cudaSuccess)
+  int blocks = 0, bd = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick(mode), kRingThreads, 0) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, pick(mode, true), kRingThreads, 0) != cudaSuccess)
     return 1;
+  blocks = bd < blocks ? bd : blocks;
   return blocks > 0 ? blocks : 1;
 }
 
 cudaError_t launch_ring(const RingArgs &a, int mode, cudaStream_t stream) {
   void *args[] = {const_cast<RingArgs *>(&a)};
-  return launch_persistent(pick(mode), unsigned(a.grid), kRingThreads, args, 0, stream, a.cooperative != 0);
+  return launch_persistent(pick(mode, a.dev != nullptr), unsigned(a.grid), kRingThreads, args, 0, stream, a.cooperative != 0);
 }
 
 }  // namespace sesgd

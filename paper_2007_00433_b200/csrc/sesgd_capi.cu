@@ -208,6 +208,86 @@ bool local_only_iteration(const sesgd_ctx *ctx) {
   return ctx->local_period > 1 && (ctx->t + 1) % ctx->local_period != 0;
 }
 
+// ---- device-resident iteration state (SESGD_OPT_DEVICE_ITER) ----
+sesgd::IterBeginArgs iter_begin_args(const sesgd_ctx *ctx, int64_t t) {
+  sesgd::IterBeginArgs a{};
+  a.seed = ctx->seed;
+  a.t = t;
+  a.n = ctx->n;
+  a.m = ctx->m;
+  a.schedule = ctx->schedule;
+  a.n_local = ctx->n_local;
+  a.rank = ctx->peers ? ctx->rank : 0;
+  a.direct = ctx->p2p_variant == 0 ? 1 : 0;
+  for (int s = 0; s < ctx->n_local; ++s) a.local_workers[s] = int8_t(ctx->local_workers[s]);
+  for (int w = 0; w < ctx->n; ++w) {
+    a.slot_of[w] = ctx->slot_of[w];
+    a.worker_rank[w] = ctx->peers ? ctx->worker_rank[w] : int8_t(ctx->slot_of[w] >= 0 ? 0 : -1);
+  }
+  return a;
+}
+
+int device_iter_enable(sesgd_ctx *ctx) {
+  if (!ctx->attached || ctx->buckets.empty()) return fail(ctx, SESGD_ESTATE, "attach and register buckets first");
+  for (auto &b : ctx->buckets)
+    if (!b.registered) return fail(ctx, SESGD_ESTATE, "bucket ids must be dense from 0");
+  if (ctx->local_period > 1) return fail(ctx, SESGD_ENOTSUP, "device iteration state with Local-SESGD");
+  if (ctx->n_local == ctx->n && !ctx->resident_tables_ok) {  // no allocation may happen inside a capture
+    const int rc = upload_resident_tables(ctx);
+    if (rc != SESGD_OK) return rc;
+  }
+  const size_t nb = ctx->buckets.size();
+  cudaError_t e = cudaSuccess;
+  if (!ctx->d_iter) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_iter), sizeof(sesgd::DevIter));
+  if (e == cudaSuccess && ctx->d_bstate) e = cudaFree(ctx->d_bstate);
+  ctx->d_bstate = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_bstate), nb * sizeof(sesgd::DevBucket));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "device iteration state");
+  sesgd::DevIter h{};
+  h.t = ctx->iter_set ? ctx->t : -1;
+  h.seq = ctx->seq;
+  h.claim_base = ctx->claim_base;
+  std::vector<sesgd::DevBucket> hb(nb);
+  for (size_t b = 0; b < nb; ++b) {
+    hb[b].calls = ctx->buckets[b].calls;
+    hb[b].hist[0] = ctx->buckets[b].seq_hist[0];
+    hb[b].hist[1] = ctx->buckets[b].seq_hist[1];
+  }
+  e = cudaDeviceSynchronize();  // no launch of this context may still read the old state
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_iter, &h, sizeof(h), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bstate, hb.data(), nb * sizeof(sesgd::DevBucket), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && ctx->iter_set) e = sesgd::launch_iter_begin(iter_begin_args(ctx, ctx->t), ctx->d_iter, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "device iteration state upload");
+  ctx->device_iter = 1;
+  return SESGD_OK;
+}
+
+int device_iter_disable(sesgd_ctx *ctx) {
+  if (!ctx->device_iter) return SESGD_OK;
+  sesgd::DevIter h{};
+  std::vector<sesgd::DevBucket> hb(ctx->buckets.size());
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(&h, ctx->d_iter, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(hb.data(), ctx->d_bstate, hb.size() * sizeof(sesgd::DevBucket), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "device iteration state download");
+  ctx->seq = h.seq;
+  ctx->claim_base = h.claim_base;
+  for (size_t b = 0; b < hb.size(); ++b) {
+    ctx->buckets[b].calls = hb[b].calls;
+    ctx->buckets[b].seq_hist[0] = hb[b].hist[0];
+    ctx->buckets[b].seq_hist[1] = hb[b].hist[1];
+  }
+  ctx->iter_set = h.t >= 0;
+  if (ctx->iter_set) {
+    ctx->t = h.t;
+    make_groups(ctx, ctx->t, ctx->canon, ctx->group_of);
+  }
+  ctx->device_iter = 0;
+  return SESGD_OK;
+}
+
 int local_step(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st) {
   ResidentArgs a{};
   a.lr = lr;
@@ -446,6 +526,20 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   bool vec = true;
   for (size_t b = 0; b < ctx->buckets.size(); ++b)
     if (bucket < 0 || int(b) == bucket) vec = vec && ctx->buckets[b].vec;
+  const bool ws_kernel = twoshot && ctx->protocol == 2 && !nvls;
+  const uint64_t claim_inc =
+      (ws_kernel && ctx->m >= 2)  // every claimed unit + one failed claim per CTA
+          ? uint64_t(ctx->n_local == 1 ? a.g1 - a.g0 : sesgd::p2p_wsm_units(ctx->n_local, ctx->m, a.g1 - a.g0)) +
+                uint64_t(ctx->grid)
+          : 0;
+  if (ctx->device_iter) {
+    if (!ws_kernel || dry)
+      return fail(ctx, SESGD_ENOTSUP, "device iteration state: the exchange needs protocol 2 (K4W / K4W-M)");
+    a.dev = ctx->d_iter;
+    a.dev_buckets = ctx->d_bstate;
+    a.dev_claim_inc = claim_inc;
+    a.kmax = ctx->kmax;
+  }
   if (dry) {
     *dry = a;
   } else {
@@ -459,10 +553,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
     if (e != cudaSuccess) return cuda_fail(ctx, e, twoshot ? "launch two-shot kernel" : "launch one-shot kernel");
     mark_end(ctx, st);
   }
-  if (twoshot && ctx->protocol == 2 && !nvls && ctx->m >= 2)  // every claimed unit + one failed claim per CTA
-    ctx->claim_base += uint64_t(ctx->n_local == 1 ? a.g1 - a.g0
-                                                  : sesgd::p2p_wsm_units(ctx->n_local, ctx->m, a.g1 - a.g0)) +
-                       uint64_t(ctx->grid);
+  ctx->claim_base += claim_inc;
   // bookkeeping
   int remote_peers = 0;
   for (int s = 0; s < ctx->n_local; ++s) {
@@ -542,6 +633,8 @@ void sesgd_destroy(sesgd_ctx *ctx) {
   if (ctx->d_bg) cudaFree(const_cast<float **>(ctx->d_bg));
   if (ctx->d_numels) cudaFree(ctx->d_numels);
   if (ctx->d_counters) cudaFree(ctx->d_counters);
+  if (ctx->d_iter) cudaFree(ctx->d_iter);
+  if (ctx->d_bstate) cudaFree(ctx->d_bstate);
   if (ctx->ev_l0) cudaEventDestroy(ctx->ev_l0);
   if (ctx->ev_l1) cudaEventDestroy(ctx->ev_l1);
   for (auto *v : {&ctx->ev_in, &ctx->ev_k, &ctx->ev_out})
@@ -632,8 +725,13 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->schedule = int(value);
       return SESGD_OK;
     }
+    case SESGD_OPT_DEVICE_ITER:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "device iteration must be 0 or 1");
+      if (value == ctx->device_iter) return SESGD_OK;
+      return value ? device_iter_enable(ctx) : device_iter_disable(ctx);
     case SESGD_OPT_LOCAL_PERIOD:
       if (value < 1) return fail(ctx, SESGD_EINVAL, "local period must be >= 1");
+      if (value > 1 && ctx->device_iter) return fail(ctx, SESGD_ENOTSUP, "Local-SESGD with the device iteration state");
       ctx->local_period = value;
       return SESGD_OK;
     case SESGD_OPT_RELEASE_STAGGER:
@@ -755,6 +853,7 @@ int sesgd_register_bucket(sesgd_ctx *ctx, int32_t bucket, int64_t numel, float *
   if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
   if (bucket < 0 || bucket >= kMaxBuckets) return fail(ctx, SESGD_EINVAL, "bucket id out of range");
   if (numel < 0 || !x || !v || !g) return fail(ctx, SESGD_EINVAL, "null pointer table or numel < 0");
+  if (ctx->device_iter) return fail(ctx, SESGD_ESTATE, "buckets are fixed while the device iteration state is on");
   if (ctx->layout_frozen && (size_t(bucket) >= ctx->buckets.size() ||
                              ctx->buckets[bucket].numel != numel))
     return fail(ctx, SESGD_ESTATE, "bucket layout is fixed once peers attach");
@@ -902,9 +1001,52 @@ int sesgd_begin_iter(sesgd_ctx *ctx, int64_t iter) {
   if (!ctx) return SESGD_EINVAL;
   if (iter < 0) return fail(ctx, SESGD_EINVAL, "iteration must be >= 0");
   if (!ctx->attached) return fail(ctx, SESGD_ESTATE, "sesgd_attach first");
+  if (ctx->device_iter)
+    return fail(ctx, SESGD_ESTATE, "the iteration lives on the device: sesgd_begin_iter_device");
   make_groups(ctx, iter, ctx->canon, ctx->group_of);
   ctx->t = iter;
   ctx->iter_set = true;
+  return SESGD_OK;
+}
+
+int sesgd_begin_iter_device(sesgd_ctx *ctx, int64_t iter, void *stream) {
+  if (!ctx) return SESGD_EINVAL;
+  if (iter < -1) return fail(ctx, SESGD_EINVAL, "iteration must be >= 0 or SESGD_ITER_NEXT");
+  if (!ctx->device_iter) return fail(ctx, SESGD_ESTATE, "SESGD_OPT_DEVICE_ITER is off");
+  cudaError_t e = sesgd::launch_iter_begin(iter_begin_args(ctx, iter), ctx->d_iter, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch begin_iter_device");
+  ctx->t = iter >= 0 ? iter : (ctx->iter_set ? ctx->t + 1 : 0);  // the host shadow (per enqueue)
+  make_groups(ctx, ctx->t, ctx->canon, ctx->group_of);
+  ctx->iter_set = true;
+  return SESGD_OK;
+}
+
+int sesgd_device_iter_ptr(const sesgd_ctx *ctx, const int64_t **t_dev_out) {
+  if (!ctx || !t_dev_out) return SESGD_EINVAL;
+  if (!ctx->device_iter) return SESGD_ESTATE;
+  *t_dev_out = &ctx->d_iter->t;
+  return SESGD_OK;
+}
+
+int sesgd_device_iter_read(const sesgd_ctx *ctx, sesgd_device_iter_state *out, int64_t *bucket_calls,
+                           int32_t nbuckets) {
+  if (!ctx || !out || nbuckets < 0 || (nbuckets > 0 && !bucket_calls)) return SESGD_EINVAL;
+  if (!ctx->device_iter) return SESGD_ESTATE;
+  sesgd::DevIter h{};
+  std::vector<sesgd::DevBucket> hb(ctx->buckets.size());
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(&h, ctx->d_iter, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(hb.data(), ctx->d_bstate, hb.size() * sizeof(sesgd::DevBucket), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return SESGD_ECUDA;
+  out->t = h.t;
+  out->seq = h.seq;
+  out->claim_base = int64_t(h.claim_base);
+  for (int i = 0; i < SESGD_MAX_WORKERS; ++i) {
+    out->canon[i] = i < ctx->n ? h.canon[i] : -1;
+    out->ring_rank[i] = i < ctx->m ? h.ring_rank[i] : -1;
+  }
+  out->ring_pos = h.ring_pos;
+  for (int b = 0; b < nbuckets && size_t(b) < hb.size(); ++b) bucket_calls[b] = hb[b].calls;
   return SESGD_OK;
 }
 
@@ -940,6 +1082,7 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     a.m = ctx->m;
     a.k = ctx->n / ctx->m;
     for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
+    a.dev = ctx->device_iter ? ctx->d_iter : nullptr;
     const int gx = resident_grid_x(ctx, b.vec, b.numel);
     mark_start(ctx, st);
     cudaError_t e = sesgd::launch_resident(a, ctx->mode, b.vec, gx, ctx->resident_unroll, st);
@@ -986,6 +1129,11 @@ int sesgd_sync_step(sesgd_ctx *ctx, int32_t bucket, float lr, float momentum, vo
     for (int q = 0; q < ctx->m; ++q) {
       ra.ring_rank[q] = ctx->worker_rank[G[q]];
       if (G[q] == me) ra.pos = q;
+    }
+    ra.seq = ctx->seq;
+    if (ctx->device_iter) {
+      ra.dev = ctx->d_iter;
+      ra.dev_buckets = ctx->d_bstate;
     }
     mark_start(ctx, st);
     cudaError_t e = sesgd::launch_ring(ra, ctx->mode, st);
@@ -1063,6 +1211,7 @@ int sesgd_sync_all(sesgd_ctx *ctx, float lr, float momentum, void *stream) {
     a.bg = ctx->d_bg;
     a.numels = ctx->d_numels;
     for (int i = 0; i < ctx->n; ++i) a.member_slot[i] = ctx->slot_of[ctx->canon[i]];
+    a.dev = ctx->device_iter ? ctx->d_iter : nullptr;
     mark_start(ctx, static_cast<cudaStream_t>(stream));
     cudaError_t e = sesgd::launch_resident(a, ctx->mode, vec, resident_grid_x(ctx, vec, biggest),
                                            ctx->resident_unroll, static_cast<cudaStream_t>(stream));
@@ -1107,9 +1256,9 @@ int sesgd_sync_all_pair(sesgd_ctx *c0, sesgd_ctx *c1, float lr, float momentum, 
     int rc = check_latched(c);
     if (rc != SESGD_OK) return rc;
     if (!c->peers || !c->iter_set) return fail(c, SESGD_ESTATE, "attach peers and begin_iter first");
-    if (c->n_ranks != 2 || c->protocol != 2 || resolve_path(c) != SESGD_PATH_TWOSHOT || c->n_local != 1 ||
-        local_only_iteration(c))
-      return fail(c, SESGD_ENOTSUP, "the pair harness runs K4W (protocol 2) on a two-rank loopback layout");
+    if (c->n_ranks != 2 || c->protocol != 2 || resolve_path(c) != SESGD_PATH_TWOSHOT || c->m < 2 ||
+        local_only_iteration(c) || c->device_iter)
+      return fail(c, SESGD_ENOTSUP, "the pair harness runs K4W / K4W-M (protocol 2) on a two-rank loopback layout");
     for (auto &b : c->buckets)
       if (b.calls != c->buckets[0].calls) return fail(c, SESGD_ESTATE, "buckets must share one call history");
   }
@@ -1126,7 +1275,8 @@ int sesgd_sync_all_pair(sesgd_ctx *c0, sesgd_ctx *c1, float lr, float momentum, 
   int rc = launch_oneshot(c0, -1, lr, momentum, st, true, false, &a0);
   if (rc == SESGD_OK) rc = launch_oneshot(c1, -1, lr, momentum, st, true, false, &a1);
   if (rc != SESGD_OK) return rc;
-  const cudaError_t e = sesgd::launch_p2p_ws_pair(a0, a1, c0->mode, vec, st);
+  const cudaError_t e = c0->n_local == 1 ? sesgd::launch_p2p_ws_pair(a0, a1, c0->mode, vec, st)
+                                         : sesgd::launch_p2p_wsm_pair(a0, a1, c0->mode, vec, st);
   if (e != cudaSuccess) return cuda_fail(c0, e, "launch the K4W pair");
   return SESGD_OK;
 }

@@ -99,7 +99,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dev::smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
-  while (!dev::mbar_try_wait(bar, parity)) {
+  while (!dev::mbar_try_wait_suspend(bar, parity)) {
   }
 }
 
@@ -133,7 +133,10 @@ __device__ __forceinline__ void wait_value(const P2PArgs &a, int cta, int me, co
   if (!pending<W>(y, nv) || (a.experiment & 2)) return;  // (experiment: nobody writes my slots)
   count(a.counters, kCntValueSpins);
   const uint64_t t0 = dev::globaltimer();
+  unsigned nap = 32;  // back off between polls: a polling warp sleeps instead of taking issue slots
   for (;;) {
+    __nanosleep(nap);
+    nap = nap < 256 ? 2 * nap : 256;
     ld_rel<W>(src, y, nv);
     if (!pending<W>(y, nv)) break;
     if (*reinterpret_cast<volatile unsigned int *>(a.abort_dev)) break;

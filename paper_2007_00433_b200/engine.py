@@ -149,6 +149,59 @@ class SESGDEngine:
     def begin_iter(self, t: int) -> None:
         C.sesgd_begin_iter(self.ctx, t)
 
+    # -------------------------------------------------------------- device-resident iterations
+    def set_device_iter(self, on: bool = True) -> None:
+        """SESGD_OPT_DEVICE_ITER: the iteration t, its groups (evaluated on the GPU from the shared
+        seed) and the exchange call history live in device memory, so one captured CUDA
+        graph replays every iteration.  Synchronous switch; off copies the state back."""
+        C.sesgd_set_option(self.ctx, C.OPT_DEVICE_ITER, int(on))
+        self.device_iter = bool(on)
+
+    def begin_iter_device(self, t: int = C.ITER_NEXT, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream if stream is not None else self.default_stream()
+        C.sesgd_begin_iter_device(self.ctx, t, s.cuda_stream)
+
+    def t_device_ptr(self) -> int:
+        """device address of the int64 iteration counter (for t-dependent kernels in the graph)"""
+        return C.sesgd_device_iter_ptr(self.ctx)
+
+    def enqueue_iteration(self, lr: float, momentum: float, produce=None, fused: bool = True,
+                          stream: Optional[torch.cuda.Stream] = None) -> None:
+        """device-iteration mode: [next iteration on the device, produce(engine, stream) (e.g. the
+        gradient fill reading t_device_ptr()), the sync launch(es)] on one stream"""
+        s = stream if stream is not None else self.default_stream()
+        self.begin_iter_device(C.ITER_NEXT, s)
+        if produce is not None:
+            produce(self, s)
+        if fused:
+            self.sync_all(lr, momentum, s)
+        else:
+            for b in range(len(self.bucket_sizes)):
+                self.sync_step(b, lr, momentum, s)
+
+    def capture_iteration(self, lr: float, momentum: float, produce=None, fused: bool = True):
+        """one iteration (enqueue_iteration) captured ONCE into a CUDA graph; every replay
+        (replay_iteration) runs the next iteration -- Algorithm 1's loop body with no
+        host work per iteration.  Captured on this engine's own stream (loopback) or a side stream"""
+        if not getattr(self, "device_iter", False):
+            raise RuntimeError("capture_iteration needs set_device_iter(True)")
+        if self.stream is not None:
+            s = self.stream
+        else:
+            if getattr(self, "_capture_stream", None) is None:
+                self._capture_stream = torch.cuda.Stream(device=self.device)
+            s = self._capture_stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.enqueue_iteration(lr, momentum, produce, fused, s)
+        return g
+
+    def replay_iteration(self, g) -> None:
+        """one replay of a captured iteration on this engine's default stream"""
+        with torch.cuda.stream(self.default_stream()):
+            g.replay()
+
     def sync_step(self, b: int, lr: float, momentum: float, stream: Optional[torch.cuda.Stream] = None):
         s = stream if stream is not None else self.default_stream()
         C.sesgd_sync_step(self.ctx, b, lr, momentum, s.cuda_stream)
@@ -161,7 +214,10 @@ class SESGDEngine:
              fused: bool = True):
         """One SESGD iteration over every bucket (Alg.1 lines 3-11 for all local workers):
         one sesgd_sync_all call (fused), or one sesgd_sync_step per bucket."""
-        self.begin_iter(t)
+        if getattr(self, "device_iter", False):
+            self.begin_iter_device(t, stream)
+        else:
+            self.begin_iter(t)
         if fused:
             self.sync_all(lr, momentum, stream)
         else:
@@ -296,6 +352,19 @@ class LoopbackGroup:
         the R persistent grids run concurrently and exchange through each other's workspaces"""
         for e in self.engines:
             e.step(t, lr, momentum, fused=fused)
+
+    def set_device_iter(self, on: bool = True) -> None:
+        for e in self.engines:
+            e.set_device_iter(on)
+
+    def capture_iteration(self, lr: float, momentum: float, produce=None, fused: bool = True):
+        """one CUDA graph per virtual rank (each captured on its own stream); replay() runs them
+        concurrently, one iteration per replay"""
+        return [e.capture_iteration(lr, momentum, produce, fused) for e in self.engines]
+
+    def replay(self, graphs) -> None:
+        for e, g in zip(self.engines, graphs):
+            e.replay_iteration(g)
 
     def step_pair(self, t: int, lr: float, momentum: float) -> None:
         """measurement harness (two virtual ranks, K4W): both ranks' iteration as ONE kernel launch

@@ -25,7 +25,8 @@ OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL, OPT_PUSH_TMA = 8
 OPT_RELEASE_DELAY, OPT_RELEASE_EVERY, OPT_LOCAL_PERIOD, OPT_SCHEDULE = 13, 14, 15, 16
 SCHEDULE_RANDOM, SCHEDULE_DIMENSION_EXCHANGE = 0, 1
 OPT_RELEASE_STAGGER, OPT_PAYLOAD_BF16, OPT_SM_BUDGET = 17, 18, 19
-OPT_EXPERIMENT, OPT_PROTOCOL, OPT_COOPERATIVE = 20, 21, 22
+OPT_EXPERIMENT, OPT_PROTOCOL, OPT_COOPERATIVE, OPT_DEVICE_ITER = 20, 21, 22, 23
+ITER_NEXT = -1
 
 # every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
 EXPORTED = (
@@ -36,6 +37,7 @@ EXPORTED = (
     "sesgd_probe_copy", "sesgd_probe_pingpong", "sesgd_profile_read", "sesgd_sync_all",
     "sesgd_global_average", "sesgd_sync_all_host", "sesgd_consensus", "sesgd_set_weight_decay",
     "sesgd_attach_multicast", "sesgd_pair_counts", "sesgd_measure_hop", "sesgd_sync_all_pair",
+    "sesgd_begin_iter_device", "sesgd_device_iter_ptr", "sesgd_device_iter_read",
 )
 
 
@@ -51,6 +53,12 @@ class sesgd_stats(ctypes.Structure):
                 ("dev_flag_stores", ctypes.c_int64), ("dev_flag_spins", ctypes.c_int64),
                 ("dev_value_spins", ctypes.c_int64), ("dev_launches", ctypes.c_int64),
                 ("last_launch_us", ctypes.c_double), ("hop_ns", ctypes.c_double)]
+
+
+class sesgd_device_iter_state(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("seq", ctypes.c_int64), ("claim_base", ctypes.c_int64),
+                ("ring_pos", ctypes.c_int32), ("canon", ctypes.c_int8 * MAX_WORKERS),
+                ("ring_rank", ctypes.c_int8 * MAX_WORKERS)]
 
 
 class SesgdError(RuntimeError):
@@ -82,6 +90,9 @@ def lib():
             "sesgd_workspace_prepare": ([P, P], ctypes.c_int),
             "sesgd_attach_peers": ([P, i32, i32, P, P], ctypes.c_int),
             "sesgd_begin_iter": ([P, i64], ctypes.c_int),
+            "sesgd_begin_iter_device": ([P, i64, P], ctypes.c_int),
+            "sesgd_device_iter_ptr": ([P, ctypes.POINTER(P)], ctypes.c_int),
+            "sesgd_device_iter_read": ([P, ctypes.POINTER(sesgd_device_iter_state), P, i32], ctypes.c_int),
             "sesgd_sync_step": ([P, i32, f32, f32, P], ctypes.c_int),
             "sesgd_sync_step_host": ([P, i32, f32, f32, P, P, P], ctypes.c_int),
             "sesgd_sync_all": ([P, f32, f32, P], ctypes.c_int),
@@ -193,6 +204,24 @@ def sesgd_attach_peers(ctx, n_ranks: int, rank: int, rank_ws_ptrs, worker_rank) 
 
 def sesgd_begin_iter(ctx, it: int) -> None:
     _check(lib().sesgd_begin_iter(ctx, it), ctx)
+
+
+def sesgd_begin_iter_device(ctx, it: int = ITER_NEXT, stream: int = 0) -> None:
+    _check(lib().sesgd_begin_iter_device(ctx, it, stream), ctx)
+
+
+def sesgd_device_iter_ptr(ctx) -> int:
+    p = ctypes.c_void_p()
+    _check(lib().sesgd_device_iter_ptr(ctx, ctypes.byref(p)), ctx)
+    return int(p.value)
+
+
+def sesgd_device_iter_read(ctx, n: int, m: int, nbuckets: int = 0) -> dict:
+    st = sesgd_device_iter_state()
+    calls = np.zeros(max(nbuckets, 1), np.int64)
+    _check(lib().sesgd_device_iter_read(ctx, ctypes.byref(st), calls.ctypes.data_as(ctypes.c_void_p), nbuckets), ctx)
+    return {"t": st.t, "seq": st.seq, "claim_base": st.claim_base, "ring_pos": st.ring_pos,
+            "canon": list(st.canon[:n]), "ring_rank": list(st.ring_rank[:m]), "calls": calls[:nbuckets].tolist()}
 
 
 def sesgd_sync_step(ctx, bucket: int, lr: float, momentum: float, stream: int = 0) -> None:

@@ -42,6 +42,8 @@ def lib():
         P, i64, u64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32
         L.synth_fill_grad_device.argtypes = [P, i64, i64, u64, i32, i64, P]
         L.synth_fill_grad_device.restype = ctypes.c_int
+        L.synth_fill_grad_device_at.argtypes = [P, i64, i64, u64, i32, P, P]
+        L.synth_fill_grad_device_at.restype = ctypes.c_int
         L.synth_fill_x0_device.argtypes = [P, i64, i64, u64, P]
         L.synth_fill_x0_device.restype = ctypes.c_int
         L.synth_fill_grad_host.argtypes = [P, i64, i64, P, u64, i32, i64]
@@ -80,6 +82,15 @@ def fill_grad_device(ptr: int, numel: int, e0: int, worker: int, t: int, stream:
     rc = lib().synth_fill_grad_device(ptr, numel, e0, s_g, worker, t, stream)
     if rc != 0:
         raise RuntimeError(f"synth_fill_grad_device: cuda error {rc}")
+
+
+def fill_grad_device_at(ptr: int, numel: int, e0: int, worker: int, t_dev_ptr: int, stream: int = 0,
+                        s_g: int = SEED_G) -> None:
+    """gradient fill for the iteration held in device memory at t_dev_ptr (int64), read when the
+    kernel runs -- graph-capturable across iterations"""
+    rc = lib().synth_fill_grad_device_at(ptr, numel, e0, s_g, worker, t_dev_ptr, stream)
+    if rc != 0:
+        raise RuntimeError(f"synth_fill_grad_device_at: cuda error {rc}")
 
 
 def fill_x0_device(ptr: int, numel: int, e0: int, stream: int = 0, s_x: int = SEED_X) -> None:

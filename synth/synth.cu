@@ -20,6 +20,18 @@ __global__ void __launch_bounds__(256) fill_grad_kernel(float *__restrict__ out,
     out[j] = synth_grad(key, e0 + j);
 }
 
+// the same fill with the iteration read from device memory (*t_dev): a captured CUDA graph that
+// replays every iteration (libsesgd's SESGD_OPT_DEVICE_ITER, sesgd_device_iter_ptr) regenerates
+// the gradients of the device's current iteration
+__global__ void __launch_bounds__(256) fill_grad_at_kernel(float *__restrict__ out, int64_t numel,
+                                                           int64_t e0, uint64_t s_g, int32_t worker,
+                                                           const int64_t *t_dev) {
+  const uint64_t key = synth_grad_key(s_g, worker, *t_dev);
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < numel; j += stride)
+    out[j] = synth_grad(key, e0 + j);
+}
+
 __global__ void __launch_bounds__(256) fill_x0_kernel(float *__restrict__ out, int64_t numel,
                                                       int64_t e0, uint64_t xkey) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -45,6 +57,14 @@ int synth_fill_grad_device(float *out, int64_t numel, int64_t e0, uint64_t s_g, 
   if (numel <= 0) return 0;
   fill_grad_kernel<<<grid_for(numel), 256, 0, (cudaStream_t)stream>>>(
       out, numel, e0, synth_grad_key(s_g, worker, t));
+  return (int)cudaGetLastError();
+}
+
+// as synth_fill_grad_device with t = *t_dev (a device int64 read when the kernel runs)
+int synth_fill_grad_device_at(float *out, int64_t numel, int64_t e0, uint64_t s_g, int32_t worker,
+                              const int64_t *t_dev, void *stream) {
+  if (numel <= 0) return 0;
+  fill_grad_at_kernel<<<grid_for(numel), 256, 0, (cudaStream_t)stream>>>(out, numel, e0, s_g, worker, t_dev);
   return (int)cudaGetLastError();
 }
 

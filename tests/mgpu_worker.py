@@ -39,6 +39,49 @@ def _rows(eng, flat, buckets, coords):
     return np.stack([f[idx].cpu().numpy() for f in flat])
 
 
+def run_iterations(engs, a, buckets, offs, host_step):
+    """T iterations from t0.  --devit 0: host iterations (begin_iter + sync per iteration);
+    1: device iteration state, eager (sesgd_begin_iter_device + gradient fill reading the device's
+    t + sync, enqueued per iteration); 2: the same iteration captured ONCE as a CUDA graph and
+    replayed T times; 3: T/3 host iterations, the graph, then host iterations again (the state
+    moves host -> device -> host)."""
+    t0, T = a.t0, a.iters
+    if a.devit == 0:
+        for t in range(t0, t0 + T):
+            host_step(t)
+        return
+    h = T // 3 if a.devit == 3 else 0
+    for t in range(t0, t0 + h):
+        host_step(t)
+    for e in engs:
+        e.set_device_iter(True)
+    if h == 0 and t0 > 0:  # so that the first ITER_NEXT lands on t0
+        for e in engs:
+            e.begin_iter_device(t0 - 1)
+
+    def produce(e, s):
+        tp = e.t_device_ptr()
+        for slot, w in enumerate(e.local_workers):
+            for b, L in enumerate(buckets):
+                synth.fill_grad_device_at(e.g(slot, b).data_ptr(), L, int(offs[b]), w, tp, s.cuda_stream)
+
+    nd = T - 2 * h
+    if a.devit == 1:
+        for _ in range(nd):
+            for e in engs:
+                e.enqueue_iteration(0.1, 0.9, produce, bool(a.fused))
+    else:
+        graphs = [e.capture_iteration(0.1, 0.9, produce, bool(a.fused)) for e in engs]
+        for _ in range(nd):
+            for e, g in zip(engs, graphs):
+                e.replay_iteration(g)
+    if a.devit == 3:
+        for e in engs:
+            e.set_device_iter(False)
+        for t in range(t0 + h + nd, t0 + T):
+            host_step(t)
+
+
 def loopback(a):
     """R virtual ranks on cuda:0 (SESGD_OPT_SM_BUDGET = SMs / R each, one stream each)"""
     from paper_2007_00433_b200.engine import LoopbackGroup
@@ -54,13 +97,15 @@ def loopback(a):
         for s in range(eng.r):
             for b, L in enumerate(buckets):
                 synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st)
-    for t in range(a.t0, a.t0 + a.iters):
+    def host_step(t):
         for eng in grp:
             st = eng.stream.cuda_stream
             for s, w in enumerate(eng.local_workers):
                 for b, L in enumerate(buckets):
                     synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
         grp.step(t, 0.1, 0.9, fused=bool(a.fused))
+
+    run_iterations(list(grp), a, buckets, offs, host_step)
     if a.final_avg:
         grp.global_average()
     grp.synchronize()
@@ -99,6 +144,7 @@ def main():
     p.add_argument("--protocol", type=int, default=-1)  # SESGD_OPT_PROTOCOL, -1 = auto
     p.add_argument("--release-every", type=int, default=0)
     p.add_argument("--loopback", type=int, default=0)
+    p.add_argument("--devit", type=int, default=0)  # device iteration state: 1 eager, 2 graph, 3 mixed
     p.add_argument("--coords", default="")
     p.add_argument("--out", required=True)
     a = p.parse_args()
@@ -119,11 +165,13 @@ def main():
     for s in range(eng.r):
         for b, L in enumerate(buckets):
             synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st)
-    for t in range(a.t0, a.t0 + a.iters):
+    def host_step(t):
         for s, w in enumerate(eng.local_workers):
             for b, L in enumerate(buckets):
                 synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
         eng.step(t, 0.1, 0.9, fused=bool(a.fused))
+
+    run_iterations([eng], a, buckets, offs, host_step)
     if a.final_avg:
         eng.global_average()
     torch.cuda.synchronize()

@@ -43,7 +43,7 @@ def _free_port():
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
             lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
-            bf16=0, coords=None, protocol=-1, release_every=0):
+            bf16=0, coords=None, protocol=-1, release_every=0, devit=0):
     """`gpus` ranks: processes on as many GPUs (nvlink) or virtual ranks on cuda:0 (loopback)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -66,7 +66,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
-               "--bf16", str(bf16), "--protocol", str(protocol), "--release-every", str(release_every), "--loopback", str(gpus if loop else 0), *extra,
+               "--bf16", str(bf16), "--protocol", str(protocol), "--release-every", str(release_every), "--devit", str(devit), "--loopback", str(gpus if loop else 0), *extra,
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -644,5 +644,44 @@ def test_k4w_multi_weight_decay(tmp_path):
     x = np.tile(synth.x0_host(sum(buckets)), (4, 1))
     v = np.zeros_like(x)
     oracle.run_local(4, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, period=1, mode=1, weight_decay=wd)
+    _compare(X, x)
+    _compare(V, v)
+
+
+# ---------------------------------------------------------------- device-resident iteration state
+# SESGD_OPT_DEVICE_ITER: t, its groups (evaluated on the GPU) and the exchange call
+# history in device memory.  devit 1: sesgd_begin_iter_device + the gradient fill reading the
+# device's t + sync, enqueued per iteration; 2: that iteration captured ONCE as a CUDA graph and
+# replayed T times; 3: host iterations, graph replays, host iterations (state host -> device -> host).
+@pytest.mark.parametrize("devit", [1, 2, 3])
+@pytest.mark.parametrize("gpus,n,m,path", [(2, 2, 2, 4), (4, 8, 2, 4), (2, 8, 4, 4), (4, 4, 2, 3), (4, 4, 4, 3)])
+def test_device_iteration_state(tmp_path, devit, gpus, n, m, path):
+    """K4W (one worker per rank), K4W-M (several) and the paper's ring K5 (path 3), bit-exact vs
+    the oracle over T = 9 iterations (both call parities, several schedules)"""
+    buckets = [70001, 4099, 333]
+    X, V = _launch(tmp_path, gpus, n, m, 9, buckets, path=path, protocol=2 if path == 4 else -1, devit=devit)
+    x, v = _oracle_ring(n, m, buckets, 9, 0) if path == 3 else _oracle(n, m, sum(buckets), 9, 0)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("fused,mode", [(0, 0), (0, 1), (1, 1)])
+def test_device_iteration_graph_per_bucket_and_grad(tmp_path, fused, mode):
+    """per-bucket launches (per-layer mode) inside the graph, and GRAD mode; t0 > 0 (resume)"""
+    buckets = [30001, 7, 4096, 1, 12345]
+    X, V = _launch(tmp_path, 2, 4, 2, 7, buckets, mode, t0=11, fused=fused, path=4, protocol=2, devit=2)
+    x, v = _oracle(4, 2, sum(buckets), 7, mode, t0=11)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_device_iteration_resnet50_graph(tmp_path):
+    """the north star's one-worker-per-GPU layout at n = 4, the five ResNet-50 buckets at full size,
+    T = 30 graph replays, sampled coordinates"""
+    from paper_2007_00433_b200.workloads import RESNET50_BUCKETS
+    buckets = list(RESNET50_BUCKETS)
+    coords = _sample(buckets)
+    X, V = _launch(tmp_path, 4, 4, 2, 30, buckets, coords=coords, path=4, protocol=2, devit=2)
+    x, v = _oracle(4, 2, sum(buckets), 30, 0, coords=coords)
     _compare(X, x)
     _compare(V, v)

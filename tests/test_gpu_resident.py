@@ -410,3 +410,81 @@ def test_bf16_payload_rejected_on_resident_path():
         eng.sync_step(0, LR, MU)
     assert ei.value.code == C.ENOTSUP
     eng.close()
+
+
+# ---------------------------------------------------------------- device-resident iteration state
+@pytest.mark.parametrize("n,m,mode,fused", [(8, 2, 0, True), (8, 2, 1, True), (8, 4, 0, False), (12, 3, 0, True),
+                                            (16, 16, 0, True)])
+def test_device_iteration_graph_resident(n, m, mode, fused):
+    """SESGD_OPT_DEVICE_ITER on the 1-GPU path (K6): ONE captured CUDA graph of [begin_iter_device
+    (next t, groups evaluated on the GPU), gradient fill reading the device's t, sync] replayed for
+    T iterations is bit-exact with the oracle; switching the option off hands t back to the host,
+    which continues with two host iterations"""
+    SESGDEngine = _cuda()
+    from paper_2007_00433_b200 import sesgd as C
+    buckets = [699_051, 262_147, 87_378]
+    T = 7
+    eng = SESGDEngine(n, m, buckets, seed=42, mode=mode)
+    offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
+    st = torch.cuda.current_stream().cuda_stream
+    for s in range(eng.r):
+        for b, L in enumerate(buckets):
+            synth.fill_x0_device(eng.x(s, b).data_ptr(), L, int(offs[b]), st)
+    eng.set_device_iter(True)
+    with pytest.raises(C.SesgdError):  # the host may not move t while the device owns it
+        eng.begin_iter(0)
+
+    def produce(e, s):
+        tp = e.t_device_ptr()
+        for slot, w in enumerate(e.local_workers):
+            for b, L in enumerate(buckets):
+                synth.fill_grad_device_at(e.g(slot, b).data_ptr(), L, int(offs[b]), w, tp, s.cuda_stream)
+
+    g = eng.capture_iteration(LR, MU, produce, fused)
+    for _ in range(T):
+        eng.replay_iteration(g)
+    torch.cuda.synchronize()
+    eng.set_device_iter(False)
+    for t in (T, T + 1):  # the host continues from the device's t
+        for s, w in enumerate(eng.local_workers):
+            for b, L in enumerate(buckets):
+                synth.fill_grad_device(eng.g(s, b).data_ptr(), L, int(offs[b]), w, t, st)
+        eng.step(t, LR, MU, fused=fused)
+    torch.cuda.synchronize()
+    eng.poll()
+    X = np.stack([torch.cat([eng.x(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    V = np.stack([torch.cat([eng.v(s, b) for b in range(len(buckets))]).cpu().numpy() for s in range(eng.r)])
+    eng.close()
+    x, v = _run_oracle(n, m, sum(buckets), T + 2, mode)
+    _compare(X, x)
+    _compare(V, v)
+
+
+def test_device_iteration_schedule_matches_host():
+    """the device's groups for t (sesgd_begin_iter_device, K6 reads them) equal sesgd_groups(t):
+    one device iteration at a time, with lr = 0 and distinct x per worker, the K6 update is the
+    group mean -- compare it with the host schedule's group means over 40 random t"""
+    SESGDEngine = _cuda()
+    n, m = 16, 4
+    eng = SESGDEngine(n, m, [1024], seed=7)
+    eng.set_device_iter(True)
+    rng = np.random.default_rng(3)
+    for t in rng.integers(0, 2**40, 40):
+        x0 = rng.standard_normal((n, 1024)).astype(np.float32)
+        for s in range(n):
+            eng.x(s, 0).copy_(torch.from_numpy(x0[s]))
+            eng.g(s, 0).zero_()
+            eng.v(s, 0).zero_()
+        eng.begin_iter_device(int(t))
+        eng.sync_all(0.0, 0.0)
+        torch.cuda.synchronize()
+        perm, _ = eng.groups(int(t))
+        got = np.stack([eng.x(s, 0).cpu().numpy() for s in range(n)])
+        for j in range(n // m):
+            G = sorted(perm[j * m:(j + 1) * m])
+            acc = x0[G[0]].copy()
+            for w in G[1:]:
+                acc = (acc + x0[w]).astype(np.float32)
+            for w in G:
+                assert np.array_equal(got[w], (acc * np.float32(0.25)).astype(np.float32)), (t, G)
+    eng.close()

@@ -84,37 +84,38 @@ def test_measure_hop_between_virtual_ranks():
     grp.close()
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_k4w_pair_harness_is_bit_exact(mode):
-    """sesgd_sync_all_pair: both virtual ranks' K4W in one grid (the ncu harness) gives the oracle's
-    bits, like two concurrent launches"""
+@pytest.mark.parametrize("n,mode", [(2, 0), (2, 1), (8, 0), (8, 1)])
+def test_k4w_pair_harness_is_bit_exact(n, mode):
+    """sesgd_sync_all_pair: both virtual ranks' K4W (n = 2, one worker each) or K4W-M (n = 8, four
+    workers each) in one grid (the ncu harness) gives the oracle's bits, like two concurrent launches"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import oracle
     from paper_2007_00433_b200 import sesgd as C
     from paper_2007_00433_b200.engine import LoopbackGroup
     buckets = [100003, 7, 40000]
-    grp = LoopbackGroup(2, 2, 2, buckets, seed=42, mode=mode, timeout_ms=10000,
+    grp = LoopbackGroup(2, n, 2, buckets, seed=42, mode=mode, timeout_ms=10000,
                         options={C.OPT_PROTOCOL: 2})
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     for e in grp:
-        for b, L in enumerate(buckets):
-            synth.fill_x0_device(e.x(0, b).data_ptr(), L, int(offs[b]), e.stream.cuda_stream)
+        for s in range(e.r):
+            for b, L in enumerate(buckets):
+                synth.fill_x0_device(e.x(s, b).data_ptr(), L, int(offs[b]), e.stream.cuda_stream)
     T = 5
     for t in range(T):
         for e in grp:
-            w = e.local_workers[0]
-            for b, L in enumerate(buckets):
-                synth.fill_grad_device(e.g(0, b).data_ptr(), L, int(offs[b]), w, t, e.stream.cuda_stream)
+            for s, w in enumerate(e.local_workers):
+                for b, L in enumerate(buckets):
+                    synth.fill_grad_device(e.g(s, b).data_ptr(), L, int(offs[b]), w, t, e.stream.cuda_stream)
         grp.step_pair(t, 0.1, 0.9)
     grp.synchronize()
     grp.poll()
-    X = np.stack([torch.cat([e.x(0, b) for b in range(len(buckets))]).cpu().numpy() for e in grp])
-    V = np.stack([torch.cat([e.v(0, b) for b in range(len(buckets))]).cpu().numpy() for e in grp])
+    X = np.stack([torch.cat([e.x(s, b) for b in range(len(buckets))]).cpu().numpy() for e in grp for s in range(e.r)])
+    V = np.stack([torch.cat([e.v(s, b) for b in range(len(buckets))]).cpu().numpy() for e in grp for s in range(e.r)])
     assert grp[0].stats(0)["dev_launches"] == T and grp[1].stats(0)["dev_launches"] == T
     grp.close()
-    x = np.tile(synth.x0_host(sum(buckets)), (2, 1))
+    x = np.tile(synth.x0_host(sum(buckets)), (n, 1))
     v = np.zeros_like(x)
-    oracle.run(2, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, mode=mode)
+    oracle.run(n, 2, 42, T, x, v, s_g=synth.SEED_G, lr=0.1, mu=0.9, mode=mode)
     assert np.array_equal(X.view(np.uint32), x.view(np.uint32))
     assert np.array_equal(V.view(np.uint32), v.view(np.uint32))

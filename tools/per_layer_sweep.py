@@ -7,10 +7,12 @@ latencies, one worker per GPU (torch.distributed.run), or R virtual ranks on one
     python -m torch.distributed.run --nproc-per-node 4 tools/per_layer_sweep.py --out gpurun_out/pl.json
     python tools/per_layer_sweep.py --loopback 4 --out gpurun_out/pl_loop.json
 
-Per (m, path, hop): W warm-up iterations, then K timed iterations two ways -- eager (161 launches
-per iteration from Python) and as ONE captured CUDA graph of the same K iterations (the kernels
-and their arguments are identical; the graph removes the host launch overhead) -- max over
-ranks.  The per-hop latency tau is measured in the same run (sesgd_measure_hop, K7 ping-pong
+Per (m, path, hop): W warm-up iterations, then K timed iterations three ways -- eager (161
+launches per iteration from Python), as ONE captured CUDA graph of the same K iterations (the
+kernels and their arguments are identical; the graph removes the host launch overhead; single
+use), and with the device-resident iteration state (SESGD_OPT_DEVICE_ITER): ONE iteration
+captured once and the graph replayed K times, t / groups / call history advancing on the device
+-- max over ranks.  The per-hop latency tau is measured in the same run (sesgd_measure_hop, K7 ping-pong
 through the workspaces), and every row carries the Eq. 2 / Eq. 3 prediction
 (sesgd_latency_model per tensor, summed over the 161 tensors) and the device-counted flag
 stores per iteration.  Paths: ring = K5, the paper's Ring-AllReduce inside each group (2(m-1)
@@ -137,10 +139,30 @@ def time_config(a, n, m, path, hop_ns, buckets, K, W):
     ev1.record(s0)
     r.sync()
     graph_ms = max_over_ranks(ev0.elapsed_time(ev1)) / K
+    # device-resident iteration state (SESGD_OPT_DEVICE_ITER): ONE iteration captured once, the
+    # graph replayed K times -- t, the groups and the call history advance on the device
+    for e in r.engs:
+        e.set_device_iter(True)
+    dgraphs = [e.capture_iteration(0.1, 0.9, None, fused=False) for e in r.engs]
+    for e, g in zip(r.engs, dgraphs):  # one warm-up replay
+        e.replay_iteration(g)
+    r.sync()
+    ev0.record(s0)
+    for _ in range(K):
+        for e, g in zip(r.engs, dgraphs):
+            e.replay_iteration(g)
+    for e in r.engs[1:]:
+        s0.wait_stream(e.default_stream())
+    ev1.record(s0)
+    r.sync()
+    devgraph_ms = max_over_ranks(ev0.elapsed_time(ev1)) / K
+    for e in r.engs:
+        e.set_device_iter(False)
     flags_per_iter = (st1["dev_flag_stores"] - st0["dev_flag_stores"]) / K
     rounds = st1["handshake_rounds"]
     r.close()
     return {"eager_ms_per_iter": eager_ms, "graph_ms_per_iter": graph_ms,
+            "device_iter_graph_ms_per_iter": devgraph_ms,
             "launches_per_iter": nb, "handshake_rounds_per_tensor": rounds,
             "device_flag_stores_per_iter_rank0": flags_per_iter}
 
