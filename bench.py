@@ -64,6 +64,7 @@ def parse():
     p.add_argument("--grid", type=int, default=0, help="CTAs per one-shot launch (0 = auto)")
     p.add_argument("--resident-unroll", type=int, default=0)
     p.add_argument("--protocol", type=int, default=-1, help="two-shot: SESGD_OPT_PROTOCOL (-1 auto)")
+    p.add_argument("--ws-split", type=int, default=0, help="K4W-M: S warps (SESGD_OPT_WS_SPLIT, 0 = default)")
     p.add_argument("--experiment", type=int, default=0,
                    help="SESGD_OPT_EXPERIMENT bits (measurement only: results are wrong)")
     return p.parse_args()
@@ -278,6 +279,7 @@ def engine_options(args, C):
                               (C.OPT_RELEASE_DELAY, args.release_delay), (C.OPT_RELEASE_EVERY, args.release_every),
                               (C.OPT_RELEASE_STAGGER, args.release_stagger),
                               (C.OPT_PAYLOAD_BF16, args.payload_bf16), (C.OPT_EXPERIMENT, args.experiment),
+                              (C.OPT_WS_SPLIT, args.ws_split),
                               ) if v} | {C.OPT_PROTOCOL: args.protocol}
 
 

@@ -175,6 +175,9 @@ extern "C" {
                                     the sync call.  Not with SESGD_OPT_LOCAL_PERIOD > 1.  The
                                     host-side counters of sesgd_get_stats count enqueued calls,
                                     not graph replays (the dev_* counters count launches) */
+#define SESGD_OPT_WS_SPLIT 24       /* K4W-M (protocol 2, several workers per GPU): warps of the
+                                    streaming role S out of 24 (8, 12 -- default -- or 16); the
+                                    fold (R) and gather (F) roles share the rest equally */
 #define SESGD_OPT_EXPERIMENT 20    /* MEASUREMENT ONLY -- results are wrong when set: bit 0 drops
                                     the system-scope fence before the two-shot flag releases,
                                     bit 1 sends the two-shot pushes to this rank's own receive

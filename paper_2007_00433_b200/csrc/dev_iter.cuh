@@ -31,16 +31,6 @@ __device__ __forceinline__ void patch(P2PArgs &s) {
   }
 }
 
-__device__ __forceinline__ void patch(RingArgs &s) {
-  const DevIter *d = s.dev;
-  const DevBucket B = s.dev_buckets[s.bucket];
-  s.call = B.calls;
-  s.parity = int(B.calls & 1);
-  s.seq = d->seq;
-  s.pos = d->ring_pos;
-  for (int q = 0; q < s.m; ++q) s.ring_rank[q] = d->ring_rank[q];
-}
-
 // thread 0 of every CTA, after the CTA's last access to its arguments: the last CTA advances the
 // call history of the launch's buckets, the launch sequence and the chunk-claim base
 __device__ __forceinline__ bool last_cta(DevIter *d) {
@@ -62,8 +52,8 @@ __device__ __forceinline__ void advance(DevIter *d, DevBucket *bk, int bucket, i
 __device__ __forceinline__ void finish(const P2PArgs &s) {
   if (last_cta(s.dev)) advance(s.dev, s.dev_buckets, s.bucket, s.nbuckets, s.seq, s.claim_base + s.dev_claim_inc);
 }
-__device__ __forceinline__ void finish(const RingArgs &s) {
-  if (last_cta(s.dev)) advance(s.dev, s.dev_buckets, s.bucket, s.nbuckets, s.seq, s.dev->claim_base);
+__device__ __forceinline__ void finish(const RingArgs &s, int64_t seq) {
+  if (last_cta(s.dev)) advance(s.dev, s.dev_buckets, s.bucket, s.nbuckets, seq, s.dev->claim_base);
 }
 
 }  // namespace devit

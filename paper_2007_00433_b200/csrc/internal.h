@@ -155,6 +155,7 @@ struct P2PArgs {
   DevBucket *dev_buckets;
   uint64_t dev_claim_inc;
   int64_t kmax;             // epochs per launch (seq_epoch0 = seq * kmax + 1)
+  int ws_split;             // K4W-M: S warps (8, 12, 16; SESGD_OPT_WS_SPLIT)
 };
 // device-side handshake counters (one block per context, cumulative; fire-and-forget atomics)
 enum DevCounter : int {
@@ -266,6 +267,7 @@ struct sesgd_ctx {
   int experiment = 0;       // SESGD_OPT_EXPERIMENT
   int protocol = -1;        // SESGD_OPT_PROTOCOL (two-shot kernel; -1 auto, resolved at layout freeze)
   int cooperative = 0;      // SESGD_OPT_COOPERATIVE
+  int ws_split = 12;        // SESGD_OPT_WS_SPLIT (K4W-M S warps)
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)

@@ -24,12 +24,11 @@ namespace sesgd {
 namespace {
 using namespace wsx;
 
+// 25 warps: P (1), S (ws_s), R (2 groups) and F (2 groups) sharing the other 24 - ws_s equally.
 // S streams every local worker's data (r items per vector); R and F only touch the groups that
-// span GPUs (a fraction of the workers), so S gets most of the warps (measured: with S = 8,
-// R = F = 2 x 4, S was busy for the whole launch and R / F waited on it)
-constexpr int kWarpsP = 1, kWarpsS = 16, kGroupsR = 2, kWarpsR = 2, kGroupsF = 2, kWarpsF = 2;
-constexpr int kThS = kWarpsS * 32, kThR = kWarpsR * 32, kThF = kWarpsF * 32;
-constexpr int kThreadsWSM = (kWarpsP + kWarpsS + kGroupsR * kWarpsR + kGroupsF * kWarpsF) * 32;  // 800
+// span GPUs, so S may take more than a third (SESGD_OPT_WS_SPLIT: ws_s = 8, 12 or 16)
+constexpr int kWarpsP = 1, kGroupsR = 2, kGroupsF = 2, kWarpsRest = 24;
+constexpr int kThreadsWSM = (kWarpsP + kWarpsRest) * 32;  // 800
 constexpr int kChunkWSM = 4096;  // K4's chunking: same slices
 constexpr int kQL = 3, kQX = 4, kQI = 8;
 constexpr int kU = 2;            // vectors in flight per R / F thread
@@ -62,12 +61,18 @@ struct WSM {
   float *ld_ring;  // [kQL][r][3][sub]
   float *x_ring;   // [kQX][r][sub]
   int r, m, sub, upc, cta;
+  int kWarpsS, kWarpsR, kWarpsF, kThS, kThR, kThF;  // the warp split (a.ws_split)
   float inv_m;  // dev::pow2_inverse(m)
   int64_t nunits;
 
   __device__ WSM(const P2PArgs &args, unsigned char *smem) : a(args) {
     r = a.r;
     m = a.m;
+    kWarpsS = a.ws_split;
+    kWarpsR = kWarpsF = (kWarpsRest - kWarpsS) / 4;
+    kThS = kWarpsS * 32;
+    kThR = kWarpsR * 32;
+    kThF = kWarpsF * 32;
     inv_m = dev::pow2_inverse(m);
     sub = sub_of(r);
     cta = int(blockIdx.x) % a.grid;
@@ -488,15 +493,15 @@ __device__ __forceinline__ void k4w_multi_body(const P2PArgs &a, unsigned char *
   if (threadIdx.x == 0) {
     for (int q = 0; q < kQL; ++q) {
       dev::mbar_init(&s.sm->full_ld[q], 1);
-      dev::mbar_init(&s.sm->empty_ld[q], kWarpsS);
+      dev::mbar_init(&s.sm->empty_ld[q], s.kWarpsS);
     }
     for (int q = 0; q < kQX; ++q) {
-      dev::mbar_init(&s.sm->full_x[q], kWarpsS);
-      dev::mbar_init(&s.sm->empty_x[q], kWarpsR);
+      dev::mbar_init(&s.sm->full_x[q], s.kWarpsS);
+      dev::mbar_init(&s.sm->empty_x[q], s.kWarpsR);
     }
     for (int q = 0; q < kQI; ++q) {
       dev::mbar_init(&s.sm->full_id[q], 1);
-      dev::mbar_init(&s.sm->empty_id[q], kWarpsF);
+      dev::mbar_init(&s.sm->empty_id[q], s.kWarpsF);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -518,17 +523,17 @@ __device__ __forceinline__ void k4w_multi_body(const P2PArgs &a, unsigned char *
     __syncthreads();
   }
   const int warp = threadIdx.x >> 5;
-  constexpr int kR0 = kWarpsP + kWarpsS, kF0 = kR0 + kGroupsR * kWarpsR;
+  const int kR0 = kWarpsP + s.kWarpsS, kF0 = kR0 + kGroupsR * s.kWarpsR;
   if (warp < kWarpsP) {
     s.run_p();
   } else if (warp < kR0) {
     s.run_s();
   } else if (warp < kF0) {
     const int w = warp - kR0;
-    s.run_r(w / kWarpsR, (w % kWarpsR) * 32 + (threadIdx.x & 31));
+    s.run_r(w / s.kWarpsR, (w % s.kWarpsR) * 32 + (threadIdx.x & 31));
   } else {
     const int w = warp - kF0;
-    s.run_f(w / kWarpsF, (w % kWarpsF) * 32 + (threadIdx.x & 31));
+    s.run_f(w / s.kWarpsF, (w % s.kWarpsF) * 32 + (threadIdx.x & 31));
   }
   __syncthreads();  // every re-arm of this CTA precedes the release
   if (threadIdx.x == 0) signal_done(a);

@@ -52,12 +52,26 @@ __device__ bool ring_wait(const RingArgs &a, const uint64_t *p, uint64_t target,
   }
 }
 
+// the per-call fields (call history, this member's ring) -- the launch's arguments, or (device
+// iteration state) the context's device memory: read by every thread, no shared-memory copy, so
+// the kernel keeps the resource footprint of the plain one (a loopback virtual rank's grid must fit
+// next to its peers' exactly; a different footprint broke that co-residency)
+struct RingCall {
+  int64_t call, seq;
+  int parity, pos;
+  const int8_t *ring;  // rank of ring position q
+};
+
 template <bool GRAD>
 struct Ring {
   const RingArgs &a;
-  __device__ explicit Ring(const RingArgs &args) : a(args) {}
+  const int64_t call;
+  const int parity, pos;
+  const int8_t *ring;
+  __device__ Ring(const RingArgs &args, const RingCall &c)
+      : a(args), call(c.call), parity(c.parity), pos(c.pos), ring(c.ring) {}
 
-  __device__ __forceinline__ int rank_at(int pos) const { return a.ring_rank[(pos % a.m + a.m) % a.m]; }
+  __device__ __forceinline__ int rank_at(int q) const { return ring[(q % a.m + a.m) % a.m]; }
   __device__ __forceinline__ int64_t slice_lo(int s) const { return int64_t(s) * a.numel / a.m; }
   // this CTA's strip [lo, hi) of slice s (vector-aligned strips; the last CTA takes the rest)
   __device__ __forceinline__ void strip(int s, int64_t &lo, int64_t &hi) const {
@@ -68,11 +82,11 @@ struct Ring {
   }
   __device__ __forceinline__ float *rbuf(int rank, int step) const {  // rank's receive buffer
     return reinterpret_cast<float *>(a.ws[rank] + a.rbuf_off) +
-           (int64_t(a.parity) * a.steps + step) * a.slice_cap;
+           (int64_t(parity) * a.steps + step) * a.slice_cap;
   }
   __device__ __forceinline__ uint64_t *flag(int rank, int step) const {
     return reinterpret_cast<uint64_t *>(a.ws[rank] + a.rflag_off) +
-           ((int64_t(a.parity) * a.nbuckets + a.bucket) * a.steps + step) * a.grid + blockIdx.x;
+           ((int64_t(parity) * a.nbuckets + a.bucket) * a.steps + step) * a.grid + blockIdx.x;
   }
   __device__ __forceinline__ uint64_t *consumed(int rank) const {
     return reinterpret_cast<uint64_t *>(a.ws[rank] + a.rcons_off) + int64_t(a.bucket) * a.grid + blockIdx.x;
@@ -113,20 +127,20 @@ struct Ring {
         while (dev::globaltimer() - t0 < a.hop_delay_ns) {
         }
       }
-      dev::st_release_sys(flag(rank_at(a.pos + 1), step), uint64_t(a.call) + 1);
+      dev::st_release_sys(flag(rank_at(pos + 1), step), uint64_t(call) + 1);
       count(a.counters, kCntFlagStores);
     }
   }
   __device__ __forceinline__ void await(int step) const {
-    if (threadIdx.x == 0) ring_wait(a, flag(a.my_rank, step), uint64_t(a.call) + 1, 2);
+    if (threadIdx.x == 0) ring_wait(a, flag(a.my_rank, step), uint64_t(call) + 1, 2);
     __syncthreads();
   }
 
   __device__ void run() const {
-    const int m = a.m, p = a.pos;
+    const int m = a.m, p = pos;
     const int next = rank_at(p + 1);
-    if (a.call >= 2 && threadIdx.x == 0)  // next member consumed its call-2 buffers
-      ring_wait(a, consumed(next), uint64_t(a.call) - 1, 1);
+    if (call >= 2 && threadIdx.x == 0)  // next member consumed its call-2 buffers
+      ring_wait(a, consumed(next), uint64_t(call) - 1, 1);
     __syncthreads();
     // ---- Scatter-Reduce: m - 1 steps
     for (int t = 0; t < m - 1; ++t) {
@@ -186,7 +200,7 @@ struct Ring {
       apply_mean(lo, hi, in, base);
     }
     __syncthreads();  // every read of my receive buffers is done
-    if (threadIdx.x == 0) dev::st_release_sys(consumed(a.my_rank), uint64_t(a.call) + 1);
+    if (threadIdx.x == 0) dev::st_release_sys(consumed(a.my_rank), uint64_t(call) + 1);
   }
 
   __device__ void local_only() const {
@@ -201,7 +215,7 @@ struct Ring {
 
 template <bool GRAD>
 __global__ void __launch_bounds__(kRingThreads) k5_ring(const __grid_constant__ RingArgs a) {
-  const Ring<GRAD> r(a);
+  const Ring<GRAD> r(a, RingCall{a.call, a.seq, a.parity, a.pos, a.ring_rank});
   if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
   if (a.m == 1)
     r.local_only();
@@ -210,22 +224,23 @@ __global__ void __launch_bounds__(kRingThreads) k5_ring(const __grid_constant__ 
 }
 
 // device-resident iteration state (SESGD_OPT_DEVICE_ITER, dev_iter.cuh)
+__device__ __forceinline__ RingCall ring_call_dev(const RingArgs &a) {
+  const DevIter *d = a.dev;
+  const DevBucket B = a.dev_buckets[a.bucket];
+  return RingCall{B.calls, d->seq, int(B.calls & 1), d->ring_pos, d->ring_rank};
+}
+
 template <bool GRAD>
-__global__ void __launch_bounds__(kRingThreads) k5_ring_dev(const __grid_constant__ RingArgs a) {
-  __shared__ RingArgs sa;
-  if (threadIdx.x == 0) {
-    sa = a;
-    devit::patch(sa);
-  }
-  __syncthreads();
-  const Ring<GRAD> r(sa);
-  if (blockIdx.x == 0 && threadIdx.x == 0) count(sa.counters, kCntLaunches);
-  if (sa.m == 1)
+__global__ void __launch_bounds__(kRingThreads, 5) k5_ring_dev(const __grid_constant__ RingArgs a) {
+  const RingCall c = ring_call_dev(a);
+  const Ring<GRAD> r(a, c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) count(a.counters, kCntLaunches);
+  if (a.m == 1)
     r.local_only();
   else
     r.run();
   __syncthreads();
-  if (threadIdx.x == 0) devit::finish(sa);
+  if (threadIdx.x == 0) devit::finish(a, c.seq);
 }
 
 const void *pick(int mode, bool devi = false) {

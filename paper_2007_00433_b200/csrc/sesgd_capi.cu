@@ -504,6 +504,7 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.protocol = ctx->protocol;
   a.cooperative = ctx->cooperative;
   a.counters = ctx->d_counters;
+  a.ws_split = ctx->ws_split;
   for (int s = 0; s < ctx->n_local; ++s) {
     const int me = ctx->local_workers[s];
     a.my_workers[s] = int8_t(me);
@@ -725,6 +726,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->schedule = int(value);
       return SESGD_OK;
     }
+    case SESGD_OPT_WS_SPLIT:
+      if (value != 8 && value != 12 && value != 16) return fail(ctx, SESGD_EINVAL, "WS split must be 8, 12 or 16");
+      ctx->ws_split = int(value);
+      return SESGD_OK;
     case SESGD_OPT_DEVICE_ITER:
       if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "device iteration must be 0 or 1");
       if (value == ctx->device_iter) return SESGD_OK;

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--rel-delay", type=int, default=0)
     ap.add_argument("--rel-every", type=int, default=0)
     ap.add_argument("--protocol", type=int, default=0)
+    ap.add_argument("--ws-split", type=int, default=0)
     ap.add_argument("--experiment", type=int, default=0)
     ap.add_argument("--out", default="gpurun_out/k3_phases.json")
     a = ap.parse_args()
@@ -57,6 +58,8 @@ def main():
         opts[C.OPT_RELEASE_EVERY] = a.rel_every
     if a.protocol:
         opts[C.OPT_PROTOCOL] = a.protocol
+    if a.ws_split:
+        opts[C.OPT_WS_SPLIT] = a.ws_split
     if a.experiment:
         opts[C.OPT_EXPERIMENT] = a.experiment
     eng = SESGDEngine(a.workers, a.gsize, buckets, rank=rank, world=world, p2p_variant=a.variant,

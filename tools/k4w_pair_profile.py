@@ -28,8 +28,10 @@ from paper_2007_00433_b200.workloads import WORKLOADS  # noqa: E402
 def main():
     iters = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    split = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     buckets = list(WORKLOADS["resnet50"])
-    grp = LoopbackGroup(2, n, 2, buckets, seed=42, options={C.OPT_PROTOCOL: 2})
+    opts = {C.OPT_PROTOCOL: 2} | ({C.OPT_WS_SPLIT: split} if split else {})
+    grp = LoopbackGroup(2, n, 2, buckets, seed=42, options=opts)
     offs = np.concatenate([[0], np.cumsum(buckets)[:-1]]).astype(np.int64)
     for e in grp:
         for s, w in enumerate(e.local_workers):
