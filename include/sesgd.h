@@ -139,16 +139,17 @@ extern "C" {
                                     before sesgd_workspace_bytes (the grid fixes the layout) */
 #define SESGD_OPT_PROTOCOL 21      /* two-shot handshake (set before sesgd_workspace_bytes, identical
                                     on every rank): -1 (default, auto) = 2 with one worker per
-                                    GPU, 1 with several, where supported (the two-shot path with
-                                    fp32 LSU pushes), else 0.
+                                    GPU (K4W) or with 4..8 (K4W-M), 1 with 2 or 3 or more than 8,
+                                    where supported (the two-shot path with fp32 LSU pushes),
+                                    else 0.
                                     0 = epoch flags released with a system-scope fence per batch.
                                     1 = value-carried validity: every receive-slot float holds a
                                     sentinel NaN (0xFFFFFFFF) until the peer's value lands; the
                                     receiver polls the values themselves and re-arms them (no
                                     sender fence, no flag).  A payload equal to the sentinel
                                     travels as the canonical NaN 0x7FFFFFFF.
-                                    2 = 1 in K4W, the warp-specialised kernel (one worker per GPU,
-                                    one CTA per SM).  1 and 2: fp32 LSU pushes only (else
+                                    2 = 1 in K4W / K4W-M, the warp-specialised kernels (one CTA
+                                    per SM; K4W-M: 2..8 workers per GPU).  1 and 2: fp32 LSU pushes only (else
                                     SESGD_ENOTSUP) */
 #define SESGD_OPT_COOPERATIVE 22   /* 1: the persistent multi-GPU grids (K4, K4W, K3, K5) are launched
                                     cooperatively -- the runtime rejects a grid that cannot be
@@ -176,7 +177,7 @@ extern "C" {
                                     host-side counters of sesgd_get_stats count enqueued calls,
                                     not graph replays (the dev_* counters count launches) */
 #define SESGD_OPT_WS_SPLIT 24       /* K4W-M (protocol 2, several workers per GPU): warps of the
-                                    streaming role S out of 24 (8, 12 -- default -- or 16); the
+                                    streaming role S out of 24 (8 -- default, measured best --, 12 or 16); the
                                     fold (R) and gather (F) roles share the rest equally */
 #define SESGD_OPT_EXPERIMENT 20    /* MEASUREMENT ONLY -- results are wrong when set: bit 0 drops
                                     the system-scope fence before the two-shot flag releases,
