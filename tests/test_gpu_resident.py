@@ -444,10 +444,10 @@ def test_device_iteration_graph_resident(n, m, mode, fused):
     for _ in range(T):
         eng.replay_iteration(g)
     torch.cuda.synchronize()
-    st = C.sesgd_device_iter_read(eng.ctx, n, m)
-    assert st["t"] == T - 1  # from "no iteration" (-1), one step per replay
-    assert sorted(st["canon"]) == list(range(n))
-    assert st["canon"] == [int(w) for w in eng.groups(T - 1)[0]]
+    state = C.sesgd_device_iter_read(eng.ctx, n, m)
+    assert state["t"] == T - 1  # from "no iteration" (-1), one step per replay
+    assert sorted(state["canon"]) == list(range(n))
+    assert state["canon"] == [int(w) for w in eng.groups(T - 1)[0]]
     eng.set_device_iter(False)
     for t in (T, T + 1):  # the host continues from the device's t
         for s, w in enumerate(eng.local_workers):
