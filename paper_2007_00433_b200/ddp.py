@@ -77,7 +77,11 @@ class SESGDDataParallel:
                  rank: int = 0, world: int = 1, seed: int = 42, mode: int = C.MODE_PARAM_AVG,
                  first_bucket_bytes: int = 1 << 20, bucket_bytes: int = 25 << 20, process_group=None,
                  overlap: bool = True, static_graph: bool = False,
-                 engine_options: Optional[dict] = None):
+                 engine_options: Optional[dict] = None, engine: Optional[SESGDEngine] = None):
+        """engine: an SESGDEngine to run on instead of creating one -- e.g. a loopback virtual
+        rank of engine.LoopbackGroup (one worker each, bucket sizes as this module's buckets), so
+        several replicas in ONE process on ONE GPU train through the NVLink-path kernels; the
+        caller then gives every replica the same x_0 (there is no process group to broadcast over)"""
         if n != world:
             raise ValueError("SESGDDataParallel runs one worker per process (n == world size)")
         if overlap and (engine_options or {}).get(C.OPT_P2P_VARIANT, 0) >= 1:
@@ -94,9 +98,15 @@ class SESGDDataParallel:
         self.bucket_params = assign_buckets(sizes, first_bucket_bytes, bucket_bytes)
         bucket_sizes = [sum(sizes[i] for i in b) for b in self.bucket_params]
         dev = self.params[0].device
-        self.engine = SESGDEngine(n, group_size, bucket_sizes, seed=seed, mode=mode, rank=rank,
-                                  world=world, device=dev.index, process_group=process_group,
-                                  options=engine_options)
+        if engine is not None:
+            if engine.r != 1 or engine.bucket_sizes != bucket_sizes or engine.n != n or engine.m != group_size:
+                raise ValueError("the given engine must hold one worker with this module's buckets")
+            self.engine = engine
+        else:
+            self.engine = SESGDEngine(n, group_size, bucket_sizes, seed=seed, mode=mode, rank=rank,
+                                      world=world, device=dev.index, process_group=process_group,
+                                      options=engine_options)
+        self._own_engine = engine is None
         self.bucket_of = {}
         with torch.no_grad():
             for b, idxs in enumerate(self.bucket_params):
@@ -111,7 +121,7 @@ class SESGDDataParallel:
                     p.grad = gview  # gradient accumulates into it (in place)
                     self.bucket_of[id(p)] = b
                     off += k
-        if world > 1:
+        if world > 1 and self._own_engine:
             self._broadcast_state(module)
         self.ready = BucketReadiness([len(b) for b in self.bucket_params])
         self.launched_in_backward = 0
@@ -191,4 +201,5 @@ class SESGDDataParallel:
         for h in self._hooks.values():
             h.remove()
         self._hooks = {}
-        self.engine.close()
+        if self._own_engine:
+            self.engine.close()

@@ -84,3 +84,69 @@ def test_ddp_one_gpu_static_graph(tmp_path):
 def test_ddp_four_gpus(tmp_path, m):
     log = _run(tmp_path, 4, m, iters=6)
     assert np.all(log[:, 4] == 3)
+
+
+# ---------------------------------------------------------------- loopback: R replicas on one GPU
+@pytest.mark.parametrize("world,m,mode,static", [(2, 2, 0, 0), (4, 2, 0, 1), (4, 4, 1, 0)])
+def test_ddp_loopback_replicas(world, m, mode, static):
+    """SESGDDataParallel on loopback virtual ranks: `world` model replicas in ONE process on ONE GPU,
+    each on an engine.LoopbackGroup rank (the NVLink-path kernel, K4W), distinct random inits made
+    equal by copying replica 0's fusion buffer (what the process-group broadcast does), the bucket
+    syncs enqueued from gradient hooks during each replica's backward; every step equals the oracle's
+    step replayed on the gradients autograd produced, bit for bit"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.nn.functional as F
+
+    import oracle
+    from paper_2007_00433_b200 import sesgd as C
+    from paper_2007_00433_b200.ddp import SESGDDataParallel
+    from paper_2007_00433_b200.engine import LoopbackGroup
+    from paper_2007_00433_b200.workloads import assign_buckets
+    LR, MU = 0.05, 0.9
+    dev = torch.device("cuda", 0)
+
+    def mlp(seed):
+        torch.manual_seed(seed)
+        return torch.nn.Sequential(torch.nn.Linear(256, 512), torch.nn.ReLU(), torch.nn.Linear(512, 512),
+                                   torch.nn.ReLU(), torch.nn.Linear(512, 10)).to(dev)
+
+    models = [mlp(r) for r in range(world)]
+    sizes = [p.numel() for p in models[0].parameters()]
+    caps = dict(first_bucket_bytes=16 << 10, bucket_bytes=256 << 10)
+    bsizes = [sum(sizes[i] for i in b) for b in assign_buckets(sizes, caps["first_bucket_bytes"], caps["bucket_bytes"])]
+    grp = LoopbackGroup(world, world, m, bsizes, seed=42, mode=mode, timeout_ms=20000)
+    ddps = [SESGDDataParallel(models[r], world, m, lr=LR, momentum=MU, rank=r, world=world, engine=grp[r],
+                              static_graph=bool(static), **caps) for r in range(world)]
+    with torch.no_grad():  # Alg.1 line 1: the same x_0 everywhere (P:197)
+        for r in range(1, world):
+            grp[r].x_flat[0].copy_(grp[0].x_flat[0])
+    torch.cuda.synchronize()
+    for t in range(4):
+        X0 = np.stack([e.x_flat[0].cpu().numpy() for e in grp])
+        V0 = np.stack([e.v_flat[0].cpu().numpy() for e in grp])
+        in_bwd = []
+        for r, (model, ddp) in enumerate(zip(models, ddps)):
+            gen = torch.Generator(device=dev).manual_seed(1000 * t + r)
+            inp = torch.randn(64, 256, device=dev, generator=gen)
+            lab = torch.randint(0, 10, (64,), device=dev, generator=gen)
+            ddp.begin_step(t)
+            F.cross_entropy(model(inp), lab).backward()
+            in_bwd.append(ddp.launched_in_backward)
+        for ddp in ddps:
+            ddp.finish_step()
+        torch.cuda.synchronize()
+        grp.poll()
+        G = np.stack([e.g_flat[0].cpu().numpy() for e in grp])
+        X1 = np.stack([e.x_flat[0].cpu().numpy() for e in grp])
+        V1 = np.stack([e.v_flat[0].cpu().numpy() for e in grp])
+        assert np.abs(G).max() > 0
+        assert all(k >= len(bsizes) - 1 for k in in_bwd), in_bwd  # synced from hooks, inside backward
+        _, canon, _ = oracle.groups(42, t, world, m)
+        x, v = X0.copy(), V0.copy()
+        oracle.step(world, m, canon, x, v, G, LR, MU, mode)
+        assert np.array_equal(x.view(np.uint32), X1.view(np.uint32)), t
+        assert np.array_equal(v.view(np.uint32), V1.view(np.uint32)), t
+    for ddp in ddps:
+        ddp.close()
+    grp.close()
