@@ -10,24 +10,34 @@
 namespace sesgd {
 namespace devit {
 
-// the launch's per-call fields from the state (thread 0; `s` is a shared-memory copy of the args)
-__device__ __forceinline__ void patch(P2PArgs &s) {
-  const DevIter *d = s.dev;
-  const DevBucket B = s.dev_buckets[s.bucket >= 0 ? s.bucket : 0];  // an all-bucket launch: one history
-  s.call = B.calls;
-  s.parity = int(B.calls & 1);
-  s.seq = d->seq;
-  s.prev2_seq = B.calls >= 2 ? B.hist[B.calls & 1] : -1;
-  s.seq_epoch0 = uint64_t(s.seq) * uint64_t(s.kmax) + 1;
-  s.prev2_epoch0 = B.calls >= 2 ? uint64_t(s.prev2_seq) * uint64_t(s.kmax) + 1 : 0;
-  s.claim_base = d->claim_base;
-  for (int i = 0; i < s.n; ++i) {
+// the launch's arguments in shared memory with the per-call fields from the state: every thread of
+// the CTA copies a part (8-byte words: the parameter block is only 8-byte aligned), then patches a part (scalars: thread 0; the schedule
+// tables: one thread per entry); the caller's __syncthreads() publishes the result
+__device__ __forceinline__ void load_patched(const P2PArgs &a, P2PArgs &s) {
+  static_assert(sizeof(P2PArgs) % 8 == 0 && alignof(P2PArgs) == 8, "8-byte copy of the arguments");
+  const int2 *src = reinterpret_cast<const int2 *>(&a);
+  int2 *dst = reinterpret_cast<int2 *>(&s);
+  for (int i = threadIdx.x; i < int(sizeof(P2PArgs) / 8); i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+  const DevIter *d = a.dev;
+  const int i = threadIdx.x;
+  if (i == 0) {
+    const DevBucket B = a.dev_buckets[a.bucket >= 0 ? a.bucket : 0];  // an all-bucket launch: one history
+    s.call = B.calls;
+    s.parity = int(B.calls & 1);
+    s.seq = d->seq;
+    s.prev2_seq = B.calls >= 2 ? B.hist[B.calls & 1] : -1;
+    s.seq_epoch0 = uint64_t(s.seq) * uint64_t(a.kmax) + 1;
+    s.prev2_epoch0 = B.calls >= 2 ? uint64_t(s.prev2_seq) * uint64_t(a.kmax) + 1 : 0;
+    s.claim_base = d->claim_base;
+  }
+  if (i < a.n) {
     s.canon[i] = d->canon[i];
     s.group_of[i] = d->group_of[i];
   }
-  for (int q = 0; q < s.r; ++q) {
-    s.my_pos[q] = d->my_pos[q];
-    s.slot_kind[q] = d->slot_kind[q];
+  if (i < a.r) {
+    s.my_pos[i] = d->my_pos[i];
+    s.slot_kind[i] = d->slot_kind[i];
   }
 }
 

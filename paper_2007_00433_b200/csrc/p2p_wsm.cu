@@ -573,10 +573,7 @@ template <int W, bool GRAD>
 __global__ void __launch_bounds__(kThreadsWSM, 1) k4w_multi_dev(const __grid_constant__ P2PArgs a) {
   extern __shared__ __align__(128) unsigned char dsmem[];
   __shared__ P2PArgs sa;
-  if (threadIdx.x == 0) {
-    sa = a;
-    devit::patch(sa);
-  }
+  devit::load_patched(a, sa);
   __syncthreads();
   k4w_multi_body<W, GRAD>(sa, dsmem);
   if (threadIdx.x == 0) devit::finish(sa);
