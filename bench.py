@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--resident-unroll", type=int, default=0)
     p.add_argument("--protocol", type=int, default=-1, help="two-shot: SESGD_OPT_PROTOCOL (-1 auto)")
     p.add_argument("--ws-split", type=int, default=0, help="K4W-M: S warps (SESGD_OPT_WS_SPLIT, 0 = default)")
+    p.add_argument("--no-hybrid", action="store_true", help="K4W-M also streams the all-local groups (SESGD_OPT_WSM_HYBRID 0)")
     p.add_argument("--experiment", type=int, default=0,
                    help="SESGD_OPT_EXPERIMENT bits (measurement only: results are wrong)")
     return p.parse_args()
@@ -149,6 +150,12 @@ def pcie_probe():
     """Measured pinned-host copy rates (tools/pcie_probe.py) committed under profiles/, or None."""
     path = os.path.join(ROOT, "profiles", "r01_pcie_probe_g1.json")
     return json.load(open(path)) if os.path.exists(path) else None
+
+
+def local_groups_on_rank(perm, m, r, rank):
+    """groups of the canonical partition `perm` whose m members all live on `rank` (worker w on
+    rank w // r)"""
+    return sum(1 for j in range(len(perm) // m) if all(int(w) // r == rank for w in perm[j * m:(j + 1) * m]))
 
 
 def nvlink_algo_bytes(perm, m, r, world, L):
@@ -280,7 +287,7 @@ def engine_options(args, C):
                               (C.OPT_RELEASE_STAGGER, args.release_stagger),
                               (C.OPT_PAYLOAD_BF16, args.payload_bf16), (C.OPT_EXPERIMENT, args.experiment),
                               (C.OPT_WS_SPLIT, args.ws_split),
-                              ) if v} | {C.OPT_PROTOCOL: args.protocol}
+                              ) if v} | {C.OPT_PROTOCOL: args.protocol} | ({C.OPT_WSM_HYBRID: 0} if args.no_hybrid else {})
 
 
 class Dist:
@@ -397,7 +404,9 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
         proto = args.protocol if args.protocol >= 0 else (2 if r == 1 or 4 <= r <= 8 else 1)  # auto (sesgd_capi.cu)
         if args.push_tma or args.payload_bf16:
             proto = 0 if args.protocol < 0 else proto
-        k4w = "k4w_twoshot" if r == 1 else "k4w_multi"
+        # several workers per GPU: by default K6 updates the all-local groups first, then K4W-M
+        # (SESGD_OPT_WSM_HYBRID); the per-launch events cover both kernels
+        k4w = "k4w_twoshot" if r == 1 else ("k4w_multi" if args.no_hybrid else "k6_resident+k4w_multi")
         kernel = {"twoshot": k4w if proto == 2 else "k4_twoshot",
                   "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the
@@ -420,6 +429,11 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
         roof.update({"hbm_achieved": achieved_hbm, "nvlink_algo_bytes_per_step": nvl_bytes,
                      "t_roof_us": max(t_hbm, t_nvl) * 1e6, "kernel": kernel})
     roof["traffic"] = traffic_for(kernel, f"{workload}_n{n}_m{m}_g{world}")
+    if kernel == "k6_resident+k4w_multi":  # the K6 launch happens only in iterations with an all-local group
+        extra_k6 = sum(1 for t in range(t_next - K, t_next) if local_groups_on_rank(eng.groups(t)[0], m, r, rank) > 0)
+        gpu_launches_extra = extra_k6
+    else:
+        gpu_launches_extra = 0
 
     # ---- e2e through the C-ABI host-buffer call (H2D of g, D2H of x inside the timed region)
     e2e = None
@@ -470,7 +484,7 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
         "value": value, "ms_per_step": ms_step, "steps": K, "warmup": W,
         "iters_per_s": 1e3 / ms_step, "gbs_per_gpu": value / world,
         "kernel_ms_per_step": {"p50": kern_p50, "p90": kern_p90},
-        "roofline": roof, "e2e": e2e, "gpu_launches": K * kernels_per_step,
+        "roofline": roof, "e2e": e2e, "gpu_launches": K * kernels_per_step + gpu_launches_extra,
         "kernel_rounds_per_bucket": stats[0]["handshake_rounds"],
         "consistency": {"after_iterations": t_next, "sum_sq_dev_from_mean": css,
                         "rms_dev": (css / (n * L)) ** 0.5, "max_abs_dev": cmx,

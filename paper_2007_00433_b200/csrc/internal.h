@@ -156,6 +156,7 @@ struct P2PArgs {
   uint64_t dev_claim_inc;
   int64_t kmax;             // epochs per launch (seq_epoch0 = seq * kmax + 1)
   int ws_split;             // K4W-M: S warps (8, 12, 16; SESGD_OPT_WS_SPLIT)
+  int wsm_spanning_only;    // K4W-M: skip the all-local groups (a K6 launch updates them)
 };
 // device-side handshake counters (one block per context, cumulative; fire-and-forget atomics)
 enum DevCounter : int {
@@ -268,6 +269,7 @@ struct sesgd_ctx {
   int protocol = -1;        // SESGD_OPT_PROTOCOL (two-shot kernel; -1 auto, resolved at layout freeze)
   int cooperative = 0;      // SESGD_OPT_COOPERATIVE
   int ws_split = 8;         // SESGD_OPT_WS_SPLIT (K4W-M S warps)
+  int wsm_hybrid = 1;       // SESGD_OPT_WSM_HYBRID: all-local groups through K6, the rest K4W-M
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)

@@ -160,6 +160,10 @@ struct WSM {
     mbar_arrive(&sm->full_id[qi]);
   }
 
+  // spanning_only: the all-local groups are updated by a K6 launch before this one (the hybrid
+  // launch of sesgd_capi.cu), so their slots are neither loaded nor streamed here
+  __device__ __forceinline__ bool skip(int s) const { return a.wsm_spanning_only && a.slot_kind[s] != 0; }
+
   // ---------------------------------------------------------------- P
   __device__ void run_p() const {
     if ((threadIdx.x & 31) != 0) return;
@@ -183,10 +187,12 @@ struct WSM {
       }
       const uint32_t bytes = uint32_t((x.phi - x.plo) / 4) * 16;  // whole float4s; tails via S
       uint32_t tx = 0;
-      for (int s = 0; s < r; ++s) tx += bytes * ((GRAD && a.slot_kind[s] == 0) ? 1u : 3u);
+      for (int s = 0; s < r; ++s)
+        if (!skip(s)) tx += bytes * ((GRAD && a.slot_kind[s] == 0) ? 1u : 3u);
       dev::mbar_arrive_expect_tx(&sm->full_ld[q], tx);
       if (bytes) {
         for (int s = 0; s < r; ++s) {
+          if (skip(s)) continue;
           const int64_t off = x.e0 + x.plo;
           dev::bulk_g2s(stage(q, s, 0), a.bg[x.b * r + s] + off, bytes, &sm->full_ld[q]);
           if (!(GRAD && a.slot_kind[s] == 0)) {
@@ -240,7 +246,7 @@ struct WSM {
       const int64_t nvec = (x.phi - x.plo + W - 1) / W;
       for (int s = 0; s < r; ++s) {
         const int kind = a.slot_kind[s];
-        if (kind == 2) continue;  // updated with its group's first member
+        if (kind == 2 || skip(s)) continue;  // updated with its group's first member / by K6
         const int8_t *G = group(a.my_workers[s]);
         for (int64_t vi = t; vi < nvec; vi += kThS) {
           const int64_t o = x.plo + vi * W;

@@ -439,6 +439,68 @@ int upload_tables(sesgd_ctx *ctx) {
   return SESGD_OK;
 }
 
+// Hybrid K4W-M launch (SESGD_OPT_WSM_HYBRID, several workers per GPU, host iterations): the groups
+// whose members are all on this GPU are updated by K6 first -- plain 128-bit streaming at ~0.96
+// of HBM, where K4W-M's TMA ring drained by its S warps reaches ~4 TB/s -- and the
+// K4W-M launch that follows streams only the workers whose group spans GPUs.  Same arithmetic
+// and fold order in both kernels, so the same bits.
+int launch_local_groups(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStream_t st) {
+  sesgd::ResidentArgs a{};
+  int rows = 0;
+  for (int s = 0; s < ctx->n_local; ++s) {
+    const int me = ctx->local_workers[s];
+    const int *G = ctx->canon + ctx->group_of[me] * ctx->m;
+    bool all_local = true;
+    for (int p = 0; p < ctx->m; ++p) all_local = all_local && ctx->worker_rank[G[p]] == ctx->rank;
+    if (!all_local || G[0] != me) continue;
+    for (int p = 0; p < ctx->m; ++p) a.member_slot[rows * ctx->m + p] = int8_t(ctx->worker_slot[G[p]]);
+    ++rows;
+  }
+  if (rows == 0) return SESGD_OK;
+  a.lr = lr;
+  a.mu = momentum;
+  a.wd = ctx->weight_decay;
+  a.m = ctx->m;
+  a.k = rows;
+  a.n_local = ctx->n_local;
+  bool vec = true;
+  int64_t biggest = 0;
+  if (bucket >= 0) {
+    const sesgd_bucket &b = ctx->buckets[bucket];
+    a.x = b.d_x;
+    a.v = b.d_v;
+    a.g = b.d_g;
+    a.numel = b.numel;
+    vec = b.vec;
+    biggest = b.numel;
+  } else {
+    if (!ctx->d_numels) {
+      std::vector<int64_t> numels(ctx->buckets.size());
+      for (size_t b = 0; b < numels.size(); ++b) numels[b] = ctx->buckets[b].numel;
+      cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&ctx->d_numels), std::max<size_t>(numels.size(), 1) * 8);
+      if (e == cudaSuccess) e = cudaMemcpy(ctx->d_numels, numels.data(), numels.size() * 8, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "bucket sizes table");
+    }
+    for (auto &b : ctx->buckets) {
+      vec = vec && b.vec;
+      biggest = std::max(biggest, b.numel);
+    }
+    a.nb = int(ctx->buckets.size());
+    a.bx = ctx->d_bx;  // the multi-GPU [NB * r] pointer tables (upload_tables)
+    a.bv = ctx->d_bv;
+    a.bg = ctx->d_bg;
+    a.numels = ctx->d_numels;
+  }
+  const int threads = sesgd::resident_block_threads();
+  const int target = ctx->sm_count * sesgd::resident_occupancy(ctx->mode, vec, ctx->m, ctx->resident_unroll);
+  int gx = (target + rows - 1) / rows;
+  const int64_t need = ((vec ? biggest / 4 : biggest) + threads - 1) / threads;
+  if (need < gx) gx = int(need > 0 ? need : 1);
+  cudaError_t e = sesgd::launch_resident(a, ctx->mode, vec, gx, ctx->resident_unroll, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "launch resident kernel (all-local groups)");
+  return SESGD_OK;
+}
+
 // One one-shot launch over bucket `bucket` (>= 0) or over every bucket (-1, all buckets
 // share the same call history).  Host bookkeeping of calls / launch sequence follows.
 // dry != nullptr: build the arguments into *dry and do the bookkeeping without launching (the
@@ -509,6 +571,9 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
   a.cooperative = ctx->cooperative;
   a.counters = ctx->d_counters;
   a.ws_split = ctx->ws_split;
+  const bool hybrid = twoshot && !nvls && ctx->protocol == 2 && ctx->n_local > 1 && ctx->wsm_hybrid &&
+                      !ctx->device_iter && !dry;
+  a.wsm_spanning_only = hybrid ? 1 : 0;
   for (int s = 0; s < ctx->n_local; ++s) {
     const int me = ctx->local_workers[s];
     a.my_workers[s] = int8_t(me);
@@ -549,6 +614,10 @@ int launch_oneshot(sesgd_ctx *ctx, int bucket, float lr, float momentum, cudaStr
     *dry = a;
   } else {
     mark_start(ctx, st);
+    if (hybrid) {
+      const int rc = launch_local_groups(ctx, bucket, lr, momentum, st);
+      if (rc != SESGD_OK) return rc;
+    }
     cudaError_t e = (twoshot && ctx->protocol == 2 && !nvls)
                         ? (ctx->n_local == 1 ? sesgd::launch_p2p_ws(a, ctx->mode, vec, st)
                                              : sesgd::launch_p2p_wsm(a, ctx->mode, vec, st))
@@ -730,6 +799,10 @@ int sesgd_set_option(sesgd_ctx *ctx, int32_t option, int64_t value) {
       ctx->schedule = int(value);
       return SESGD_OK;
     }
+    case SESGD_OPT_WSM_HYBRID:
+      if (value != 0 && value != 1) return fail(ctx, SESGD_EINVAL, "WSM hybrid must be 0 or 1");
+      ctx->wsm_hybrid = int(value);
+      return SESGD_OK;
     case SESGD_OPT_WS_SPLIT:
       if (value != 8 && value != 12 && value != 16) return fail(ctx, SESGD_EINVAL, "WS split must be 8, 12 or 16");
       ctx->ws_split = int(value);

@@ -25,7 +25,7 @@ OPT_PROFILE, OPT_COMM_BATCH, OPT_FOLD_LAG, OPT_RESIDENT_UNROLL, OPT_PUSH_TMA = 8
 OPT_RELEASE_DELAY, OPT_RELEASE_EVERY, OPT_LOCAL_PERIOD, OPT_SCHEDULE = 13, 14, 15, 16
 SCHEDULE_RANDOM, SCHEDULE_DIMENSION_EXCHANGE = 0, 1
 OPT_RELEASE_STAGGER, OPT_PAYLOAD_BF16, OPT_SM_BUDGET = 17, 18, 19
-OPT_EXPERIMENT, OPT_PROTOCOL, OPT_COOPERATIVE, OPT_DEVICE_ITER, OPT_WS_SPLIT = 20, 21, 22, 23, 24
+OPT_EXPERIMENT, OPT_PROTOCOL, OPT_COOPERATIVE, OPT_DEVICE_ITER, OPT_WS_SPLIT, OPT_WSM_HYBRID = 20, 21, 22, 23, 24, 25
 ITER_NEXT = -1
 
 # every symbol include/sesgd.h declares (checked by tests/test_boundary.py)
