@@ -65,7 +65,7 @@ def parse():
     p.add_argument("--resident-unroll", type=int, default=0)
     p.add_argument("--protocol", type=int, default=-1, help="two-shot: SESGD_OPT_PROTOCOL (-1 auto)")
     p.add_argument("--ws-split", type=int, default=0, help="K4W-M: S warps (SESGD_OPT_WS_SPLIT, 0 = default)")
-    p.add_argument("--no-hybrid", action="store_true", help="K4W-M also streams the all-local groups (SESGD_OPT_WSM_HYBRID 0)")
+    p.add_argument("--hybrid", action="store_true", help="K6 for the all-local groups, then K4W-M (SESGD_OPT_WSM_HYBRID 1)")
     p.add_argument("--experiment", type=int, default=0,
                    help="SESGD_OPT_EXPERIMENT bits (measurement only: results are wrong)")
     return p.parse_args()
@@ -287,7 +287,7 @@ def engine_options(args, C):
                               (C.OPT_RELEASE_STAGGER, args.release_stagger),
                               (C.OPT_PAYLOAD_BF16, args.payload_bf16), (C.OPT_EXPERIMENT, args.experiment),
                               (C.OPT_WS_SPLIT, args.ws_split),
-                              ) if v} | {C.OPT_PROTOCOL: args.protocol} | ({C.OPT_WSM_HYBRID: 0} if args.no_hybrid else {})
+                              ) if v} | {C.OPT_PROTOCOL: args.protocol} | ({C.OPT_WSM_HYBRID: 1} if args.hybrid else {})
 
 
 class Dist:
@@ -404,9 +404,9 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
         proto = args.protocol if args.protocol >= 0 else (2 if r == 1 or 4 <= r <= 8 else 1)  # auto (sesgd_capi.cu)
         if args.push_tma or args.payload_bf16:
             proto = 0 if args.protocol < 0 else proto
-        # several workers per GPU: by default K6 updates the all-local groups first, then K4W-M
+        # several workers per GPU; --hybrid: K6 updates the all-local groups first, then K4W-M
         # (SESGD_OPT_WSM_HYBRID); the per-launch events cover both kernels
-        k4w = "k4w_twoshot" if r == 1 else ("k4w_multi" if args.no_hybrid else "k6_resident+k4w_multi")
+        k4w = "k4w_twoshot" if r == 1 else ("k6_resident+k4w_multi" if args.hybrid else "k4w_multi")
         kernel = {"twoshot": k4w if proto == 2 else "k4_twoshot",
                   "ring": "k5_ring", "nvls": "k4_nvls"}.get(eff_path, "k3_push")
         # NVLink: bandwidth-optimal group-allreduce bytes per GPU per direction, from the

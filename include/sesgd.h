@@ -179,11 +179,14 @@ extern "C" {
 #define SESGD_OPT_WS_SPLIT 24       /* K4W-M (protocol 2, several workers per GPU): warps of the
                                     streaming role S out of 24 (8 -- default, measured best --, 12 or 16); the
                                     fold (R) and gather (F) roles share the rest equally */
-#define SESGD_OPT_WSM_HYBRID 25     /* K4W-M with host iterations: 1 (default) = the groups whose
-                                    members all live on this GPU are updated by the 1-GPU kernel
-                                    K6 first (HBM-efficient streaming), then K4W-M streams only
-                                    the workers whose group spans GPUs; 0 = K4W-M does both.
-                                    Same bits either way.  Device-resident iterations use 0 */
+#define SESGD_OPT_WSM_HYBRID 25     /* K4W-M with host iterations: 1 = the groups whose members all
+                                    live on this GPU are updated by the 1-GPU kernel K6 first,
+                                    then K4W-M streams only the workers whose group spans GPUs;
+                                    0 (default) = K4W-M does both.  Same bits either way.
+                                    Measured slower (cfg 2, 2 GPUs: 0.71 vs 0.66 ms; the two
+                                    kernels serialise and ranks with more all-local groups start
+                                    the exchange later), kept for the record.  Device-resident
+                                    iterations always use 0 */
 #define SESGD_OPT_EXPERIMENT 20    /* MEASUREMENT ONLY -- results are wrong when set: bit 0 drops
                                     the system-scope fence before the two-shot flag releases,
                                     bit 1 sends the two-shot pushes to this rank's own receive

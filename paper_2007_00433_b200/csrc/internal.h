@@ -269,7 +269,7 @@ struct sesgd_ctx {
   int protocol = -1;        // SESGD_OPT_PROTOCOL (two-shot kernel; -1 auto, resolved at layout freeze)
   int cooperative = 0;      // SESGD_OPT_COOPERATIVE
   int ws_split = 8;         // SESGD_OPT_WS_SPLIT (K4W-M S warps)
-  int wsm_hybrid = 1;       // SESGD_OPT_WSM_HYBRID: all-local groups through K6, the rest K4W-M
+  int wsm_hybrid = 0;       // SESGD_OPT_WSM_HYBRID: all-local groups through K6, the rest K4W-M
   int schedule = 0;         // SESGD_OPT_SCHEDULE: 0 uniform random (R1), 1 dimension exchange
   float weight_decay = 0.f; // sesgd_set_weight_decay
   // sesgd_sync_all_host: copy streams and per-bucket events (created on first use)

@@ -22,7 +22,8 @@ def _options(a):
     return {k: v for k, v in ((C.OPT_COMM_BATCH, a.batch), (C.OPT_FOLD_LAG, a.lag),
                               (C.OPT_PUSH_TMA, a.tma), (C.OPT_LOCAL_PERIOD, a.period),
                               (C.OPT_SCHEDULE, a.schedule), (C.OPT_PAYLOAD_BF16, a.bf16),
-                              (C.OPT_RELEASE_EVERY, a.release_every)) if v} | {C.OPT_PROTOCOL: a.protocol}
+                              (C.OPT_RELEASE_EVERY, a.release_every), (C.OPT_WSM_HYBRID, a.hybrid)) if v} | {
+        C.OPT_PROTOCOL: a.protocol}
 
 
 def _padded(idx, buckets, offsets):
@@ -145,6 +146,7 @@ def main():
     p.add_argument("--release-every", type=int, default=0)
     p.add_argument("--loopback", type=int, default=0)
     p.add_argument("--devit", type=int, default=0)  # device iteration state: 1 eager, 2 graph, 3 mixed
+    p.add_argument("--hybrid", type=int, default=0)  # SESGD_OPT_WSM_HYBRID
     p.add_argument("--coords", default="")
     p.add_argument("--out", required=True)
     a = p.parse_args()

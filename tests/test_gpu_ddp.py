@@ -112,6 +112,12 @@ def test_ddp_loopback_replicas(world, m, mode, static):
                                    torch.nn.ReLU(), torch.nn.Linear(512, 10)).to(dev)
 
     models = [mlp(r) for r in range(world)]
+    # load every forward / backward kernel once before any virtual rank's exchange kernel spins:
+    # with CUDA's lazy module loading, a first-use load behind a spinning grid on the same GPU can
+    # stall until the peer timeout (one process per GPU never has that)
+    warm = mlp(99)
+    F.cross_entropy(warm(torch.randn(64, 256, device=dev)), torch.randint(0, 10, (64,), device=dev)).backward()
+    torch.cuda.synchronize()
     sizes = [p.numel() for p in models[0].parameters()]
     caps = dict(first_bucket_bytes=16 << 10, bucket_bytes=256 << 10)
     bsizes = [sum(sizes[i] for i in b) for b in assign_buckets(sizes, caps["first_bucket_bytes"], caps["bucket_bytes"])]

@@ -43,7 +43,7 @@ def _free_port():
 
 def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, fused=1, batch=0,
             lag=0, path=0, hop_ns=0, tma=0, period=1, final_avg=0, schedule=0, consensus=0, wd=0.0,
-            bf16=0, coords=None, protocol=-1, release_every=0, devit=0):
+            bf16=0, coords=None, protocol=-1, release_every=0, devit=0, hybrid=0):
     """`gpus` ranks: processes on as many GPUs (nvlink) or virtual ranks on cuda:0 (loopback)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -66,7 +66,7 @@ def _launch(tmp_path, gpus, n, m, T, buckets, mode=0, t0=0, grid=0, variant=-1, 
                "--batch", str(batch), "--lag", str(lag), "--path", str(path), "--hop-ns", str(hop_ns),
                "--tma", str(tma), "--period", str(period), "--final-avg", str(final_avg),
                "--schedule", str(schedule), "--consensus", str(consensus), "--wd", repr(wd),
-               "--bf16", str(bf16), "--protocol", str(protocol), "--release-every", str(release_every), "--devit", str(devit), "--loopback", str(gpus if loop else 0), *extra,
+               "--bf16", str(bf16), "--protocol", str(protocol), "--release-every", str(release_every), "--devit", str(devit), "--hybrid", str(hybrid), "--loopback", str(gpus if loop else 0), *extra,
                "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
@@ -633,6 +633,16 @@ def test_k4w_multi_resnet50_bench_shape(tmp_path, gpus):
     coords = _sample(buckets)
     X, V = _launch(tmp_path, gpus, 8, 2, 100, buckets, coords=coords, path=4, protocol=2)
     x, v = _oracle(8, 2, sum(buckets), 100, 0, coords=coords)
+    _compare(X, x)
+    _compare(V, v)
+
+
+@pytest.mark.parametrize("n,m,mode,fused", [(8, 2, 0, 1), (8, 4, 1, 1), (16, 2, 0, 0)])
+def test_k4w_multi_hybrid(tmp_path, n, m, mode, fused):
+    """SESGD_OPT_WSM_HYBRID: K6 updates the all-local groups, K4W-M the spanning ones -- same bits"""
+    buckets = [60001, 4097, 3]
+    X, V = _launch(tmp_path, 2, n, m, 6, buckets, mode, fused=fused, path=4, protocol=2, hybrid=1)
+    x, v = _oracle(n, m, sum(buckets), 6, mode)
     _compare(X, x)
     _compare(V, v)
 
