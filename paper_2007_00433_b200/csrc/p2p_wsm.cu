@@ -216,113 +216,6 @@ struct WSM {
     }
   }
 
-  // one S item: vector o of local slot s (kind 1: its whole all-local group; kind 0: this worker's
-  // contribution to the reduce-scatter of slice x.j)
-  __device__ __forceinline__ void s_item(int q, int qx, const Unit &x, const UnitPtr &pt, int s, int kind, int64_t o,
-                                         int nv, int64_t e, int64_t len4) const {
-    const int8_t *G = group(a.my_workers[s]);
-    if (kind == 1) {  // every member here: the 1-GPU kernel's arithmetic in registers
-      float acc[W];
-#pragma unroll 2
-      for (int rr = 0; rr < m; ++rr) {  // ascending member id (unrolled: two members' loads in flight)
-        const int sl = a.worker_slot[G[rr]];
-        float gr[W];
-        get(q, sl, 0, x, o, nv, len4, gr);
-        if constexpr (!GRAD) {
-          float v[W], xx[W];
-          get(q, sl, 1, x, o, nv, len4, v);
-          get(q, sl, 2, x, o, nv, len4, xx);
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            v[w] = dev::momentum(a.mu, v[w], dev::decay(gr[w], a.wd, xx[w]));
-            const float xh = dev::sgd(xx[w], a.lr, v[w]);
-            acc[w] = (rr == 0) ? xh : __fadd_rn(acc[w], xh);
-          }
-          stm<W>(pt.bv[sl] + e, v, nv);
-        } else {
-#pragma unroll
-          for (int w = 0; w < W; ++w) acc[w] = (rr == 0) ? gr[w] : __fadd_rn(acc[w], gr[w]);
-        }
-      }
-#pragma unroll
-      for (int w = 0; w < W; ++w) acc[w] = dev::mean_rt(acc[w], m, inv_m);
-      for (int rr = 0; rr < m; ++rr) {
-        const int sl = a.worker_slot[G[rr]];
-        if constexpr (!GRAD) {
-          stm<W>(pt.bx[sl] + e, acc, nv);
-        } else {
-          float v[W], xx[W];
-          get(q, sl, 1, x, o, nv, len4, v);
-          get(q, sl, 2, x, o, nv, len4, xx);
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            v[w] = dev::momentum(a.mu, v[w], dev::decay(acc[w], a.wd, xx[w]));
-            xx[w] = dev::sgd(xx[w], a.lr, v[w]);
-          }
-          stm<W>(pt.bv[sl] + e, v, nv);
-          stm<W>(pt.bx[sl] + e, xx, nv);
-        }
-      }
-    } else {  // a group with remote members: reduce-scatter my contribution of slice j
-      float val[W];
-      get(q, s, 0, x, o, nv, len4, val);
-      if constexpr (!GRAD) {
-        float v[W], xx[W];
-        get(q, s, 1, x, o, nv, len4, v);
-        get(q, s, 2, x, o, nv, len4, xx);
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          v[w] = dev::momentum(a.mu, v[w], dev::decay(val[w], a.wd, xx[w]));
-          val[w] = dev::sgd(xx[w], a.lr, v[w]);  // x_hat
-        }
-        stm<W>(pt.bv[s] + e, v, nv);
-      }
-      const int w = G[x.j];  // the slice's owner
-      if (local(w)) {
-        float *dst = xent(qx, s) + (o - x.plo);
-        SESGD_CHECK(o - x.plo + nv <= sub);
-#pragma unroll
-        for (int q2 = 0; q2 < W; ++q2)
-          if (q2 < nv) dst[q2] = val[q2];
-      } else {
-        push<W>(recv(w, a.my_pos[s]) + x.soff + e, val, nv);
-      }
-    }
-  }
-
-  // two spanning slots sa, sb (kind 0), one full vector each, PARAM mode, from the TMA stage
-  __device__ __forceinline__ void span_pair(int q, int qx, const Unit &x, const UnitPtr &pt, int sa, int sb, int64_t o,
-                                            int64_t e) const {
-    const float4 ga = *reinterpret_cast<const float4 *>(stage(q, sa, 0) + (o - x.plo));
-    const float4 gb = *reinterpret_cast<const float4 *>(stage(q, sb, 0) + (o - x.plo));
-    const float4 va = *reinterpret_cast<const float4 *>(stage(q, sa, 1) + (o - x.plo));
-    const float4 vb = *reinterpret_cast<const float4 *>(stage(q, sb, 1) + (o - x.plo));
-    const float4 xa = *reinterpret_cast<const float4 *>(stage(q, sa, 2) + (o - x.plo));
-    const float4 xb = *reinterpret_cast<const float4 *>(stage(q, sb, 2) + (o - x.plo));
-    float g2[2][4] = {{ga.x, ga.y, ga.z, ga.w}, {gb.x, gb.y, gb.z, gb.w}};
-    float v2[2][4] = {{va.x, va.y, va.z, va.w}, {vb.x, vb.y, vb.z, vb.w}};
-    float x2[2][4] = {{xa.x, xa.y, xa.z, xa.w}, {xb.x, xb.y, xb.z, xb.w}};
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        v2[h][w] = dev::momentum(a.mu, v2[h][w], dev::decay(g2[h][w], a.wd, x2[h][w]));
-        x2[h][w] = dev::sgd(x2[h][w], a.lr, v2[h][w]);  // x_hat
-      }
-    const int sl[2] = {sa, sb};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      dev::st4(pt.bv[sl[h]] + e, make_float4(v2[h][0], v2[h][1], v2[h][2], v2[h][3]));
-      const int w = group(a.my_workers[sl[h]])[x.j];  // the slice's owner
-      if (local(w)) {
-        *reinterpret_cast<float4 *>(xent(qx, sl[h]) + (o - x.plo)) = make_float4(x2[h][0], x2[h][1], x2[h][2], x2[h][3]);
-      } else {
-        float val[4] = {x2[h][0], x2[h][1], x2[h][2], x2[h][3]};
-        push<4>(recv(w, a.my_pos[sl[h]]) + x.soff + e, val, 4);
-      }
-    }
-  }
-
   // ---------------------------------------------------------------- S
   __device__ void run_s() const {
     const int t = threadIdx.x - kWarpsP * 32;
@@ -351,30 +244,81 @@ struct WSM {
       const UnitPtr &pt = sm->uptr[k % kQI];  // P rewrites it only after this step (see post_id)
       const int64_t len4 = x.plo + ((x.phi - x.plo) & ~int64_t(3));
       const int64_t nvec = (x.phi - x.plo + W - 1) / W;
-      // vector-major: for each of this thread's vectors, every local slot; two spanning slots (kind
-      // 0) with full vectors are processed together -- their loads and arithmetic interleave, which
-      // is the latency hiding 8 S warps (2 per scheduler) cannot provide on their own
-      for (int64_t vi = t; vi < nvec; vi += kThS) {
-        const int64_t o = x.plo + vi * W;
-        const int nv = int(min(int64_t(W), x.phi - o));
-        const int64_t e = x.e0 + o;
-        const bool full = kTma && !GRAD && o + W <= len4;
-        int pend = -1;  // a spanning slot waiting for a partner
-        for (int s = 0; s < r; ++s) {
-          const int kind = a.slot_kind[s];
-          if (kind == 2 || skip(s)) continue;  // updated with its group's first member / by K6
-          if (full && kind == 0) {
-            if (pend < 0) {
-              pend = s;
-            } else {
-              span_pair(q, qx, x, pt, pend, s, o, e);
-              pend = -1;
+      for (int s = 0; s < r; ++s) {
+        const int kind = a.slot_kind[s];
+        if (kind == 2 || skip(s)) continue;  // updated with its group's first member / by K6
+        const int8_t *G = group(a.my_workers[s]);
+        for (int64_t vi = t; vi < nvec; vi += kThS) {
+          const int64_t o = x.plo + vi * W;
+          const int nv = int(min(int64_t(W), x.phi - o));
+          const int64_t e = x.e0 + o;
+          if (kind == 1) {  // every member here: the 1-GPU kernel's arithmetic in registers
+            float acc[W];
+            for (int rr = 0; rr < m; ++rr) {  // ascending member id
+              const int sl = a.worker_slot[G[rr]];
+              float gr[W];
+              get(q, sl, 0, x, o, nv, len4, gr);
+              if constexpr (!GRAD) {
+                float v[W], xx[W];
+                get(q, sl, 1, x, o, nv, len4, v);
+                get(q, sl, 2, x, o, nv, len4, xx);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                  v[w] = dev::momentum(a.mu, v[w], dev::decay(gr[w], a.wd, xx[w]));
+                  const float xh = dev::sgd(xx[w], a.lr, v[w]);
+                  acc[w] = (rr == 0) ? xh : __fadd_rn(acc[w], xh);
+                }
+                stm<W>(pt.bv[sl] + e, v, nv);
+              } else {
+#pragma unroll
+                for (int w = 0; w < W; ++w) acc[w] = (rr == 0) ? gr[w] : __fadd_rn(acc[w], gr[w]);
+              }
             }
-            continue;
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = dev::mean_rt(acc[w], m, inv_m);
+            for (int rr = 0; rr < m; ++rr) {
+              const int sl = a.worker_slot[G[rr]];
+              if constexpr (!GRAD) {
+                stm<W>(pt.bx[sl] + e, acc, nv);
+              } else {
+                float v[W], xx[W];
+                get(q, sl, 1, x, o, nv, len4, v);
+                get(q, sl, 2, x, o, nv, len4, xx);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                  v[w] = dev::momentum(a.mu, v[w], dev::decay(acc[w], a.wd, xx[w]));
+                  xx[w] = dev::sgd(xx[w], a.lr, v[w]);
+                }
+                stm<W>(pt.bv[sl] + e, v, nv);
+                stm<W>(pt.bx[sl] + e, xx, nv);
+              }
+            }
+          } else {  // a group with remote members: reduce-scatter my contribution of slice j
+            float val[W];
+            get(q, s, 0, x, o, nv, len4, val);
+            if constexpr (!GRAD) {
+              float v[W], xx[W];
+              get(q, s, 1, x, o, nv, len4, v);
+              get(q, s, 2, x, o, nv, len4, xx);
+#pragma unroll
+              for (int w = 0; w < W; ++w) {
+                v[w] = dev::momentum(a.mu, v[w], dev::decay(val[w], a.wd, xx[w]));
+                val[w] = dev::sgd(xx[w], a.lr, v[w]);  // x_hat
+              }
+              stm<W>(pt.bv[s] + e, v, nv);
+            }
+            const int w = G[x.j];  // the slice's owner
+            if (local(w)) {
+              float *dst = xent(qx, s) + (o - x.plo);
+              SESGD_CHECK(o - x.plo + nv <= sub);
+#pragma unroll
+              for (int q2 = 0; q2 < W; ++q2)
+                if (q2 < nv) dst[q2] = val[q2];
+            } else {
+              push<W>(recv(w, a.my_pos[s]) + x.soff + e, val, nv);
+            }
           }
-          s_item(q, qx, x, pt, s, kind, o, nv, e, len4);
         }
-        if (pend >= 0) s_item(q, qx, x, pt, pend, 0, o, nv, e, len4);
       }
       __syncwarp();
       if ((t & 31) == 0) {
