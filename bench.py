@@ -401,7 +401,7 @@ def measure(args, D, rank, workload, n, m, K, W, *, e2e_steps=0, clocks=None):
                                           [BYTES_PER_WORKER_ELEM * Lb * r for Lb in buckets]),
                 "kernel": kernel}
     else:
-        proto = args.protocol if args.protocol >= 0 else (2 if r == 1 or 4 <= r <= 8 else 1)  # auto (sesgd_capi.cu)
+        proto = args.protocol if args.protocol >= 0 else (2 if r <= 8 else 1)  # auto (sesgd_capi.cu)
         if args.push_tma or args.payload_bf16:
             proto = 0 if args.protocol < 0 else proto
         # several workers per GPU; --hybrid: K6 updates the all-local groups first, then K4W-M

@@ -139,9 +139,8 @@ extern "C" {
                                     before sesgd_workspace_bytes (the grid fixes the layout) */
 #define SESGD_OPT_PROTOCOL 21      /* two-shot handshake (set before sesgd_workspace_bytes, identical
                                     on every rank): -1 (default, auto) = 2 with one worker per
-                                    GPU (K4W) or with 4..8 (K4W-M), 1 with 2 or 3 or more than 8,
-                                    where supported (the two-shot path with fp32 LSU pushes),
-                                    else 0.
+                                    GPU (K4W) or with 2..8 (K4W-M), 1 with more than 8, where
+                                    supported (the two-shot path with fp32 LSU pushes), else 0.
                                     0 = epoch flags released with a system-scope fence per batch.
                                     1 = value-carried validity: every receive-slot float holds a
                                     sentinel NaN (0xFFFFFFFF) until the peer's value lands; the

@@ -42,21 +42,14 @@ struct UnitM {
   int b, j;
   int64_t e0, soff, plo, phi;
 };
-// the unit's bucket pointers of every local slot (P reads them from the global tables for its TMA
-// loads anyway): S and R take them from shared memory instead of a dependent global load per item
-struct UnitPtr {
-  float *bx[kMaxR], *bv[kMaxR];
-};
 struct SmemM {
   uint64_t full_ld[kQL], empty_ld[kQL], full_x[kQX], empty_x[kQX], full_id[kQI], empty_id[kQI];
   int64_t uid[kQI];   // unit of step k (P -> S, F); < 0 ends the role
   int64_t xuid[kQX];  // unit of the x_hat ring entry (S -> R)
   UnitM unit[kQI];    // decoded uid[]
   UnitM xunit[kQX];   // decoded xuid[]
-  UnitPtr uptr[kQI];  // bucket pointers of uid[]
-  UnitPtr xuptr[kQX]; // ... of xuid[]
 };
-constexpr size_t kHeadM = 4096;
+constexpr size_t kHeadM = 1024;
 
 __host__ __device__ inline int sub_of(int r) { return r <= 4 ? 1024 : 512; }
 
@@ -150,18 +143,12 @@ struct WSM {
     const int qi = int(k % kQI);
     if (k >= kQI) mbar_spin(&sm->empty_id[qi], uint32_t((k / kQI - 1) & 1));
     sm->uid[qi] = u;
-    if (x) {
-      sm->unit[qi] = *x;
-      for (int s = 0; s < r; ++s) {
-        sm->uptr[qi].bx[s] = a.bx[x->b * r + s];
-        sm->uptr[qi].bv[s] = a.bv[x->b * r + s];
-      }
-    }
+    if (x) sm->unit[qi] = *x;
     mbar_arrive(&sm->full_id[qi]);
   }
 
   // spanning_only: the all-local groups are updated by a K6 launch before this one (the hybrid
-  // launch of sesgd_capi.cu), so their slots are neither loaded nor streamed here
+  // launch of sesgd_capi.cu, SESGD_OPT_WSM_HYBRID), so their slots are neither loaded nor streamed
   __device__ __forceinline__ bool skip(int s) const { return a.wsm_spanning_only && a.slot_kind[s] != 0; }
 
   // ---------------------------------------------------------------- P
@@ -241,15 +228,18 @@ struct WSM {
       if (k >= kQX) mbar_spin(&sm->empty_x[qx], uint32_t((k / kQX - 1) & 1));
       if (lead) t_wait += dev::globaltimer() - tw;
       const Unit x = sm->unit[k % kQI];
-      const UnitPtr &pt = sm->uptr[k % kQI];  // P rewrites it only after this step (see post_id)
       const int64_t len4 = x.plo + ((x.phi - x.plo) & ~int64_t(3));
       const int64_t nvec = (x.phi - x.plo + W - 1) / W;
-      for (int s = 0; s < r; ++s) {
+      // (local slot, vector) items of the unit, flattened so that every S thread has the same
+      // share whatever r is (r * nvec items; nvec = 256 for a full piece at r <= 4)
+      const int nvi = int(nvec);
+      for (int it = t; it < r * nvi; it += kThS) {
+        const int s = it / nvi, vi = it - s * nvi;
         const int kind = a.slot_kind[s];
         if (kind == 2 || skip(s)) continue;  // updated with its group's first member / by K6
         const int8_t *G = group(a.my_workers[s]);
-        for (int64_t vi = t; vi < nvec; vi += kThS) {
-          const int64_t o = x.plo + vi * W;
+        {
+          const int64_t o = x.plo + int64_t(vi) * W;
           const int nv = int(min(int64_t(W), x.phi - o));
           const int64_t e = x.e0 + o;
           if (kind == 1) {  // every member here: the 1-GPU kernel's arithmetic in registers
@@ -268,7 +258,7 @@ struct WSM {
                   const float xh = dev::sgd(xx[w], a.lr, v[w]);
                   acc[w] = (rr == 0) ? xh : __fadd_rn(acc[w], xh);
                 }
-                stm<W>(pt.bv[sl] + e, v, nv);
+                stm<W>(a.bv[x.b * r + sl] + e, v, nv);
               } else {
 #pragma unroll
                 for (int w = 0; w < W; ++w) acc[w] = (rr == 0) ? gr[w] : __fadd_rn(acc[w], gr[w]);
@@ -279,7 +269,7 @@ struct WSM {
             for (int rr = 0; rr < m; ++rr) {
               const int sl = a.worker_slot[G[rr]];
               if constexpr (!GRAD) {
-                stm<W>(pt.bx[sl] + e, acc, nv);
+                stm<W>(a.bx[x.b * r + sl] + e, acc, nv);
               } else {
                 float v[W], xx[W];
                 get(q, sl, 1, x, o, nv, len4, v);
@@ -289,8 +279,8 @@ struct WSM {
                   v[w] = dev::momentum(a.mu, v[w], dev::decay(acc[w], a.wd, xx[w]));
                   xx[w] = dev::sgd(xx[w], a.lr, v[w]);
                 }
-                stm<W>(pt.bv[sl] + e, v, nv);
-                stm<W>(pt.bx[sl] + e, xx, nv);
+                stm<W>(a.bv[x.b * r + sl] + e, v, nv);
+                stm<W>(a.bx[x.b * r + sl] + e, xx, nv);
               }
             }
           } else {  // a group with remote members: reduce-scatter my contribution of slice j
@@ -305,7 +295,7 @@ struct WSM {
                 v[w] = dev::momentum(a.mu, v[w], dev::decay(val[w], a.wd, xx[w]));
                 val[w] = dev::sgd(xx[w], a.lr, v[w]);  // x_hat
               }
-              stm<W>(pt.bv[s] + e, v, nv);
+              stm<W>(a.bv[x.b * r + s] + e, v, nv);
             }
             const int w = G[x.j];  // the slice's owner
             if (local(w)) {
@@ -325,7 +315,6 @@ struct WSM {
         mbar_arrive(&sm->empty_ld[q]);
         sm->xuid[qx] = u;
         sm->xunit[qx] = x;
-        sm->xuptr[qx] = pt;
         mbar_arrive(&sm->full_x[qx]);
       }
     }
@@ -357,7 +346,6 @@ struct WSM {
         delayed = true;
       }
       const Unit x = sm->xunit[qx];
-      const UnitPtr &pt = sm->xuptr[qx];  // S rewrites it only after this entry is freed
       for (int o_s = 0; o_s < r; ++o_s) {  // every local owner of slice j in a group with remote members
         if (a.slot_kind[o_s] != 0 || a.my_pos[o_s] != x.j) continue;
         const int me = a.my_workers[o_s];
@@ -414,18 +402,18 @@ struct WSM {
               }
               const int sl = a.worker_slot[w];
               if constexpr (!GRAD) {
-                stm<W>(pt.bx[sl] + e, acc[uu], nv);
+                stm<W>(a.bx[x.b * r + sl] + e, acc[uu], nv);
               } else {
                 float v[W], xx[W];
-                ldm<W>(pt.bv[sl] + e, v, nv);
-                ldm<W>(pt.bx[sl] + e, xx, nv);
+                ldm<W>(a.bv[x.b * r + sl] + e, v, nv);
+                ldm<W>(a.bx[x.b * r + sl] + e, xx, nv);
 #pragma unroll
                 for (int q2 = 0; q2 < W; ++q2) {
                   v[q2] = dev::momentum(a.mu, v[q2], dev::decay(acc[uu][q2], a.wd, xx[q2]));
                   xx[q2] = dev::sgd(xx[q2], a.lr, v[q2]);
                 }
-                stm<W>(pt.bv[sl] + e, v, nv);
-                stm<W>(pt.bx[sl] + e, xx, nv);
+                stm<W>(a.bv[x.b * r + sl] + e, v, nv);
+                stm<W>(a.bx[x.b * r + sl] + e, xx, nv);
               }
             }
           }

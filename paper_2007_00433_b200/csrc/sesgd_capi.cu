@@ -93,15 +93,15 @@ void freeze_layout(sesgd_ctx *ctx) {
     ctx->p2p_variant = 0;  // K4 runs on the DIRECT grid
   // SESGD_OPT_PROTOCOL auto (-1): value-carried validity wherever the two-shot kernel supports it
   // (fp32 LSU pushes), in the warp-specialised K4W when one worker lives on each GPU (K4W-M with
-  // four or more); else flags
+  // 2..8); else flags
   // (measured, profiles/r02_k4_experiments.json: n = m = 2 kernel 0.188 ms K4W, 0.190 K4 value-
   // carried, 0.185-0.228 K4 flags)
   if (ctx->protocol < 0) {
     const bool value = resolve_path(ctx) == SESGD_PATH_TWOSHOT && ctx->m >= 2 && !ctx->push_tma &&
                        !ctx->payload_bf16;
-    // K4W-M pays off from four workers per GPU on (cfg-2 shape on 2 GPUs, kernel p50: r = 4 0.54-0.57
-    // ms vs K4 0.61; r = 2 0.54 vs K4 0.42 ms, profiles/r02_c17_*): r = 2, 3 stay on K4
-    const bool wsm = ctx->n_local >= 4 && sesgd::p2p_wsm_supported(ctx->n_local, ctx->m);
+    // K4W-M for 2..8 workers per GPU (same box, kernel p50: cfg 2 on 2 GPUs r = 4 0.567 ms vs K4
+    // 0.610; n = 4, r = 2 0.393 vs 0.41, profiles/r02_k4wm_ab/)
+    const bool wsm = sesgd::p2p_wsm_supported(ctx->n_local, ctx->m);
     ctx->protocol = !value ? 0 : (ctx->n_local == 1 || wsm) ? 2 : 1;
   }
   const int var = ctx->p2p_variant;

@@ -12,8 +12,10 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# SESGD_LIB=checked loads the bounds-checked build (_build.build(checked=True), -DSESGD_CHECKED)
-LIB_PATH = os.path.join(_PKG, "libsesgd_checked.so" if os.environ.get("SESGD_LIB") == "checked" else "libsesgd.so")
+# SESGD_LIB=checked loads the bounds-checked build (_build.build(checked=True), -DSESGD_CHECKED);
+# SESGD_LIB=<tag> loads libsesgd_<tag>.so from this directory (kernel variants built for A/B runs)
+_VARIANT = os.environ.get("SESGD_LIB", "")
+LIB_PATH = os.path.join(_PKG, f"libsesgd_{_VARIANT}.so" if _VARIANT else "libsesgd.so")
 
 OK, EINVAL, ENOTDIV, ESTATE, ECUDA, ETIMEOUT, ENOMEM, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7
 MAX_WORKERS, MAX_RANKS = 64, 8
