@@ -26,7 +26,7 @@ using namespace wsx;
 
 // 25 warps: P (1), S (ws_s), R (2 groups) and F (2 groups) sharing the other 24 - ws_s equally.
 // S streams every local worker's data (r items per vector); R and F only touch the groups that
-// span GPUs, so S may take more than a third (SESGD_OPT_WS_SPLIT: ws_s = 8, 12 or 16)
+// span GPUs (SESGD_OPT_WS_SPLIT: ws_s = 8 -- the default, measured best -- 12 or 16)
 constexpr int kWarpsP = 1, kGroupsR = 2, kGroupsF = 2, kWarpsRest = 24;
 constexpr int kThreadsWSM = (kWarpsP + kWarpsRest) * 32;  // 800
 constexpr int kChunkWSM = 4096;  // K4's chunking: same slices

@@ -695,3 +695,16 @@ def test_device_iteration_resnet50_graph(tmp_path):
     x, v = _oracle(4, 2, sum(buckets), 30, 0, coords=coords)
     _compare(X, x)
     _compare(V, v)
+
+
+@pytest.mark.parametrize("gpus,n,m,grid,mode", [(2, 2, 2, 3, 0), (2, 8, 2, 0, 1), (4, 8, 4, 8, 0), (4, 4, 2, 0, 1)])
+def test_stress_device_iteration_graph(tmp_path, gpus, n, m, grid, mode):
+    """500 replays of ONE captured iteration graph (device-resident t, groups and call history;
+    K4W / K4W-M, small grids so every CTA walks many chunks and both call parities recycle the
+    receive slots hundreds of times), bit-exact with the oracle"""
+    buckets = [3001, 17, 4099]
+    T = 500
+    X, V = _launch(tmp_path, gpus, n, m, T, buckets, mode, grid=grid, path=4, protocol=2, devit=2)
+    x, v = _oracle(n, m, sum(buckets), T, mode)
+    _compare(X, x)
+    _compare(V, v)
