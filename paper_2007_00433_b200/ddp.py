@@ -154,12 +154,25 @@ class SESGDDataParallel:
         torch.cuda.synchronize(self.engine.device)
 
     # ------------------------------------------------------------------ per step
+    def enable_graphs(self) -> None:
+        """Device-resident iterations (SESGD_OPT_DEVICE_ITER): from now on begin_step advances the
+        iteration ON THE DEVICE (sesgd_begin_iter_device, the groups evaluated on the GPU), so a
+        whole training step -- begin_step, forward, backward with the hook-launched bucket syncs on
+        the side stream, finish_step -- can be captured once with torch.cuda.graph and replayed for
+        every iteration.  Continues from the current iteration; needs the warm-up steps (and, with
+        static_graph, the hook trimming of the first step) done eagerly first."""
+        self.engine.set_device_iter(True)
+
     def begin_step(self, t: Optional[int] = None) -> None:
-        """Start iteration t: zero the gradient buffers, set the schedule of t."""
+        """Start iteration t: zero the gradient buffers, set the schedule of t (device-resident
+        iterations: the next iteration, on the device; t is ignored)."""
         self.t = self.t if t is None else t
         for g in self.engine.g_flat:
             g.zero_()
-        self.engine.begin_iter(self.t)
+        if getattr(self.engine, "device_iter", False):
+            self.engine.begin_iter_device(C.ITER_NEXT, torch.cuda.current_stream(self.engine.device))
+        else:
+            self.engine.begin_iter(self.t)
         self.ready.reset(self._hooked)
         self.launched_in_backward = 0  # buckets whose sync was enqueued from a gradient hook
         self._order = []

@@ -156,3 +156,96 @@ def test_ddp_loopback_replicas(world, m, mode, static):
     for ddp in ddps:
         ddp.close()
     grp.close()
+
+
+@pytest.mark.parametrize("world,m,static", [(2, 2, 1), (4, 2, 0)])
+def test_ddp_loopback_captured_training_step(world, m, static):
+    """A whole SESGDDataParallel training step -- zero grads, device-side begin_iter, forward,
+    backward with the bucket syncs launched from gradient hooks on the side stream, finish -- captured
+    ONCE per replica with torch.cuda.graph (device-resident iterations) and replayed for 4 steps on
+    loopback virtual ranks: every replayed step equals the oracle's step on the gradients it produced"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.nn.functional as F
+
+    import oracle
+    from paper_2007_00433_b200.ddp import SESGDDataParallel
+    from paper_2007_00433_b200.engine import LoopbackGroup
+    from paper_2007_00433_b200.workloads import assign_buckets
+    LR, MU = 0.05, 0.9
+    dev = torch.device("cuda", 0)
+
+    def mlp(seed):
+        torch.manual_seed(seed)
+        return torch.nn.Sequential(torch.nn.Linear(256, 512), torch.nn.ReLU(), torch.nn.Linear(512, 10)).to(dev)
+
+    warm = mlp(99)
+    F.cross_entropy(warm(torch.randn(64, 256, device=dev)), torch.randint(0, 10, (64,), device=dev)).backward()
+    torch.cuda.synchronize()
+    models = [mlp(r) for r in range(world)]
+    sizes = [p.numel() for p in models[0].parameters()]
+    caps = dict(first_bucket_bytes=16 << 10, bucket_bytes=256 << 10)
+    bsizes = [sum(sizes[i] for i in b) for b in assign_buckets(sizes, caps["first_bucket_bytes"], caps["bucket_bytes"])]
+    grp = LoopbackGroup(world, world, m, bsizes, seed=42, timeout_ms=20000)
+    ddps = [SESGDDataParallel(models[r], world, m, lr=LR, momentum=MU, rank=r, world=world, engine=grp[r],
+                              static_graph=bool(static), **caps) for r in range(world)]
+    with torch.no_grad():
+        for r in range(1, world):
+            grp[r].x_flat[0].copy_(grp[0].x_flat[0])
+    inp = [torch.zeros(64, 256, device=dev) for _ in range(world)]
+    lab = [torch.zeros(64, dtype=torch.long, device=dev) for _ in range(world)]
+
+    def feed(t):
+        for r in range(world):
+            gen = torch.Generator(device=dev).manual_seed(1000 * t + r)
+            inp[r].copy_(torch.randn(64, 256, device=dev, generator=gen))
+            lab[r].copy_(torch.randint(0, 10, (64,), device=dev, generator=gen))
+
+    def check(t, X0, V0):
+        torch.cuda.synchronize()
+        grp.poll()
+        G = np.stack([e.g_flat[0].cpu().numpy() for e in grp])
+        X1 = np.stack([e.x_flat[0].cpu().numpy() for e in grp])
+        V1 = np.stack([e.v_flat[0].cpu().numpy() for e in grp])
+        assert np.abs(G).max() > 0
+        _, canon, _ = oracle.groups(42, t, world, m)
+        x, v = X0.copy(), V0.copy()
+        oracle.step(world, m, canon, x, v, G, LR, MU, 0)
+        assert np.array_equal(x.view(np.uint32), X1.view(np.uint32)), t
+        assert np.array_equal(v.view(np.uint32), V1.view(np.uint32)), t
+
+    def state():
+        torch.cuda.synchronize()
+        return (np.stack([e.x_flat[0].cpu().numpy() for e in grp]), np.stack([e.v_flat[0].cpu().numpy() for e in grp]))
+
+    T_eager = 2
+    for t in range(T_eager):  # eager warm-up steps (host iterations; static_graph trims the hooks)
+        feed(t)
+        X0, V0 = state()
+        for r in range(world):
+            ddps[r].begin_step(t)
+            F.cross_entropy(models[r](inp[r]), lab[r]).backward()
+        for d in ddps:
+            d.finish_step()
+        check(t, X0, V0)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    graphs = []
+    for r in range(world):
+        ddps[r].enable_graphs()
+        g = torch.cuda.CUDAGraph()
+        streams[r].wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=streams[r]):
+            ddps[r].begin_step()
+            F.cross_entropy(models[r](inp[r]), lab[r]).backward()
+            ddps[r].finish_step()
+        graphs.append(g)
+    for t in range(T_eager, T_eager + 4):
+        feed(t)
+        X0, V0 = state()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                graphs[r].replay()
+        check(t, X0, V0)
+    for d in ddps:
+        d.close()
+    grp.close()
