@@ -13,6 +13,9 @@ over ranks:
   compute_accum  the floor with gradients accumulated in place into one flat buffer (what every
             bucketed data-parallel wrapper, torch DDP's gradient_as_bucket_view included, pays)
   compute_hooks  the floor plus a no-op Python hook per parameter
+  sesgd_graph   sesgd, but after the eager warm-up the whole step (zero grads, device-side
+            begin_iter, forward, backward with the hook-launched bucket syncs on the side stream,
+            finish) is captured once with torch.cuda.graph (SESGD_OPT_DEVICE_ITER) and replayed
 The sync hidden fraction is (sesgd_seq - sesgd) / (sesgd_seq - floor), floor = compute_accum when
 timed, else compute.
 
@@ -50,9 +53,9 @@ def time_arm(arm, a, rank, world, dev, images, labels):
     model.train()
     ddp = opt = None
     net = model
-    if arm in ("sesgd", "sesgd_seq"):
+    if arm in ("sesgd", "sesgd_seq", "sesgd_graph"):
         ddp = SESGDDataParallel(model, world, min(a.gsize, world), lr=LR, momentum=MU, rank=rank,
-                                world=world, overlap=(arm == "sesgd"), static_graph=bool(a.static),
+                                world=world, overlap=(arm != "sesgd_seq"), static_graph=bool(a.static),
                                 engine_options={} if not a.grid else {C.OPT_GRID: a.grid})
     elif arm == "compute_hooks":  # the floor plus one no-op Python hook per parameter
         hooks = [p.register_post_accumulate_grad_hook(lambda p: None) for p in model.parameters()]
@@ -91,6 +94,27 @@ def time_arm(arm, a, rank, world, dev, images, labels):
 
     for t in range(a.warmup):
         step(t)
+    if arm == "sesgd_graph":  # capture one step, replay it every step
+        torch.cuda.synchronize()
+        ddp.enable_graphs()
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        cap_amp = torch.autocast("cuda", dtype=torch.bfloat16, enabled=a.amp == "bf16", cache_enabled=False)
+        with torch.cuda.graph(graph, stream=cap):
+            ddp.begin_step()
+            with cap_amp:
+                static_loss = F.cross_entropy(net(images), labels)
+            static_loss.backward()
+            ddp.finish_step()
+        torch.cuda.current_stream().wait_stream(cap)
+
+        def step(t):  # noqa: F811 -- the replayed step
+            graph.replay()
+            return static_loss
+
+        for t in range(2):
+            step(t)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
