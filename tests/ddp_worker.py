@@ -36,6 +36,7 @@ def main():
     p.add_argument("--overlap", type=int, default=1)
     p.add_argument("--mode", type=int, default=0)
     p.add_argument("--static", type=int, default=0)
+    p.add_argument("--graph", type=int, default=0)  # steps >= 2 replay one captured step (enable_graphs)
     p.add_argument("--out", required=True)
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -56,17 +57,39 @@ def main():
     X_init = gather(eng.x_flat[0])  # identical x_0 on every worker (Alg.1 line 1)
     assert np.array_equal(X_init, np.broadcast_to(X_init[:1], X_init.shape)), "x_0 differs across ranks"
     log = []
+    inp = torch.zeros(64, 256, device=dev)
+    lab = torch.zeros(64, dtype=torch.long, device=dev)
+    graph = None
     for t in range(a.iters):
         torch.cuda.synchronize()
         x_prev, v_prev = eng.x_flat[0].clone(), eng.v_flat[0].clone()
         gen = torch.Generator(device=dev).manual_seed(1000 * t + rank)
-        inp = torch.randn(64, 256, device=dev, generator=gen)
-        lab = torch.randint(0, 10, (64,), device=dev, generator=gen)
-        ddp.begin_step(t)
-        loss = F.cross_entropy(model(inp), lab)
-        loss.backward()
-        in_bwd = ddp.launched_in_backward
-        ddp.finish_step()
+        inp.copy_(torch.randn(64, 256, device=dev, generator=gen))
+        lab.copy_(torch.randint(0, 10, (64,), device=dev, generator=gen))
+        if a.graph and t == 2:  # after two eager steps: capture the whole step once (enable_graphs)
+            # drop the last eager loss: its autograd graph keeps AccumulateGrad nodes bound to the
+            # legacy stream, which the captured backward would then have to join (illegal in capture)
+            loss = None
+            ddp.enable_graphs()
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(graph, stream=cap):
+                ddp.begin_step()
+                static_loss = F.cross_entropy(model(inp), lab)
+                static_loss.backward()
+                ddp.finish_step()
+            torch.cuda.current_stream().wait_stream(cap)
+        if graph is not None:
+            graph.replay()
+            loss = static_loss
+            in_bwd = len(ddp.bucket_params)
+        else:
+            ddp.begin_step(t)
+            loss = F.cross_entropy(model(inp), lab)
+            loss.backward()
+            in_bwd = ddp.launched_in_backward
+            ddp.finish_step()
         torch.cuda.synchronize()
         eng.poll()
         X0, V0, G = gather(x_prev), gather(v_prev), gather(eng.g_flat[0])
@@ -78,6 +101,9 @@ def main():
             bad_x = int(np.count_nonzero(x.view(np.uint32) != X1.view(np.uint32)))
             bad_v = int(np.count_nonzero(v.view(np.uint32) != V1.view(np.uint32)))
             log.append((t, float(loss), bad_x, bad_v, in_bwd, float(np.abs(G).max()), len(ddp._hooks)))
+    if graph is not None:  # release the captured graph before the engine and the process group go
+        torch.cuda.synchronize()
+        del graph, static_loss
     # model parameters are the engine's x: the module sees the synchronised values
     first = next(model.parameters())
     assert first.data_ptr() >= eng.x_flat[0].data_ptr()

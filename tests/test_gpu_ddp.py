@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _run(tmp_path, gpus, m, overlap=1, mode=0, iters=4, static=0):
+def _run(tmp_path, gpus, m, overlap=1, mode=0, iters=4, static=0, graph=0):
     if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     out = str(tmp_path / "log.npy")
@@ -31,7 +31,8 @@ def _run(tmp_path, gpus, m, overlap=1, mode=0, iters=4, static=0):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
                "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
                os.path.join(ROOT, "tests", "ddp_worker.py"), "--gsize", str(m), "--iters", str(iters),
-               "--overlap", str(overlap), "--mode", str(mode), "--static", str(static), "--out", out]
+               "--overlap", str(overlap), "--mode", str(mode), "--static", str(static), "--graph", str(graph),
+               "--out", out]
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         if "EADDRINUSE" not in res.stderr:
             break
@@ -72,6 +73,14 @@ def test_ddp_two_gpus_static_graph(tmp_path):
     log = _run(tmp_path, 2, 2, static=1, iters=5)
     assert np.all(log[:, 4] == 3)
     assert np.all(log[:, 6] == 3)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("gpus,static", [(2, 1), (4, 0)])
+def test_ddp_captured_training_step_multigpu(tmp_path, gpus, static):
+    """one process per GPU: from step 2 on, the whole training step is ONE replayed CUDA graph
+    (SESGDDataParallel.enable_graphs), every step still equal to the oracle's replay"""
+    _run(tmp_path, gpus, 2, static=static, iters=6, graph=1)
 
 
 def test_ddp_one_gpu_static_graph(tmp_path):
