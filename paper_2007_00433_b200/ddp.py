@@ -160,7 +160,9 @@ class SESGDDataParallel:
         whole training step -- begin_step, forward, backward with the hook-launched bucket syncs on
         the side stream, finish_step -- can be captured once with torch.cuda.graph and replayed for
         every iteration.  Continues from the current iteration; needs the warm-up steps (and, with
-        static_graph, the hook trimming of the first step) done eagerly first."""
+        static_graph, the hook trimming of the first step) done eagerly first, and no tensor (e.g.
+        the last eager loss) may still hold an eager step's autograd graph when the capture starts
+        -- its AccumulateGrad nodes are bound to the eager stream, which a capture cannot join."""
         self.engine.set_device_iter(True)
 
     def begin_step(self, t: Optional[int] = None) -> None:
