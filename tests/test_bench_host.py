@@ -107,3 +107,14 @@ def test_all_core_oracle_leg_runs_the_plain_oracle_on_every_core():
     assert info["nproc"] >= 1 and info["cpu_count"] >= info["nproc"]
     r = bench.cpu_oracle_all_cores(4, 2, "param", 1 << 20, "config1", rate_1core=2e6, budget_s=0.2)
     assert r["cores"] == info["nproc"] and r["value"] > 0 and r["kind"] == "oracle"
+
+
+def test_local_groups_on_rank_counts_groups_whose_members_all_live_there():
+    """the extra K6 launches of the hybrid K4W-M launch are counted from this host helper:
+    worker w lives on rank w // r; a group counts for a rank only if every member lives there"""
+    perm = [0, 1, 2, 5, 3, 4, 6, 7]  # canonical groups of m = 2: {0,1} {2,5} {3,4} {6,7}
+    assert bench.local_groups_on_rank(perm, 2, 4, 0) == 1  # {0,1}; {2,5} spans ranks 0 and 1
+    assert bench.local_groups_on_rank(perm, 2, 4, 1) == 1  # {6,7}
+    assert bench.local_groups_on_rank(perm, 2, 2, 1) == 0  # r = 2: rank 1 holds {2, 3}, both partners elsewhere
+    assert bench.local_groups_on_rank(perm, 4, 4, 0) == 0  # {0,1,2,5} spans ranks 0 and 1
+    assert bench.local_groups_on_rank(list(range(8)), 4, 4, 1) == 1
